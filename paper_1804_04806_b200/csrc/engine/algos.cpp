@@ -1,0 +1,35 @@
+#include "algos.h"
+
+#include "../kernels/igemm.h"
+
+namespace ucudnn {
+
+namespace {
+
+bool igemm_supports(int, const ConvShape&) { return true; }
+std::int64_t no_workspace(int, const ConvShape&) { return 0; }
+
+cudaError_t igemm_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void*, float alpha,
+                      float beta, cudaStream_t st) {
+  switch (op) {
+    case 0: return igemm_forward(s, a, b, out, alpha, beta, st);
+    case 1: return igemm_backward_data(s, a, b, out, alpha, beta, st);
+    case 2: return igemm_backward_filter(s, a, b, out, alpha, beta, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
+
+}  // namespace
+
+const AlgoImpl* find_algo(int id) {
+  switch (id) {
+    case 0: return &kImplicitGemm;
+    default: return nullptr;
+  }
+}
+
+int algo_count() { return 5; }
+
+}  // namespace ucudnn

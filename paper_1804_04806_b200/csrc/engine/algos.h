@@ -1,0 +1,32 @@
+// Registry of the concrete B200 convolution algorithms. Each algorithm has a
+// different workspace footprint; the cost table holds one (time, workspace,
+// feasible) row per (kernel, algorithm, micro-batch) and the planner picks
+// among them.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../kernels/conv_common.h"
+
+namespace ucudnn {
+
+struct AlgoImpl {
+  int id;
+  const char* name;
+  // Whether the algorithm implements `op` for this shape (any micro-batch).
+  bool (*supports)(int op, const ConvShape& s);
+  // Workspace bytes at micro-batch s.N.
+  std::int64_t (*workspace)(int op, const ConvShape& s);
+  // op 0: a = x, b = w, out = y; op 1: a = dy, b = w, out = dx;
+  // op 2: a = x, b = dy, out = dw.
+  cudaError_t (*run)(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
+                     float alpha, float beta, cudaStream_t stream);
+};
+
+// nullptr for ids that are reserved / not built.
+const AlgoImpl* find_algo(int id);
+int algo_count();  // ids are 0 .. algo_count()-1
+
+}  // namespace ucudnn

@@ -1,0 +1,25 @@
+// Device algorithm entry points (all launch on `stream`, no host sync).
+// Pointers address the micro-batch slice; alpha/beta follow cuDNN:
+// out = alpha * conv + beta * out (beta == 0 never reads out).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_common.h"
+
+namespace ucudnn {
+
+// IMPLICIT_GEMM (0 workspace).
+cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
+                          cudaStream_t stream);
+cudaError_t igemm_backward_data(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha,
+                                float beta, cudaStream_t stream);
+// dw = beta * dw + alpha * sum (split-K with fp32 atomics)
+cudaError_t igemm_backward_filter(const ConvShape& s, const float* x, const float* dy, float* dw, float alpha,
+                                  float beta, cudaStream_t stream);
+
+cudaError_t scale_tensor(float* p, std::int64_t n, float beta, cudaStream_t stream);
+
+}  // namespace ucudnn

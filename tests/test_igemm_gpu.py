@@ -1,0 +1,71 @@
+"""IMPLICIT_GEMM (tcgen05, 0 workspace) vs the fp64 oracle, through the C ABI.
+
+Integer data in [-3, 3] is exact in TF32 and every partial sum here stays
+below 2^24, so the GPU result must equal the oracle bit-for-bit. Gaussian
+data checks the stated TF32 tolerance: normwise relative error <= 3e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1804_04806_b200 import ConvShape, Handle
+from tests.oracle_py import conv_ref, inputs_for, out_shape
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    ConvShape(2, 3, 11, 11, 16, 3, 3, 1, 1, 1, 1),
+    ConvShape(3, 8, 9, 7, 24, 3, 3, 0, 0, 1, 1),
+    ConvShape(2, 5, 13, 13, 7, 5, 5, 2, 2, 1, 1),
+    ConvShape(2, 3, 31, 31, 16, 11, 11, 2, 2, 4, 4),      # AlexNet conv1 geometry
+    ConvShape(2, 16, 14, 14, 32, 1, 1, 0, 0, 2, 2),       # ResNet 1x1 s2 shortcut
+    ConvShape(2, 16, 15, 15, 32, 3, 3, 1, 1, 2, 2),       # ResNet 3x3 s2
+    ConvShape(1, 3, 30, 30, 64, 7, 7, 3, 3, 2, 2),        # ResNet conv1 geometry
+    ConvShape(4, 64, 27, 27, 192, 5, 5, 2, 2, 1, 1),      # AlexNet conv2
+    ConvShape(2, 192, 13, 13, 384, 3, 3, 1, 1, 1, 1),     # AlexNet conv3 (N tiles of 192)
+    ConvShape(2, 40, 6, 6, 300, 3, 3, 1, 1, 1, 1),        # ragged tiles
+]
+
+
+def _run(h, op, s, a, b, dev, alpha=1.0, beta=0.0, init=None):
+    ta, tb = torch.from_numpy(a).float().to(dev), torch.from_numpy(b).float().to(dev)
+    out = torch.from_numpy(init).float().to(dev) if init is not None else \
+        torch.full(out_shape(op, s), float("nan"), device=dev)
+    h.run(op, s, ta, tb, out, 0, None, alpha, beta)
+    torch.cuda.synchronize()
+    return out.cpu().double().numpy()
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=lambda s: f"{s.N}x{s.C}x{s.H}x{s.W}-k{s.K}r{s.R}s{s.sh}")
+@pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
+def test_integer_bit_exact(cuda, op, s):
+    rng = np.random.default_rng(1804 + op)
+    a, b = inputs_for(op, s, rng, integer=True)
+    h = Handle()
+    got = _run(h, op, s, a, b, cuda)
+    ref = conv_ref(op, s, a, b)
+    assert np.array_equal(got, ref), f"max abs diff {np.abs(got - ref).max()}"
+
+
+@pytest.mark.parametrize("s", SHAPES[:8], ids=lambda s: f"{s.N}x{s.C}x{s.H}-k{s.K}r{s.R}s{s.sh}")
+@pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
+def test_gaussian_tf32_tolerance(cuda, op, s):
+    rng = np.random.default_rng(7 + op)
+    a, b = inputs_for(op, s, rng, integer=False)
+    h = Handle()
+    got = _run(h, op, s, a, b, cuda)
+    ref = conv_ref(op, s, a, b)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 3e-3, err
+
+
+@pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
+def test_alpha_beta(cuda, op):
+    s = ConvShape(3, 6, 10, 10, 20, 3, 3, 1, 1, 1, 1)
+    rng = np.random.default_rng(3)
+    a, b = inputs_for(op, s, rng, integer=True)
+    init = np.random.default_rng(4).integers(-3, 4, size=out_shape(op, s)).astype(np.float64)
+    h = Handle()
+    got = _run(h, op, s, a, b, cuda, alpha=2.0, beta=-1.0, init=init)
+    ref = 2.0 * conv_ref(op, s, a, b) - init
+    assert np.array_equal(got, ref)

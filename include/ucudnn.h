@@ -68,7 +68,8 @@ typedef enum {
   UCUDNN_ALGO_FFT = 2,               /* FFT-tiled (reserved: infeasible rows today)   */
   UCUDNN_ALGO_GEMM = 3,              /* explicit im2col + tcgen05 GEMM                */
   UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (reserved)                          */
-  UCUDNN_ALGO_COUNT = 5
+  UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* NHWC copy + TMA-im2col tcgen05 GEMM, ws ~ b  */
+  UCUDNN_ALGO_COUNT = 6
 } ucudnnAlgo_t;
 
 /* Returned by Get*Algorithm: a plan handle, >= UCUDNN_VIRTUAL_ALGO_BASE

@@ -1,6 +1,7 @@
 #include "algos.h"
 
 #include "../kernels/igemm.h"
+#include "../kernels/precomp.h"
 
 namespace ucudnn {
 
@@ -20,16 +21,18 @@ cudaError_t igemm_run(int op, const ConvShape& s, const float* a, const float* b
 }
 
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
+const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 
 }  // namespace
 
 const AlgoImpl* find_algo(int id) {
   switch (id) {
     case 0: return &kImplicitGemm;
+    case 5: return &kPrecomp;
     default: return nullptr;
   }
 }
 
-int algo_count() { return 5; }
+int algo_count() { return 6; }
 
 }  // namespace ucudnn

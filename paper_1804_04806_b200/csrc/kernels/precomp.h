@@ -1,0 +1,17 @@
+// UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM (TMA-fed implicit GEMM; see precomp.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_common.h"
+
+namespace ucudnn {
+
+bool precomp_supports(int op, const ConvShape& s);
+std::int64_t precomp_workspace(int op, const ConvShape& s);
+cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
+                        float alpha, float beta, cudaStream_t stream);
+
+}  // namespace ucudnn

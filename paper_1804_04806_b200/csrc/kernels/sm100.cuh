@@ -138,3 +138,44 @@ __device__ __forceinline__ void red_add(float* p, float v) {
 
 }  // namespace sm100
 }  // namespace ucudnn
+
+namespace ucudnn {
+namespace sm100 {
+
+// SWIZZLE_128B K-major smem descriptor: 8-row x 128 B atoms (1024 B apart).
+__device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr) {
+  std::uint64_t d = 0;
+  d |= std::uint64_t((saddr >> 4) & 0x3FFF);
+  d |= std::uint64_t(1) << 16;                 // LBO (unused for swizzled K-major)
+  d |= std::uint64_t(1024 >> 4) << 32;         // SBO
+  d |= std::uint64_t(1) << 46;                 // version
+  d |= std::uint64_t(2) << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// TMA im2col load of a 4-D NHWC tensor: `pixels x channels` box starting at
+// input coordinate (c, w, h, n) with filter-tap offsets (ow, oh).
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const void* tmap, std::uint64_t* bar, int c, int w, int h,
+                                              int n, unsigned short ow, unsigned short oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+
+// TMA tiled 2-D load: box at (x = inner coordinate, y).
+__device__ __forceinline__ void tma_2d(void* dst, const void* tmap, std::uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+}  // namespace sm100
+}  // namespace ucudnn

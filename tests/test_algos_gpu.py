@@ -1,14 +1,15 @@
-"""IMPLICIT_GEMM (tcgen05, 0 workspace) vs the fp64 oracle, through the C ABI.
+"""Every concrete algorithm vs the fp64 oracle, through the C ABI (undivided).
 
 Integer data in [-3, 3] is exact in TF32 and every partial sum here stays
-below 2^24, so the GPU result must equal the oracle bit-for-bit. Gaussian
-data checks the stated TF32 tolerance: normwise relative error <= 3e-3.
+below 2^24, so GEMM-class results must equal the oracle bit-for-bit.
+Gaussian data checks the stated TF32 tolerance: normwise relative error
+<= 3e-3 (TF32 keeps 10 mantissa bits; accumulation is fp32).
 """
 import numpy as np
 import pytest
 import torch
 
-from paper_1804_04806_b200 import ConvShape, Handle
+from paper_1804_04806_b200 import ConvShape, Handle, algorithm_workspace
 from tests.oracle_py import conv_ref, inputs_for, out_shape
 
 pytestmark = pytest.mark.gpu
@@ -24,48 +25,58 @@ SHAPES = [
     ConvShape(4, 64, 27, 27, 192, 5, 5, 2, 2, 1, 1),      # AlexNet conv2
     ConvShape(2, 192, 13, 13, 384, 3, 3, 1, 1, 1, 1),     # AlexNet conv3 (N tiles of 192)
     ConvShape(2, 40, 6, 6, 300, 3, 3, 1, 1, 1, 1),        # ragged tiles
+    ConvShape(3, 64, 7, 7, 64, 3, 3, 1, 1, 1, 1),         # ResNet l4-like spatial size
 ]
+ALGOS = [0, 5]
 
 
-def _run(h, op, s, a, b, dev, alpha=1.0, beta=0.0, init=None):
+def _sid(s):
+    return f"{s.N}x{s.C}x{s.H}x{s.W}-k{s.K}r{s.R}p{s.ph}s{s.sh}"
+
+
+def run_algo(h, op, s, a, b, dev, algo, alpha=1.0, beta=0.0, init=None):
+    ws_bytes, ok = algorithm_workspace(op, s, algo, s.N)
+    if not ok:
+        pytest.skip(f"algorithm {algo} does not implement op {op} for {s}")
     ta, tb = torch.from_numpy(a).float().to(dev), torch.from_numpy(b).float().to(dev)
     out = torch.from_numpy(init).float().to(dev) if init is not None else \
         torch.full(out_shape(op, s), float("nan"), device=dev)
-    h.run(op, s, ta, tb, out, 0, None, alpha, beta)
+    ws = torch.empty(max(ws_bytes, 4) // 4 + 1, device=dev)
+    h.run(op, s, ta, tb, out, algo, ws, alpha, beta)
     torch.cuda.synchronize()
     return out.cpu().double().numpy()
 
 
-@pytest.mark.parametrize("s", SHAPES, ids=lambda s: f"{s.N}x{s.C}x{s.H}x{s.W}-k{s.K}r{s.R}s{s.sh}")
+@pytest.mark.parametrize("s", SHAPES, ids=_sid)
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
-def test_integer_bit_exact(cuda, op, s):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_integer_bit_exact(cuda, algo, op, s):
     rng = np.random.default_rng(1804 + op)
     a, b = inputs_for(op, s, rng, integer=True)
-    h = Handle()
-    got = _run(h, op, s, a, b, cuda)
+    got = run_algo(Handle(), op, s, a, b, cuda, algo)
     ref = conv_ref(op, s, a, b)
     assert np.array_equal(got, ref), f"max abs diff {np.abs(got - ref).max()}"
 
 
-@pytest.mark.parametrize("s", SHAPES[:8], ids=lambda s: f"{s.N}x{s.C}x{s.H}-k{s.K}r{s.R}s{s.sh}")
+@pytest.mark.parametrize("s", SHAPES[:9], ids=_sid)
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
-def test_gaussian_tf32_tolerance(cuda, op, s):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_gaussian_tf32_tolerance(cuda, algo, op, s):
     rng = np.random.default_rng(7 + op)
     a, b = inputs_for(op, s, rng, integer=False)
-    h = Handle()
-    got = _run(h, op, s, a, b, cuda)
+    got = run_algo(Handle(), op, s, a, b, cuda, algo)
     ref = conv_ref(op, s, a, b)
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert err <= 3e-3, err
 
 
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
-def test_alpha_beta(cuda, op):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_alpha_beta(cuda, algo, op):
     s = ConvShape(3, 6, 10, 10, 20, 3, 3, 1, 1, 1, 1)
     rng = np.random.default_rng(3)
     a, b = inputs_for(op, s, rng, integer=True)
     init = np.random.default_rng(4).integers(-3, 4, size=out_shape(op, s)).astype(np.float64)
-    h = Handle()
-    got = _run(h, op, s, a, b, cuda, alpha=2.0, beta=-1.0, init=init)
+    got = run_algo(Handle(), op, s, a, b, cuda, algo, alpha=2.0, beta=-1.0, init=init)
     ref = 2.0 * conv_ref(op, s, a, b) - init
     assert np.array_equal(got, ref)

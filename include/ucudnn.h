@@ -229,6 +229,11 @@ ucudnnStatus_t ucudnnPlanKernels(const char* network_name, const int64_t* kernel
                                  unsigned jobs, char* out, size_t* len);
 /* FNV-1a canonical hash of a kernel (domain.hpp:159-180). */
 uint64_t ucudnnKernelHash(const int64_t* kernel12);
+/* Cost-table seam utilities: parse an exact time ("27.6", "3/4") and render
+ * it canonically (rational.hpp:161-230); parse a cost-table CSV and re-emit
+ * it sorted and canonical (cost_database.hpp:119-222). */
+ucudnnStatus_t ucudnnCanonicalTime(const char* text, char* out, size_t* len);
+ucudnnStatus_t ucudnnCanonicalCostTable(const char* csv_text, char* out, size_t* len);
 
 #ifdef __cplusplus
 }

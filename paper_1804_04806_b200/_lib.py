@@ -66,6 +66,8 @@ PROTOTYPES = {
     "ucudnnPlanKernels": (C.c_int, [C.c_char_p, i64p, C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_int,
                                     C.c_int, i64, C.c_uint, C.c_char_p, C.POINTER(C.c_size_t)]),
     "ucudnnKernelHash": (C.c_uint64, [i64p]),
+    "ucudnnCanonicalTime": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_size_t)]),
+    "ucudnnCanonicalCostTable": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_size_t)]),
 }
 
 STATUS = {0: "SUCCESS", 1: "NOT_INITIALIZED", 2: "ALLOC_FAILED", 3: "BAD_PARAM", 4: "INTERNAL_ERROR",

@@ -84,6 +84,16 @@ def kernel_hash(op: int, s: ConvShape) -> int:
     return int(lib().ucudnnKernelHash(arr))
 
 
+def canonical_time(text: str) -> str:
+    """Exact time parse + canonical render (the cost-table time_us column)."""
+    return call_string(lib().ucudnnCanonicalTime, text.encode())
+
+
+def canonical_cost_table(csv_text: str) -> str:
+    """Parse a cost-table CSV and re-emit it sorted / canonical."""
+    return call_string(lib().ucudnnCanonicalCostTable, csv_text.encode())
+
+
 def algorithm_workspace(op: int, s: ConvShape, algo: int, micro_batch: int):
     ws, ok = C.c_int64(), C.c_int()
     check(lib().ucudnnAlgorithmWorkspace(op, s.as11(), algo, micro_batch, C.byref(ws), C.byref(ok)))

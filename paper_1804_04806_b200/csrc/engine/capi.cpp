@@ -833,6 +833,20 @@ ucudnnStatus_t ucudnnPlanKernels(const char* network_name, const int64_t* k12, c
   });
 }
 
+ucudnnStatus_t ucudnnCanonicalTime(const char* text, char* out, size_t* len) {
+  return guarded([&] {
+    require(text != nullptr, "null text");
+    return copy_out(Ratio::parse(text).str(), out, len);
+  });
+}
+
+ucudnnStatus_t ucudnnCanonicalCostTable(const char* csv_text, char* out, size_t* len) {
+  return guarded([&] {
+    require(csv_text != nullptr, "null text");
+    return copy_out(CostTable::from_csv_text(csv_text, "cost-table")->to_csv(), out, len);
+  });
+}
+
 uint64_t ucudnnKernelHash(const int64_t* r) {
   Kernel k;
   k.op = Op(r[0]); k.batch = r[1]; k.c = r[2]; k.h = r[3]; k.w = r[4]; k.k = r[5]; k.r = r[6]; k.s = r[7];

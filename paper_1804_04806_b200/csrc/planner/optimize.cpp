@@ -124,26 +124,59 @@ PlanSet plan_front(const CostSource& src, const Kernel& k, std::int64_t B, std::
   std::vector<std::vector<Micro>> mu(std::size_t(B) + 1);
   for (std::int64_t s : sizes) mu[s] = src.front(k, s, budget);
 
+  // The reference materialises every candidate plan, sorts them canonically,
+  // drops duplicates and then keeps the (time, ws) front with canonical ties
+  // (wd_optimizer.hpp:110-143). Equivalent and much cheaper: sort unmaterialised
+  // (time, ws, head, tail) tuples by (time, ws); a (time, ws) group that
+  // survives the front contributes its canonically least plan, so only those
+  // groups' plans are ever built. Duplicated plans have equal (time, ws), so
+  // the reference's unique() cannot change the result.
+  struct Cand {
+    Ratio time;
+    std::int64_t ws;
+    std::int32_t s, mi, ri;  // head = mu[s][mi], tail = C[b - s][ri] (ri < 0: none)
+  };
   std::vector<std::vector<Costed>> C(std::size_t(B) + 1);
+  std::vector<Cand> cand;
   for (std::int64_t b = 1; b <= B; ++b) {
-    std::vector<Costed> cand;
+    cand.clear();
     for (std::int64_t s : sizes) {
       if (s > b) break;
-      for (const Micro& m : mu[s]) {
+      const auto& heads = mu[s];
+      for (std::size_t mi = 0; mi < heads.size(); ++mi) {
+        const Micro& m = heads[mi];
         if (s == b) {
-          cand.push_back(Costed{m.time, m.ws, Plan::one(m)});
+          cand.push_back(Cand{m.time, m.ws, std::int32_t(s), std::int32_t(mi), -1});
           continue;
         }
-        Plan head = Plan::one(m);
-        for (const Costed& rest : C[b - s])
-          cand.push_back(Costed{m.time + rest.time, std::max(m.ws, rest.ws), Plan::join(head, rest.plan)});
+        const auto& tails = C[b - s];
+        for (std::size_t ri = 0; ri < tails.size(); ++ri)
+          cand.push_back(Cand{m.time + tails[ri].time, std::max(m.ws, tails[ri].ws), std::int32_t(s),
+                              std::int32_t(mi), std::int32_t(ri)});
       }
     }
-    std::sort(cand.begin(), cand.end(), tie_of);
-    cand.erase(std::unique(cand.begin(), cand.end(),
-                           [](const Costed& a, const Costed& b) { return a.plan == b.plan; }),
-               cand.end());
-    C[b] = pareto(std::move(cand), time_of, ws_of, tie_of);
+    std::sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) {
+      if (int c = Ratio::cmp(x.time, y.time)) return c < 0;
+      return x.ws < y.ws;
+    });
+    auto build = [&](const Cand& c) {
+      Plan head = Plan::one(mu[c.s][std::size_t(c.mi)]);
+      return c.ri < 0 ? head : Plan::join(head, C[b - c.s][std::size_t(c.ri)].plan);
+    };
+    std::vector<Costed>& out = C[b];
+    for (std::size_t i = 0; i < cand.size();) {
+      std::size_t j = i + 1;
+      while (j < cand.size() && cand[j].ws == cand[i].ws && cand[j].time == cand[i].time) ++j;
+      if (out.empty() || cand[i].ws < out.back().ws) {
+        Plan best = build(cand[i]);
+        for (std::size_t k = i + 1; k < j; ++k) {
+          Plan p = build(cand[k]);
+          if (plan_before(p, best)) best = std::move(p);
+        }
+        out.push_back(Costed{cand[i].time, cand[i].ws, std::move(best)});
+      }
+      i = j;
+    }
     if (C[b].size() > cap) {
       std::ostringstream os;
       os << "configuration front for kernel '" << k.name << "' exceeds cap (" << C[b].size() << " > " << cap

@@ -1,0 +1,116 @@
+"""Planner parity: the C++ planner in libucudnn.so vs the reference planner.
+
+Golden reports in tests/golden/ were produced by the unmodified reference
+(oracle/_ref/ref_plan over /root/reference/proj/include; see
+tests/golden/make_golden.py). Parity is byte equality of the machine report
+(reference report.hpp:148-197). Replays from a measurement CSV drop the
+`algorithm ` catalog lines exactly as the reference's own replay test does
+(tests/CMakeLists.txt:50-55), since a table-only provider names algorithms
+`alg<id>` (cost_provider.hpp:173-185).
+"""
+import json
+import os
+import subprocess
+
+import pytest
+
+from paper_1804_04806_b200 import UcudnnError, plan_network_file
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+GOLD = os.path.join(HERE, "golden")
+REF_PLAN = os.path.join(ROOT, "oracle", "_ref", "ref_plan")
+MiB = 1 << 20
+
+CASES = []
+for line in open(os.path.join(GOLD, "make_golden.py")):
+    line = line.strip()
+    if line.startswith('("') and line.endswith("),"):
+        CASES.append(eval(line[:-1].replace("MiB", str(MiB))))
+
+
+def strip_catalog(text):
+    return "".join(l for l in text.splitlines(True) if not l.startswith("algorithm "))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_builtin_model_report_identical(case):
+    name, net, batch, mode, policy, limit, _ = case
+    want = open(os.path.join(GOLD, "reports", name + ".txt")).read()
+    got = plan_network_file(os.path.join(ROOT, "configs", net + ".net"), batch, None, None, mode, policy, limit,
+                            jobs=4)
+    assert got == want
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[6]], ids=[c[0] for c in CASES if c[6]])
+def test_measurement_csv_replay_identical(case):
+    name, net, batch, mode, policy, limit, _ = case
+    want = open(os.path.join(GOLD, "reports", name + ".txt")).read()
+    got = plan_network_file(os.path.join(ROOT, "configs", net + ".net"), batch,
+                            os.path.join(GOLD, "csv", name + ".csv"), None, mode, policy, limit, jobs=2)
+    assert strip_catalog(got) == strip_catalog(want)
+
+
+def _random_records():
+    with open(os.path.join(GOLD, "random.jsonl")) as f:
+        return [json.loads(l) for l in f]
+
+
+def test_random_instances_model_and_replay(tmp_path):
+    """300 seeded instances (random models, 1-3 layers, WR and WD, all
+    policies, random budgets): model-backed reports identical, CSV replays
+    identical modulo the catalog, infeasibility and min-workspace identical."""
+    n_feasible = 0
+    for i, rec in enumerate(_random_records()):
+        net, model, csv = tmp_path / f"{i}.net", tmp_path / f"{i}.model", tmp_path / f"{i}.csv"
+        net.write_text(rec["net"])
+        model.write_text(rec["model"])
+        csv.write_text(rec["csv"])
+        mode, policy, limit = rec["args"].split()
+        for cost, strip in ((str(model), False), (str(csv), True)):
+            try:
+                got = plan_network_file(str(net), 0, cost, None, mode, policy, int(limit))
+            except UcudnnError as e:
+                assert e.status == 9, e
+                got = f"infeasible {e.min_total_workspace}\n"
+            want = rec["report"]
+            if strip and not want.startswith("infeasible"):
+                got, want = strip_catalog(got), strip_catalog(want)
+            assert got == want, f"instance {i} ({cost})"
+        n_feasible += not rec["report"].startswith("infeasible")
+    assert n_feasible >= 150
+
+
+def test_thread_count_does_not_change_reports():
+    net = os.path.join(ROOT, "configs", "alexnet.net")
+    a = plan_network_file(net, 256, None, None, "wd", "all", 120 * MiB, jobs=1)
+    b = plan_network_file(net, 256, None, None, "wd", "all", 120 * MiB, jobs=8)
+    assert a == b
+
+
+def test_cache_write_through_round_trip(tmp_path):
+    """A model-backed run with a cache CSV, then a table-only replay of that
+    CSV, reproduce the same plans (reference acceptance criterion 9)."""
+    net = os.path.join(ROOT, "configs", "resnet18.net")
+    cache = tmp_path / "cache.csv"
+    a = plan_network_file(net, 256, None, str(cache), "wr", "powerOfTwo", 64 * MiB)
+    b = plan_network_file(net, 256, str(cache), None, "wr", "powerOfTwo", 64 * MiB)
+    assert strip_catalog(a) == strip_catalog(b)
+    c = plan_network_file(net, 256, None, str(cache), "wr", "powerOfTwo", 64 * MiB)  # warm cache
+    assert a == c
+
+
+@pytest.mark.skipif(not os.path.exists(REF_PLAN), reason="oracle/_ref not built (needs /root/reference)")
+def test_live_reference_on_fresh_random_seeds(tmp_path):
+    """Beyond the committed fixtures: fresh seeds straight from the reference."""
+    subprocess.check_call([REF_PLAN, "random", str(tmp_path), "120", "777000"])
+    for i in range(120):
+        b = tmp_path / str(i)
+        mode, policy, limit = (b.with_suffix(".args")).read_text().split()
+        want = (b.with_suffix(".report")).read_text()
+        try:
+            got = plan_network_file(str(b.with_suffix(".net")), 0, str(b.with_suffix(".model")), None, mode, policy,
+                                    int(limit))
+        except UcudnnError as e:
+            got = f"infeasible {e.min_total_workspace}\n"
+        assert got == want, i

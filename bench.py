@@ -1,0 +1,307 @@
+#!/usr/bin/env python3
+"""Headline benchmark: AlexNet bs256 conv fwd+bwd ms/iter at a 64 MiB
+per-kernel workspace limit (WR), and the speedup over the undivided plan
+(BASELINE.json `metric`; configs C2 / C5 of SURVEY.md section 8).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N > 1): each rank micro-batches its own
+bs256 shard with the same plan and all-reduces every layer's filter gradient
+over NCCL (weak scaling). Timing: CUDA events on the compute stream over K
+steps after W warm-up steps, barrier + synchronize on both sides, max over
+ranks. The step's working set (AlexNet activations ~1.1 GB) exceeds the
+126 MB L2, so no explicit flush is needed between steps. Rank 0 prints one
+JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MiB = 1 << 20
+METRIC = "AlexNet bs256 conv fwd+bwd ms/iter @64 MiB WS; speedup vs undivided"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------ CPU reference arm
+def cpu_reference(net_path: str, sample_n: int, threads: int):
+    """The reference fp64 convolution (oracle/_ref/ref_conv.so, compiled from
+    /root/reference/proj/include/ubatch/reference_conv.hpp) on `sample_n`
+    samples of every AlexNet kernel, all host threads; returns (seconds for
+    the sample, extrapolated ms per bs256 iteration, kind)."""
+    import numpy as np
+    from paper_1804_04806_b200.network import parse_net
+    from tests import oracle_py
+    _, layers = parse_net(net_path, 256)
+    rng = np.random.default_rng(0)
+    use_ref = oracle_py.ref_available()
+    total = 0.0
+    for L in layers:
+        s = L.shape.with_batch(sample_n)
+        for op in range(3):
+            a, b = oracle_py.inputs_for(op, s, rng, integer=False)
+            t0 = time.perf_counter()
+            if use_ref:
+                oracle_py.ref_conv_threads(op, s, a, b, threads)
+            else:
+                oracle_py.oracle().oracle_set_threads(threads)
+                oracle_py.conv_ref(op, s, a, b)
+            total += time.perf_counter() - t0
+    return total, total * 1e3 * 256.0 / sample_n, ("reference" if use_ref else "port")
+
+
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    net = os.path.join(ROOT, "configs", "alexnet.net")
+    sample_n = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_reference(net, sample_n, threads)
+    vals = []
+    for _ in range(args.steps):
+        _, ms, kind = cpu_reference(net, sample_n, threads)
+        vals.append(ms)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/iter", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "AlexNet conv1-5 F+BD+BF, batch 256 (CPU: extrapolated from a "
+                                   f"{sample_n}-sample slice per step)", "net": "alexnet", "global_batch": 256},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms/iter", "cores": threads, "kind": kind,
+                             "sample": f"{sample_n} of 256 samples of all 15 kernels per step, x{256 // sample_n}"},
+            "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows if len(r) >= 9 for j in range(4) if r[5 + j].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ GPU arm
+def timed(fn, steps, warmup, dev, dist_on):
+    import torch
+    for _ in range(warmup):
+        fn()
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    if dist_on:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+        ms = float(t.item())
+    return ms
+
+
+def tf32_peak(dev):
+    """cuBLAS TF32 GEMM (8192^3, best of 10) -- the tensor-pipe roofline
+    denominator for TF32 kernels (MEASURED_PEAKS.json carries bf16 only)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device=dev)
+    b = torch.randn(8192, 8192, device=dev)
+    best = 1e9
+    for i in range(13):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            best = min(best, e0.elapsed_time(e1))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--net", default="alexnet")
+    ap.add_argument("--policy", default="powerOfTwo")
+    ap.add_argument("--limit-mib", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=0, help="samples per step (0: one per host core, <= 64)")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cores = os.cpu_count() or 1
+    args.ref_sample = args.ref_sample or min(64, cores)
+    args.cpu_sample = args.cpu_sample or min(64, cores)
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    from paper_1804_04806_b200 import Handle, OP_NAMES
+    from paper_1804_04806_b200._lib import lib
+    from paper_1804_04806_b200.network import ConvStack
+
+    rank, world, local = env_rank()
+    dist_on = world > 1
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if dist_on:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    net_path = os.path.join(ROOT, "configs", args.net + ".net")
+    limit = args.limit_mib * MiB
+    stack = ConvStack(net_path, 256, dev)
+    db = args.db or os.path.join(tempfile.gettempdir(), f"ucudnn_bench_{os.getpid()}_{rank}.csv")
+
+    # plan: benchmark every (algorithm x micro-batch) on the device, WR DP
+    t0 = time.perf_counter()
+    h = Handle(policy=args.policy, mode="wr", database=db, stream=stream.cuda_stream)
+    stack.plan(h, limit)
+    h.flush_database()
+    plan_s = time.perf_counter() - t0
+    plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": h.plan(a) for (i, op), a in stack.algos.items()}
+    base = Handle(policy="undivided", mode="wr", database=db, stream=stream.cuda_stream)
+    base_stack_algos = {}
+    for (i, op) in stack.kernels():
+        base_stack_algos[(i, op)] = base.get_algorithm(op, stack.layers[i].shape, limit)
+    base_plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": base.plan(a) for (i, op), a in base_stack_algos.items()}
+
+    comm = torch.distributed.group.WORLD if dist_on else None
+    comm_stream = torch.cuda.Stream(dev) if dist_on else None
+
+    def step_ours():
+        stack.step(h, comm, comm_stream)
+
+    ours_algos = stack.algos
+
+    def step_base():
+        stack.algos = base_stack_algos
+        stack.step(base, comm, comm_stream)
+        stack.algos = ours_algos
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    n0 = lib().ucudnnGetLaunchCount()
+    ms = timed(step_ours, args.steps, args.warmup, dev, dist_on)
+    launches = (lib().ucudnnGetLaunchCount() - n0)
+    clocks = sampler.stop() if sampler else None
+    launches_per_step = launches // (args.steps + args.warmup)
+    ms_base = timed(step_base, args.steps, args.warmup, dev, dist_on)
+
+    # per-kernel device times of our plan (dominant kernel -> roofline)
+    evs = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in stack.kernels()}
+    per = {k: [] for k in stack.kernels()}
+    for it in range(3 + 5):
+        stack.step(h, events=evs)
+        torch.cuda.synchronize(dev)
+        if it >= 3:
+            for k, (a, b) in evs.items():
+                per[k].append(a.elapsed_time(b))
+    per_ms = {k: statistics.median(v) for k, v in per.items()}
+    dom = max(per_ms, key=per_ms.get)
+    dom_flops = stack.layers[dom[0]].shape.flops()
+    dom_tflops = dom_flops / (per_ms[dom] * 1e-3) / 1e12
+    peak = tf32_peak(dev) if rank == 0 else None
+
+    # end-to-end through the public API with host buffers: H2D of the step's
+    # inputs (conv1 input images + top-layer output gradient), 15 planned
+    # convolutions, D2H of every filter gradient
+    x_host = stack.t[0]["x"].cpu().pin_memory()
+    dy_host = stack.t[-1]["dy"].cpu().pin_memory()
+    dw_host = [t["dw"].cpu().pin_memory() for t in stack.t]
+    h2d = x_host.numel() * 4 + dy_host.numel() * 4
+    d2h = sum(d.numel() * 4 for d in dw_host)
+
+    def step_e2e():
+        stack.t[0]["x"].copy_(x_host, non_blocking=True)
+        stack.t[-1]["dy"].copy_(dy_host, non_blocking=True)
+        stack.step(h, comm, comm_stream)
+        for d, t in zip(dw_host, stack.t):
+            d.copy_(t["dw"], non_blocking=True)
+
+    ms_e2e = timed(step_e2e, args.steps, args.warmup, dev, dist_on)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            sec, cpu_ms, kind = cpu_reference(net_path, args.cpu_sample, os.cpu_count() or 1)
+            cpu = {"value": round(cpu_ms, 1), "unit": "ms/iter", "cores": os.cpu_count(), "kind": kind,
+                   "sample": f"{args.cpu_sample} of 256 samples of each of the 15 kernels ({sec:.1f} s), "
+                             f"x{256 // args.cpu_sample}"}
+        total_flops = stack.flops()
+        line = {
+            "metric": METRIC, "value": round(ms, 4), "unit": "ms/iter", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "tf32", "data": "synthetic (N(0,1) activations, He-init filters)",
+            "speedup_vs_undivided": round(ms_base / ms, 4), "undivided_ms_per_step": round(ms_base, 4),
+            "images_per_s": round(256 * world / (ms * 1e-3), 1),
+            "tflops_effective": round(total_flops / (ms * 1e-3) / 1e12, 2),
+            "config": {"workload": "AlexNet conv1-5, Forward + BackwardData + BackwardFilter (15 kernels), "
+                                   "batch 256 per GPU", "net": args.net, "global_batch": 256 * world,
+                       "ws_limit_bytes": limit, "mode": "wr", "policy": args.policy,
+                       "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)"},
+            "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
+                         "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                         "frac": round(dom_tflops / peak, 3), "traffic": None,
+                         "peak_source": "cuBLAS TF32 8192^3 GEMM measured in this run"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(ms_e2e, 4), "unit": "ms/iter", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "plan_seconds": round(plan_s, 1),
+            "per_kernel_ms": {f"{stack.layers[i].name}/{OP_NAMES[op]}": round(v, 4) for (i, op), v in per_ms.items()},
+            "plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in plans.items()},
+            "undivided_plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in base_plans.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,8 @@ const char* ucudnnGetLastError(void);
  * domain.hpp:48-58). */
 int64_t ucudnnGetMinTotalWorkspace(void);
 size_t ucudnnGetVersion(void);
+/* Number of device kernels this library has launched in this process. */
+uint64_t ucudnnGetLaunchCount(void);
 
 /* ------------------------------------------------------------ handle ----- */
 /* Replaces cudnnCreate/cudnnDestroy/cudnnSetStream. The

@@ -26,6 +26,7 @@ PROTOTYPES = {
     "ucudnnGetLastError": (C.c_char_p, []),
     "ucudnnGetMinTotalWorkspace": (i64, []),
     "ucudnnGetVersion": (C.c_size_t, []),
+    "ucudnnGetLaunchCount": (C.c_uint64, []),
     "ucudnnCreate": (C.c_int, [C.POINTER(vp)]),
     "ucudnnDestroy": (C.c_int, [vp]),
     "ucudnnSetStream": (C.c_int, [vp, vp]),

@@ -1,9 +1,17 @@
 #include "algos.h"
 
+#include <atomic>
+
 #include "../kernels/igemm.h"
 #include "../kernels/precomp.h"
 
 namespace ucudnn {
+
+namespace {
+std::atomic<std::uint64_t> g_launches{0};
+}  // namespace
+void count_launch(int n) { g_launches.fetch_add(std::uint64_t(n), std::memory_order_relaxed); }
+std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 

@@ -396,6 +396,7 @@ const char* ucudnnGetErrorString(ucudnnStatus_t s) {
 const char* ucudnnGetLastError(void) { return g_last_error.c_str(); }
 int64_t ucudnnGetMinTotalWorkspace(void) { return g_min_ws; }
 size_t ucudnnGetVersion(void) { return UCUDNN_VERSION; }
+uint64_t ucudnnGetLaunchCount(void) { return launch_count(); }
 
 ucudnnStatus_t ucudnnCreate(UcudnnHandle_t* out) {
   return guarded([&] {

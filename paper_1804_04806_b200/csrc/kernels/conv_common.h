@@ -11,6 +11,11 @@
 
 namespace ucudnn {
 
+// Host-side count of device kernels this library has launched (evidence for
+// bench.py's gpu_launches; see ucudnnGetLaunchCount).
+void count_launch(int n = 1);
+std::uint64_t launch_count();
+
 // Unsigned division by a runtime constant via multiply-high (valid for
 // dividends < 2^31): q = umulhi(n, mul) >> shr, or n when d == 1.
 struct FastDiv {

@@ -387,6 +387,7 @@ cudaError_t launch(int op, IgemmParams p, int grid_x, int grid_y, int grid_z, cu
                                                                                 : igemm_kernel<kBwdFilter>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   kern<<<dim3(grid_x, grid_y, grid_z), kThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
@@ -455,6 +456,7 @@ cudaError_t igemm_backward_data(const ConvShape& s, const float* dy, const float
 cudaError_t scale_tensor(float* p, std::int64_t n, float beta, cudaStream_t stream) {
   if (beta == 1.f || n == 0) return cudaSuccess;
   int blocks = int(std::min<std::int64_t>((n + 255) / 256, 4 * num_sms()));
+  count_launch();
   scale_kernel<<<blocks, 256, 0, stream>>>(p, n, beta);
   return cudaGetLastError();
 }

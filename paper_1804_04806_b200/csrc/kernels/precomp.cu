@@ -313,10 +313,12 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   float* btiles = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                            align256(std::size_t(g.N) * g.Hin * g.Win * Cp * 4));
   const int HW = g.Hin * g.Win;
+  count_launch();
   to_nhwc_kernel<<<dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st>>>(act, act_nhwc, g.Cin, HW, Cp);
   {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
+    count_launch();
     pack_filter_kernel<<<blocks, 256, 0, st>>>(w, btiles, g.Nout, g.Cin, taps, BN, n_tiles, ksteps, Cp == 4 ? 1 : 0,
                                                Cp / 32, flip);
   }
@@ -372,6 +374,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int grid = std::min(sm_count(), p.m_tiles * p.n_tiles);
+  count_launch();
   precomp_kernel<<<grid, kThreads, smem, st>>>(amap, p);
   return cudaGetLastError();
 }

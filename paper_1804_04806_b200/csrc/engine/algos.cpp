@@ -2,6 +2,7 @@
 
 #include <atomic>
 
+#include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
 #include "../kernels/precomp.h"
 
@@ -29,6 +30,7 @@ cudaError_t igemm_run(int op, const ConvShape& s, const float* a, const float* b
 }
 
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
+const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 
 }  // namespace
@@ -36,6 +38,7 @@ const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_wo
 const AlgoImpl* find_algo(int id) {
   switch (id) {
     case 0: return &kImplicitGemm;
+    case 3: return &kGemm;
     case 5: return &kPrecomp;
     default: return nullptr;
   }

@@ -392,6 +392,9 @@ Geo bwd_data_geo(const ConvShape& s) {
 bool precomp_supports(int op, const ConvShape& s) {
   if (op == kFwd) return s.sh <= 8 && s.sw <= 8 && s.ph <= 127 && s.pw <= 127 && s.R <= 64 && s.S <= 64;
   if (op == kBwdData) return s.sh == 1 && s.sw == 1 && s.ph <= s.R - 1 && s.pw <= s.S - 1;
+  // BackwardFilter would need MN-major (pixel-reduction) operands, which
+  // tcgen05 kind::tf32 does not execute on this part; the
+  // GEMM algorithm covers it.
   return false;
 }
 

@@ -153,6 +153,25 @@ __device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr) {
   return d;
 }
 
+// SWIZZLE_128B MN-major descriptor: atoms of 8 K-rows x 128 B (32 MN
+// elements); `lbo` = byte stride between 32-element MN blocks, `sbo` = byte
+// stride between 8-row K groups.
+__device__ __forceinline__ std::uint64_t umma_desc_mn_sw128(std::uint32_t saddr, std::uint32_t lbo,
+                                                            std::uint32_t sbo) {
+  std::uint64_t d = 0;
+  d |= std::uint64_t((saddr >> 4) & 0x3FFF);
+  d |= std::uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= std::uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= std::uint64_t(1) << 46;
+  d |= std::uint64_t(2) << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::tf32 with both operands MN-major.
+__host__ __device__ constexpr std::uint32_t idesc_tf32_mn(int M, int N) {
+  return idesc_tf32(M, N) | (1u << 15) | (1u << 16);
+}
+
 // TMA im2col load of a 4-D NHWC tensor: `pixels x channels` box starting at
 // input coordinate (c, w, h, n) with filter-tap offsets (ow, oh).
 __device__ __forceinline__ void tma_im2col_4d(void* dst, const void* tmap, std::uint64_t* bar, int c, int w, int h,

@@ -27,7 +27,7 @@ SHAPES = [
     ConvShape(2, 40, 6, 6, 300, 3, 3, 1, 1, 1, 1),        # ragged tiles
     ConvShape(3, 64, 7, 7, 64, 3, 3, 1, 1, 1, 1),         # ResNet l4-like spatial size
 ]
-ALGOS = [0, 5]
+ALGOS = [0, 3, 5]
 
 
 def _sid(s):

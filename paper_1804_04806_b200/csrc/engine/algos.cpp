@@ -20,7 +20,7 @@ bool igemm_supports(int, const ConvShape&) { return true; }
 std::int64_t no_workspace(int, const ConvShape&) { return 0; }
 
 cudaError_t igemm_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void*, float alpha,
-                      float beta, cudaStream_t st) {
+                      float beta, cudaStream_t st, int) {
   switch (op) {
     case 0: return igemm_forward(s, a, b, out, alpha, beta, st);
     case 1: return igemm_backward_data(s, a, b, out, alpha, beta, st);

@@ -20,9 +20,11 @@ struct AlgoImpl {
   // Workspace bytes at micro-batch s.N.
   std::int64_t (*workspace)(int op, const ConvShape& s);
   // op 0: a = x, b = w, out = y; op 1: a = dy, b = w, out = dx;
-  // op 2: a = x, b = dy, out = dw.
+  // op 2: a = x, b = dy, out = dw. flags & kFilterReady: the previous
+  // micro-batch of the same call already prepared the (batch-independent)
+  // filter operand at the start of `ws`, so it is not re-packed.
   cudaError_t (*run)(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
-                     float alpha, float beta, cudaStream_t stream);
+                     float alpha, float beta, cudaStream_t stream, int flags);
 };
 
 // nullptr for ids that are reserved / not built.

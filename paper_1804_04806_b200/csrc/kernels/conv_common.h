@@ -55,6 +55,7 @@ struct ConvShape {
 };
 
 enum ConvOp : int { kFwd = 0, kBwdData = 1, kBwdFilter = 2 };
+constexpr int kFilterReady = 1;
 
 // Parameters of one implicit-GEMM launch. GEMM view per op:
 //   Fwd : rows = output pixels (n,oh,ow), cols = K, red = (c,r,s)

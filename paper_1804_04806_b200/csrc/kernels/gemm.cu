@@ -55,32 +55,49 @@ struct PackParams {
   FastDiv fd_P, fd_OW, fd_RS, fd_S, fd_ks;
 };
 
-__device__ __forceinline__ float gather(const PackParams& p, int row, int col) {
-  if (row >= p.rows || col >= p.cols) return 0.f;
+// Every packed element is src[ro(row) + co(col)] when (rh + ch) < Hlim and
+// (rw + cw) < Wlim (unsigned), else 0: rows and columns decode separately,
+// once per block, so the gather loop is two adds, two compares and a load.
+struct Dec {
+  int off, h, w;
+};
+constexpr int kBad = 1 << 20;
+
+__device__ __forceinline__ Dec decode_pixel(const PackParams& p, int pix, bool im2col) {
+  if (pix >= (p.kind == kIm2colPix || p.kind == kDyPixK ? p.rows : p.cols)) return Dec{0, kBad, 0};
+  std::uint32_t n, pp, oh, ow;
+  p.fd_P.divmod(std::uint32_t(pix), n, pp);
+  if (!im2col) return Dec{int(n) * p.K * p.P + int(pp), 0, 0};
+  p.fd_OW.divmod(pp, oh, ow);
+  const int h = int(oh) * p.sh - p.ph, w = int(ow) * p.sw - p.pw;
+  return Dec{int(n) * p.C * p.H * p.W + h * p.W + w, h, w};
+}
+__device__ __forceinline__ Dec decode_crs(const PackParams& p, int crs, int limit) {
+  if (crs >= limit) return Dec{0, kBad, 0};
+  std::uint32_t c, rs, r, s;
+  p.fd_RS.divmod(std::uint32_t(crs), c, rs);
+  p.fd_S.divmod(rs, r, s);
+  return Dec{int(c) * p.H * p.W + int(r) * p.W + int(s), int(r), int(s)};
+}
+__device__ __forceinline__ Dec decode_row(const PackParams& p, int row) {
   switch (p.kind) {
-    case kIm2colPix:
-    case kIm2colCrs: {
-      const int pix = p.kind == kIm2colPix ? row : col, crs = p.kind == kIm2colPix ? col : row;
-      std::uint32_t n, pp, oh, ow, c, rs, r, s;
-      p.fd_P.divmod(std::uint32_t(pix), n, pp);
-      p.fd_OW.divmod(pp, oh, ow);
-      p.fd_RS.divmod(std::uint32_t(crs), c, rs);
-      p.fd_S.divmod(rs, r, s);
-      const int h = int(oh) * p.sh - p.ph + int(r), w = int(ow) * p.sw - p.pw + int(s);
-      if (unsigned(h) >= unsigned(p.H) || unsigned(w) >= unsigned(p.W)) return 0.f;
-      return __ldg(p.src + ((std::int64_t(n) * p.C + c) * p.H + h) * p.W + w);
-    }
-    case kRowMajor: return __ldg(p.src + std::int64_t(row) * p.ld + col);
-    case kColMajor: return __ldg(p.src + std::int64_t(col) * p.ld + row);
-    case kDyKPix:
-    case kDyPixK: {
-      const int pix = p.kind == kDyKPix ? col : row, k = p.kind == kDyKPix ? row : col;
-      std::uint32_t n, pp;
-      p.fd_P.divmod(std::uint32_t(pix), n, pp);
-      return __ldg(p.src + (std::int64_t(n) * p.K + k) * p.P + pp);
-    }
+    case kIm2colPix: return decode_pixel(p, row, true);
+    case kIm2colCrs: return decode_crs(p, row, p.rows);
+    case kRowMajor: return row < p.rows ? Dec{row * p.ld, 0, 0} : Dec{0, kBad, 0};
+    case kColMajor: return row < p.rows ? Dec{row, 0, 0} : Dec{0, kBad, 0};
+    case kDyKPix: return row < p.rows ? Dec{row * p.P, 0, 0} : Dec{0, kBad, 0};
+    default: return decode_pixel(p, row, false);  // kDyPixK
   }
-  return 0.f;
+}
+__device__ __forceinline__ Dec decode_col(const PackParams& p, int col) {
+  switch (p.kind) {
+    case kIm2colPix: return decode_crs(p, col, p.cols);
+    case kIm2colCrs: return decode_pixel(p, col, true);
+    case kRowMajor: return col < p.cols ? Dec{col, 0, 0} : Dec{0, kBad, 0};
+    case kColMajor: return col < p.cols ? Dec{col * p.ld, 0, 0} : Dec{0, kBad, 0};
+    case kDyKPix: return decode_pixel(p, col, false);
+    default: return col < p.cols ? Dec{col * p.P, 0, 0} : Dec{0, kBad, 0};  // kDyPixK
+  }
 }
 
 // One block per (row tile, 32-column step): gather with lanes along the
@@ -88,9 +105,15 @@ __device__ __forceinline__ float gather(const PackParams& p, int row, int col) {
 // canonical block contiguously.
 __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
   __shared__ float tile[32][kMaxBN + 1];
+  __shared__ Dec rdec[kMaxBN], cdec[32];
   std::uint32_t rt, ks;
   p.fd_ks.divmod(blockIdx.x, rt, ks);
   const int row0 = int(rt) * p.ROWS, col0 = int(ks) * 32;
+  for (int i = threadIdx.x; i < p.ROWS; i += blockDim.x) rdec[i] = decode_row(p, row0 + i);
+  if (threadIdx.x < 32) cdec[threadIdx.x] = decode_col(p, col0 + threadIdx.x);
+  __syncthreads();
+  const bool im2col = p.kind == kIm2colPix || p.kind == kIm2colCrs;
+  const unsigned hl = im2col ? unsigned(p.H) : 1u, wl = im2col ? unsigned(p.W) : 1u;
   const bool col_fast = p.kind == kIm2colCrs || p.kind == kRowMajor || p.kind == kDyKPix;
   for (int idx = threadIdx.x; idx < p.ROWS * 32; idx += blockDim.x) {
     int r, c;
@@ -101,7 +124,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
       r = idx % p.ROWS;
       c = idx / p.ROWS;
     }
-    tile[c][r] = gather(p, row0 + r, col0 + c);
+    const Dec a = rdec[r], b = cdec[c];
+    tile[c][r] = (unsigned(a.h + b.h) < hl && unsigned(a.w + b.w) < wl) ? __ldg(p.src + a.off + b.off) : 0.f;
   }
   __syncthreads();
   float4* out = reinterpret_cast<float4*>(p.dst) + std::size_t(blockIdx.x) * (p.ROWS * 8);
@@ -394,8 +418,12 @@ cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, floa
   g.fd_P = FastDiv(std::uint32_t(P > 0 ? P : 1));
   const int stage = kBM * 128 + ((q.BN * 128 + 127) & ~127);
   const int smem = std::max(kStages * stage + 1024 + 256, 116 * 1024);
-  cudaError_t e = cudaFuncSetAttribute(tiled_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static int smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(tiled_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    smem_set = 227 * 1024;
+  }
   count_launch();
   tiled_gemm_kernel<<<std::min(sms(), tiles * g.splits), kThreads, smem, st>>>(g);
   return cudaGetLastError();
@@ -410,21 +438,26 @@ bool gemm_supports(int, const ConvShape& s) {
 std::int64_t gemm_workspace(int op, const ConvShape& s) { return std::int64_t(workspace_of(op, s)); }
 
 cudaError_t gemm_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
-                     float beta, cudaStream_t st) {
+                     float beta, cudaStream_t st, int flags) {
   const Problem q = problem_of(op, s);
-  float* A = static_cast<float*>(ws);
-  float* B = reinterpret_cast<float*>(static_cast<char*>(ws) + a256(q.a_bytes()));
+  // B (the filter for Forward / BackwardData) first: batch-independent, so
+  // later micro-batches of one call reuse it (kFilterReady)
+  float* B = static_cast<float*>(ws);
+  float* A = reinterpret_cast<float*>(static_cast<char*>(ws) + a256(q.b_bytes()));
+  const bool filter_ready = (flags & kFilterReady) && op != kBwdFilter;
   const int CRS = s.C * s.R * s.S, P = s.OH() * s.OW();
   cudaError_t e;
   if (op == kFwd) {
     if ((e = pack(pack_params(s, kIm2colPix, a, A, q.M, CRS, 0, kBM), st)) != cudaSuccess) return e;
-    if ((e = pack(pack_params(s, kRowMajor, b, B, s.K, CRS, CRS, q.BN), st)) != cudaSuccess) return e;
+    if (!filter_ready && (e = pack(pack_params(s, kRowMajor, b, B, s.K, CRS, CRS, q.BN), st)) != cudaSuccess)
+      return e;
     return gemm(q, A, B, kEpiNchw, out, alpha, beta, P, 0, false, st);
   }
   if (op == kBwdData) {
-    float* dcol = reinterpret_cast<float*>(reinterpret_cast<char*>(B) + a256(q.b_bytes()));
+    float* dcol = reinterpret_cast<float*>(reinterpret_cast<char*>(A) + a256(q.a_bytes()));
     if ((e = pack(pack_params(s, kDyPixK, a, A, q.M, s.K, 0, kBM), st)) != cudaSuccess) return e;
-    if ((e = pack(pack_params(s, kColMajor, b, B, CRS, s.K, CRS, q.BN), st)) != cudaSuccess) return e;
+    if (!filter_ready && (e = pack(pack_params(s, kColMajor, b, B, CRS, s.K, CRS, q.BN), st)) != cudaSuccess)
+      return e;
     if ((e = gemm(q, A, B, kEpiRowMajor, dcol, 1.f, 0.f, 0, CRS, false, st)) != cudaSuccess) return e;
     const std::int64_t total = s.x_elems();
     count_launch();

@@ -300,22 +300,24 @@ std::size_t geo_ws(const Geo& g, int* ksteps_out = nullptr, int* bn_out = nullpt
   const int BN = pick_bn(g.Nout), n_tiles = (g.Nout + BN - 1) / BN;
   if (ksteps_out) *ksteps_out = ksteps;
   if (bn_out) *bn_out = BN;
-  return align256(std::size_t(g.N) * g.Hin * g.Win * Cp * 4) + std::size_t(n_tiles) * ksteps * BN * 128;
+  return align256(std::size_t(n_tiles) * ksteps * BN * 128) + align256(std::size_t(g.N) * g.Hin * g.Win * Cp * 4);
 }
 
 cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, float* out, void* ws, float alpha,
-                    float beta, cudaStream_t st) {
+                    float beta, cudaStream_t st, int flags) {
   const int Cp = cpad(g.Cin), taps = g.R * g.S;
   int ksteps = 0, BN = 0;
   geo_ws(g, &ksteps, &BN);
   const int n_tiles = (g.Nout + BN - 1) / BN;
-  float* act_nhwc = static_cast<float*>(ws);
-  float* btiles = reinterpret_cast<float*>(static_cast<char*>(ws) +
-                                           align256(std::size_t(g.N) * g.Hin * g.Win * Cp * 4));
+  // packed filter first: its size does not depend on the micro-batch, so
+  // later micro-batches of the same call reuse it (kFilterReady)
+  float* btiles = static_cast<float*>(ws);
+  float* act_nhwc = reinterpret_cast<float*>(static_cast<char*>(ws) +
+                                             align256(std::size_t(n_tiles) * ksteps * BN * 128));
   const int HW = g.Hin * g.Win;
   count_launch();
   to_nhwc_kernel<<<dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st>>>(act, act_nhwc, g.Cin, HW, Cp);
-  {
+  if (!(flags & kFilterReady)) {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     count_launch();
@@ -371,8 +373,12 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)
   const int smem = std::max(kStages * stage_bytes + 1024 + 256, 116 * 1024);
-  e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static int smem_set = 0;
+  if (smem > smem_set) {
+    e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    smem_set = 227 * 1024;
+  }
   const int grid = std::min(sm_count(), p.m_tiles * p.n_tiles);
   count_launch();
   precomp_kernel<<<grid, kThreads, smem, st>>>(amap, p);
@@ -405,9 +411,9 @@ std::int64_t precomp_workspace(int op, const ConvShape& s) {
 }
 
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
-                        float beta, cudaStream_t st) {
-  if (op == kFwd) return run_geo(fwd_geo(s), a, b, 0, out, ws, alpha, beta, st);
-  if (op == kBwdData) return run_geo(bwd_data_geo(s), a, b, 1, out, ws, alpha, beta, st);
+                        float beta, cudaStream_t st, int flags) {
+  if (op == kFwd) return run_geo(fwd_geo(s), a, b, 0, out, ws, alpha, beta, st, flags);
+  if (op == kBwdData) return run_geo(bwd_data_geo(s), a, b, 1, out, ws, alpha, beta, st, flags);
   return cudaErrorNotSupported;
 }
 

@@ -12,6 +12,6 @@ namespace ucudnn {
 bool precomp_supports(int op, const ConvShape& s);
 std::int64_t precomp_workspace(int op, const ConvShape& s);
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
-                        float alpha, float beta, cudaStream_t stream);
+                        float alpha, float beta, cudaStream_t stream, int flags);
 
 }  // namespace ucudnn

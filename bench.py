@@ -200,6 +200,18 @@ def main():
 
     # plan: benchmark every (algorithm x micro-batch) on the device, WR DP
     t0 = time.perf_counter()
+    if dist_on:
+        # rank 0 benchmarks; every rank plans from its table -> identical plans
+        from paper_1804_04806_b200.network import share_cost_table
+        if rank == 0:
+            h0 = Handle(policy=args.policy, mode="wr", database=db, stream=stream.cuda_stream)
+            stack.plan(h0, limit)
+            h0.flush_database()
+            h0.close()
+        else:
+            open(db, "w").write("")
+        torch.distributed.barrier()
+        share_cost_table(db)
     h = Handle(policy=args.policy, mode="wr", database=db, stream=stream.cuda_stream)
     stack.plan(h, limit)
     h.flush_database()

@@ -47,6 +47,34 @@ def parse_net(path: str, batch: Optional[int] = None):
     return name, [Layer(nm, ConvShape(n, c, h, w, k, r, s, p, p, st, st)) for nm, c, h, w, k, r, s, p, st in layers]
 
 
+def shard(global_batch: int, world: int, rank: int):
+    """Contiguous data-parallel shard (start, count) of a global mini-batch."""
+    base, extra = divmod(global_batch, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+def share_cost_table(csv_path: str, group=None) -> str:
+    """Rank 0's benchmarked cost table (the reference CSV format,
+    cost_database.hpp:32-45) broadcast to every rank, so all ranks plan from
+    the same rows -- and the planner being deterministic, run the same plan."""
+    import torch.distributed as dist
+    payload = [open(csv_path).read() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(payload, src=0, group=group)
+    if dist.get_rank(group) != 0:
+        with open(csv_path, "w") as f:
+            f.write(payload[0])
+    return payload[0]
+
+
+def allreduce_filter_grads(grads, group=None, async_op=False):
+    """Sum each layer's filter gradient over the data-parallel ranks (the
+    caller applies 1/N, reference SPEC.md:370: BackwardFilter has no 1/N)."""
+    import torch.distributed as dist
+    works = [dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group, async_op=async_op) for g in grads]
+    return works if async_op else None
+
+
 class ConvStack:
     def __init__(self, net_path: str, batch: int, device, seed: int = 1804):
         self.name, self.layers = parse_net(net_path, batch)

@@ -71,5 +71,31 @@ def main():
     print("random instances: 300")
 
 
+
+def make_conv_golden():
+    """Small conv golden vectors from the reference's own execute_plan
+    (oracle/_ref/ref_conv.so): integer inputs, one stride-2 and one padded
+    case per op, a non-trivial micro-batch plan each."""
+    import sys
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    from paper_1804_04806_b200.api import ConvShape
+    from tests.oracle_py import conv_ref, inputs_for
+    cases = [(ConvShape(5, 3, 9, 8, 4, 3, 3, 1, 1, 2, 2), [2, 2, 1]),
+             (ConvShape(4, 2, 7, 7, 3, 5, 5, 2, 2, 1, 1), [3, 1]),
+             (ConvShape(3, 4, 11, 11, 2, 11, 11, 2, 2, 4, 4), [1, 1, 1])]
+    out = {}
+    for i, (s, plan) in enumerate(cases):
+        for op in range(3):
+            a, b = inputs_for(op, s, np.random.default_rng(100 * i + op), integer=True)
+            out[f"c{i}_op{op}_a"], out[f"c{i}_op{op}_b"] = a, b
+            out[f"c{i}_op{op}_out"] = conv_ref(op, s, a, b, plan, use_reference=True)
+        out[f"c{i}_shape"] = np.array([s.N, s.C, s.H, s.W, s.K, s.R, s.S, s.ph, s.pw, s.sh, s.sw])
+        out[f"c{i}_plan"] = np.array(plan)
+    np.savez_compressed(os.path.join(OUT, "conv_golden.npz"), **out)
+    print("conv golden:", len(cases), "cases x 3 ops")
+
+
 if __name__ == "__main__":
     main()
+    make_conv_golden()

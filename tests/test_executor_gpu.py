@@ -1,0 +1,88 @@
+"""The micro-batch executor through the C ABI (virtual algorithm ids).
+
+A cost table injected through ucudnnSetCostDatabase forces a plan that mixes
+algorithms and micro-batch sizes; the executor must then reproduce the
+reference execute_plan semantics (reference_conv.hpp:205-278): canonical
+micro order, disjoint F/BD slices with per-slice alpha/beta, BF accumulating
+with the user's beta on the first micro-batch only.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1804_04806_b200 import ConvShape, Handle, algorithm_workspace, kernel_hash
+from tests.oracle_py import conv_ref, inputs_for, out_shape
+
+pytestmark = pytest.mark.gpu
+HEADER = "kernel_hash,op_type,algorithm,micro_batch,time_us,workspace_bytes,feasible"
+OPS = ["Forward", "BackwardData", "BackwardFilter"]
+
+
+def forced_table(s, op, times):
+    """times[alg][b] -> us (missing: infeasible); real workspace sizes."""
+    h = kernel_hash(op, s)
+    rows = []
+    for alg in range(6):
+        for b in range(1, s.N + 1):
+            t = times.get(alg, {}).get(b)
+            ws, ok = algorithm_workspace(op, s, alg, b)
+            if t is None or not ok:
+                rows.append(f"{h:016x},{OPS[op]},{alg},{b},0,0,0")
+            else:
+                rows.append(f"{h:016x},{OPS[op]},{alg},{b},{t},{ws},1")
+    return HEADER + "\n" + "\n".join(rows) + "\n"
+
+
+BIG = 10 ** 6
+TIMES = {3: {1: 100, 2: 10, 3: BIG, 4: BIG, 5: BIG}, 0: {1: 5, 2: BIG, 3: BIG, 4: BIG, 5: BIG}}
+
+
+@pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
+def test_forced_mixed_plan_matches_oracle(cuda, tmp_path, op):
+    s = ConvShape(5, 4, 9, 9, 8, 3, 3, 1, 1, 2, 2)
+    db = tmp_path / "t.csv"
+    db.write_text(forced_table(s, op, TIMES))
+    h = Handle(policy="all", database=str(db))
+    algo = h.get_algorithm(op, s, 1 << 30)
+    assert h.plan(algo) == [(3, 2), (3, 2), (0, 1)]
+    rng = np.random.default_rng(31 + op)
+    a, b = inputs_for(op, s, rng, integer=True)
+    init = np.random.default_rng(1).integers(-3, 4, size=out_shape(op, s)).astype(np.float64)
+    ta, tb = torch.from_numpy(a).float().to(cuda), torch.from_numpy(b).float().to(cuda)
+    out = torch.from_numpy(init).float().to(cuda)
+    ws = torch.empty(h.workspace_size(algo, op, s) // 4 + 1, device=cuda)
+    h.run(op, s, ta, tb, out, algo, ws, alpha=1.0, beta=2.0)
+    torch.cuda.synchronize()
+    want = conv_ref(op, s, a, b, [2, 2, 1]) + 2.0 * init
+    assert np.array_equal(out.cpu().double().numpy(), want)
+
+
+def test_wd_mode_plans_network_and_uses_arena(cuda):
+    s = ConvShape(4, 16, 10, 10, 32, 3, 3, 1, 1, 1, 1)
+    h = Handle(policy="powerOfTwo", mode="wd", total_workspace=64 << 20)
+    h.set_benchmark_iterations(1, 2)
+    algos = [h.get_algorithm(op, s, 0) for op in range(3)]
+    h.optimize_network()
+    assert all(h.workspace_size(a, op, s) == 0 for op, a in enumerate(algos))
+    rng = np.random.default_rng(4)
+    x, w, dy = (inputs_for(0, s, rng)[0], inputs_for(0, s, rng)[1], inputs_for(1, s, rng)[0])
+    tx, tw, tdy = (torch.from_numpy(v).float().to(cuda) for v in (x, w, dy))
+    outs = [torch.empty(out_shape(op, s), device=cuda) for op in range(3)]
+    for op, (ia, ib) in enumerate(((tx, tw), (tdy, tw), (tx, tdy))):
+        h.run(op, s, ia, ib, outs[op], algos[op])
+    torch.cuda.synchronize()
+    for op, (ia, ib) in enumerate(((x, w), (dy, w), (x, dy))):
+        assert np.array_equal(outs[op].cpu().double().numpy(), conv_ref(op, s, ia, ib))
+    rep = h.machine_report()
+    assert "mode wd" in rep and "kernel-count 3" in rep and rep.endswith("end\n")
+
+
+def test_wr_plan_respects_workspace_limit(cuda):
+    s = ConvShape(16, 64, 13, 13, 64, 3, 3, 1, 1, 1, 1)
+    h = Handle(policy="powerOfTwo")
+    h.set_benchmark_iterations(1, 3)
+    for limit in (0, 1 << 20, 64 << 20):
+        for op in range(3):
+            a = h.get_algorithm(op, s, limit)
+            assert h.workspace_size(a, op, s) <= limit
+            assert sum(b for _, b in h.plan(a)) == s.N

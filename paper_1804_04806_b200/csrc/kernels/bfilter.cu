@@ -1,0 +1,465 @@
+// UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM, BackwardFilter: a tcgen05 GEMM whose
+// operands are fetched by plain TMA *tiled* loads -- no im2col buffer.
+//
+//   dW[k][c][r][s] += alpha * sum_{n,oh,ow} dy[n][k][oh][ow] * x[n][c][oh*sh-ph+r][ow*sw-pw+s]
+//   (reference_conv.hpp:141-171; beta applied once up front, :173-180)
+//
+// tcgen05 kind::tf32 only executes K-major operands,
+// so the reduction axis -- output pixels -- must be the contiguous one in
+// shared memory. NCHW already has pixels contiguous; what stops TMA is the
+// 16-byte stride rule (rows of 27 / 13 / 55 floats) and the conv geometry.
+// Two cheap, HBM-bound re-layouts in the workspace fix both:
+//
+//   x_ph[n][cc][Hq*Wq]  cc = (a, b, c): the zero-padded input split into
+//                       its (sh x sw) stride phases (only phases a < R,
+//                       b < S are kept), plane i*Wq + j = x_pad[i*sh+a][j*sw+b]
+//   dy_p[n][k][OH*Wq]   dy with rows re-pitched from OW to Wq, zero in
+//                       columns ow >= OW
+//
+// In these layouts output pixel (oh, ow) sits at flat position
+// j = oh*Wq + ow of dy_p, and its tap (r, s) = (qh*sh + a, qw*sw + b) reads
+// x_ph plane (a, b, c) at j + qh*Wq + qw. So for a fixed (qh, qw) the A
+// operand of a 32-pixel reduction step is a dense [channels x 32] box of
+// x_ph at a shifted flat coordinate, and the B operand a dense [k x 32] box
+// of dy_p: each lands in shared memory as the SWIZZLE_128B K-major UMMA
+// layout directly. The padded columns of dy_p are zero, so whatever x_ph
+// holds under them contributes nothing; TMA's out-of-bounds zero fill
+// covers every other edge. GEMM rows are (qh, qw, cc) -- for strided convs
+// all phases of one shifted window share one box (AlexNet conv1: 48 rows).
+// TMA requires the innermost start coordinate to be 16-byte aligned (a
+// misaligned one is an illegal instruction on this part), so x_ph is stored
+// as T <= 4 replicas shifted by 0..T-1 elements and a tap offset o reads
+// replica (o mod 4) at o rounded down; with Qw < 4 the pitch Wq is rounded
+// to a multiple of 4 so only T = Qw replicas exist.
+//
+// Persistent kernel, one CTA per SM, split-K over (image, 32-pixel step)
+// units, 256 threads: warp 0 = TMA producer over a 4-stage mbarrier ring,
+// warp 1 = TMEM owner + MMA issuer (two 256-column accumulators), warps 4-7
+// = epilogue (TMEM -> fp32 RED into dW), overlapping the next unit.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "bfilter.h"
+#include "conv_common.h"
+#include "sm100.cuh"
+
+namespace ucudnn {
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 256;
+constexpr int kMaxBN = 256;
+
+struct BfGeo {
+  int N, C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
+  int Ah, Bw, Qh, Qw;  // phases kept, tap offsets per phase
+  int CC, CCp, Gb;     // phase-channels, padded to a multiple of Gb, rows per box
+  int Hq, Wq, Lq, Lp;  // phase plane: rows, pitch, length, padded length (x 4 floats)
+  int T;               // shifted replicas of x_ph (TMA start coordinates are 16 B aligned)
+  int Ld, Ldp;         // dy_p plane: OH*Wq and its padded length
+  int Lc;              // 32-pixel reduction steps per image
+  int M, BN, m_tiles, n_tiles;
+};
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+BfGeo make_geo(const ConvShape& s) {
+  BfGeo g{};
+  g.N = s.N; g.C = s.C; g.H = s.H; g.W = s.W; g.K = s.K; g.R = s.R; g.S = s.S;
+  g.ph = s.ph; g.pw = s.pw; g.sh = s.sh; g.sw = s.sw; g.OH = s.OH(); g.OW = s.OW();
+  g.Ah = std::min(s.sh, s.R);
+  g.Bw = std::min(s.sw, s.S);
+  g.Qh = (s.R + s.sh - 1) / s.sh;
+  g.Qw = (s.S + s.sw - 1) / s.sw;
+  g.CC = g.Ah * g.Bw * s.C;
+  // rows per TMA box = largest power of two <= 128 dividing CCp: pad small
+  // channel counts to a power of two (MMA rows are cheaper than TMA boxes)
+  if (g.CC < 128) {
+    g.CCp = 8;
+    while (g.CCp < g.CC) g.CCp <<= 1;
+  } else {
+    g.CCp = round_up(g.CC, 32);
+  }
+  g.Gb = 128;
+  while (g.CCp % g.Gb) g.Gb >>= 1;
+  g.Hq = (s.H + 2 * s.ph + s.sh - 1) / s.sh;
+  g.Wq = (s.W + 2 * s.pw + s.sw - 1) / s.sw;
+  // A tap offset qh*Wq + qw needs replica (offset mod 4). With a pitch that
+  // is a multiple of 4 only qw mod 4 matters (Qw replicas); with >= 4 column
+  // offsets all four are needed anyway, so keep the tight pitch.
+  if (g.Qw < 4 && g.Qh * g.Qw > 1) {
+    g.Wq = round_up(g.Wq, 4);
+    g.T = g.Qw;
+  } else {
+    g.T = g.Qh * g.Qw > 1 ? 4 : 1;
+  }
+  g.Lq = g.Hq * g.Wq;
+  g.Lp = round_up(g.Lq, 4);
+  g.Ld = g.OH * g.Wq;
+  g.Ldp = round_up(g.Ld, 4);
+  g.Lc = (g.Ld + 31) / 32;
+  g.M = g.Qh * g.Qw * g.CCp;
+  const int nt = (s.K + kMaxBN - 1) / kMaxBN;
+  g.BN = round_up((s.K + nt - 1) / nt, 16);
+  g.n_tiles = (s.K + g.BN - 1) / g.BN;
+  g.m_tiles = (g.M + kBM - 1) / kBM;
+  return g;
+}
+
+std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
+std::size_t x_bytes(const BfGeo& g) { return a256(std::size_t(g.T) * g.N * g.CC * g.Lp * 4); }
+std::size_t dy_bytes(const BfGeo& g) { return a256(std::size_t(g.N) * g.K * g.Ldp * 4); }
+
+struct BfParams {
+  float* dw;
+  float alpha;
+  int K, CRS, RS, S, R, C, Bw, Ah, sh, sw, Qw, CCp, CC, Gb, Wq, M, BN;
+  int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages;
+};
+
+__device__ __forceinline__ void tma_4d(void* dst, const void* tmap, std::uint64_t* bar, int x, int y, int z, int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    bf_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap, const BfParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t a_bytes = kBM * 128;
+  const std::uint32_t b_bytes = std::uint32_t(p.BN) * 128;
+  const std::uint32_t stage_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&dmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int units = p.tiles * p.splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      const int boxes = kBM / p.Gb;
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = u % p.tiles, split = u / p.tiles;
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        int n = g0 / p.Lc, ch = g0 - n * p.Lc;
+        for (int g = g0; g < g1; ++g, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          unsigned char* sa = smem + st * stage_bytes;
+          mbar_expect_tx(&full[st], a_bytes + b_bytes);
+          const int j0 = ch * 32;
+#pragma unroll 1
+          for (int bx = 0; bx < boxes; ++bx) {
+            const int row0 = mt * kBM + bx * p.Gb;
+            const int q = row0 / p.CCp, cc0 = row0 - q * p.CCp;
+            const int qh = q / p.Qw, qw = q - qh * p.Qw;
+            // rows past M: an out-of-range channel coordinate makes TMA zero-fill the box
+            // TMA wants the innermost start coordinate 16-byte aligned: the
+            // misaligned part of the tap offset selects a pre-shifted replica
+            const int o = j0 + qh * p.Wq + qw;
+            tma_4d(sa + bx * (p.Gb * 128), &xmap, &full[st], o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
+          }
+          tma_4d(sa + a_bytes, &dmap, &full[st], j0, nt * p.BN, n, 0);
+          if (++ch == p.Lc) {
+            ch = 0;
+            ++n;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint32_t sbase = smem_u32(smem);
+    int it = 0, tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int split = u / p.tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      for (int g = g0; g < g1; ++g, ++it) {
+        const int st = it % kStages;
+        mbar_wait(&full[st], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            mma_tf32(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
+                     (g != g0 || q != 0) ? 1u : 0u);
+          mma_commit(&empty[st]);
+          if (g == g1 - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+      if (g1 <= g0 && lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue: RED into dW
+    const int ew = warp - 4;
+    int tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      // this thread's GEMM row -> dW offset (c, r, s), or invalid
+      const int row = mt * kBM + ew * 32 + lane;
+      int off = -1;
+      if (row < p.M && g1 > g0) {
+        const int q = row / p.CCp, cc = row - q * p.CCp;
+        const int qh = q / p.Qw, qw = q - qh * p.Qw;
+        if (cc < p.CC) {
+          const int ab = cc / p.C, c = cc - ab * p.C;
+          const int a = ab / p.Bw, b = ab - a * p.Bw;
+          const int r = qh * p.sh + a, s = qw * p.sw + b;
+          if (r < p.R && s < p.S) off = c * p.RS + r * p.S + s;
+        }
+      }
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (off < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = nt * p.BN + c0 + j;
+          if (c0 + j >= p.BN || k >= p.K) break;
+          red_add(p.dw + std::int64_t(k) * p.CRS + off, p.alpha * v[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// x (NCHW) -> x_ph[t][n][(a,b,c)][Lp]: zero padding + stride-phase split,
+// replica t shifted left by t elements. One thread = 4 consecutive plane
+// positions of every replica (float4 stores; HBM-bound).
+struct XPhaseArgs {
+  const float* x;
+  float* out;
+  int C, H, W, ph, pw, sh, sw, Bw, CC, T;
+  std::int64_t units, rep;  // float4 units per replica, floats per replica
+  FastDiv fd_u, fd_wq, fd_c, fd_bw;  // units per plane, plane pitch, C, Bw
+};
+__global__ void __launch_bounds__(256) x_phase_kernel(const XPhaseArgs a) {
+  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < a.units;
+       u += std::int64_t(gridDim.x) * blockDim.x) {
+    std::uint32_t plane, q;
+    a.fd_u.divmod(std::uint32_t(u), plane, q);
+    std::uint32_t n, cc, ab, c, pa, pb;
+    n = plane / std::uint32_t(a.CC);
+    cc = plane - n * std::uint32_t(a.CC);
+    a.fd_c.divmod(cc, ab, c);
+    a.fd_bw.divmod(ab, pa, pb);
+    const float* src = a.x + (std::int64_t(n) * a.C + c) * a.H * a.W;
+    const int p0 = int(q) * 4;
+    float v[7];
+    std::uint32_t i, j;
+    a.fd_wq.divmod(std::uint32_t(p0), i, j);
+#pragma unroll
+    for (int e = 0; e < 7; ++e) {
+      const int h = int(i) * a.sh + int(pa) - a.ph, w = int(j) * a.sw + int(pb) - a.pw;
+      v[e] = (e < a.T + 3 && unsigned(h) < unsigned(a.H) && unsigned(w) < unsigned(a.W)) ? __ldg(src + h * a.W + w)
+                                                                                        : 0.f;
+      if (++j == a.fd_wq.d) {
+        j = 0;
+        ++i;
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(a.out) + u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < a.T) dst[t * (a.rep / 4)] = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
+  }
+}
+
+// dy (NCHW) -> dy_p[n][k][Ldp]: rows re-pitched to Wq, zero beyond OW.
+__global__ void __launch_bounds__(256) dy_pitch_kernel(const float* __restrict__ dy, float* __restrict__ out, int OH,
+                                                       int OW, std::int64_t units, FastDiv fd_u, FastDiv fd_wq) {
+  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < units;
+       u += std::int64_t(gridDim.x) * blockDim.x) {
+    std::uint32_t plane, q, i, j;
+    fd_u.divmod(std::uint32_t(u), plane, q);
+    const float* src = dy + std::int64_t(plane) * OH * OW;
+    fd_wq.divmod(q * 4, i, j);
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] = (int(i) < OH && int(j) < OW) ? __ldg(src + int(i) * OW + int(j)) : 0.f;
+      if (++j == fd_wq.d) {
+        j = 0;
+        ++i;
+      }
+    }
+    reinterpret_cast<float4*>(out)[u] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+__global__ void bf_scale_kernel(float* p, std::int64_t n, float beta) {
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += std::int64_t(gridDim.x) * blockDim.x)
+    p[i] = beta == 0.f ? 0.f : p[i] * beta;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+int sm_count() {
+  static int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+// dims (d0, d1, d2, d3) with element pitches of dims 1..3; box (box0, box1, 1, 1)
+bool encode_4d(CUtensorMap* m, const float* base, int d0, int d1, int d2, int d3, std::int64_t pitch1,
+               std::int64_t pitch2, std::int64_t pitch3, int box0, int box1) {
+  const cuuint64_t dims[4] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2), cuuint64_t(d3)};
+  const cuuint64_t strides[3] = {cuuint64_t(pitch1) * 4, cuuint64_t(pitch2) * 4, cuuint64_t(pitch3) * 4};
+  const cuuint32_t box[4] = {cuuint32_t(box0), cuuint32_t(box1), 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool bf_supports(const ConvShape& s) {
+  const BfGeo g = make_geo(s);
+  // TMA coordinates are int32 and box dims <= 256; flat offsets must fit
+  return std::int64_t(g.Lq) + 64 < (std::int64_t(1) << 30) && g.CC < (1 << 20) && s.K < (1 << 20) &&
+         std::int64_t(g.N) * g.CC * g.Lp / 4 < (std::int64_t(1) << 31) &&
+         std::int64_t(g.N) * g.K * g.Ldp / 4 < (std::int64_t(1) << 31);
+}
+
+std::int64_t bf_workspace(const ConvShape& s) {
+  const BfGeo g = make_geo(s);
+  return std::int64_t(x_bytes(g) + dy_bytes(g));
+}
+
+cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
+                   cudaStream_t st) {
+  const BfGeo g = make_geo(s);
+  float* xph = static_cast<float*>(ws);
+  float* dyp = reinterpret_cast<float*>(static_cast<char*>(ws) + x_bytes(g));
+  if (beta != 1.f) {
+    const std::int64_t n = s.w_elems();
+    count_launch();
+    bf_scale_kernel<<<int(std::min<std::int64_t>((n + 255) / 256, 4 * sm_count())), 256, 0, st>>>(dw, n, beta);
+  }
+  const FastDiv fd_wq(std::uint32_t(g.Wq));
+  const int sms = sm_count();
+  XPhaseArgs xa{x, xph, g.C, g.H, g.W, g.ph, g.pw, g.sh, g.sw, g.Bw, g.CC, g.T,
+                std::int64_t(g.N) * g.CC * (g.Lp / 4), std::int64_t(g.N) * g.CC * g.Lp,
+                FastDiv(std::uint32_t(g.Lp / 4)), fd_wq, FastDiv(std::uint32_t(g.C)), FastDiv(std::uint32_t(g.Bw))};
+  count_launch();
+  x_phase_kernel<<<int(std::min<std::int64_t>((xa.units + 255) / 256, 16 * sms)), 256, 0, st>>>(xa);
+  const std::int64_t dunits = std::int64_t(g.N) * g.K * (g.Ldp / 4);
+  count_launch();
+  dy_pitch_kernel<<<int(std::min<std::int64_t>((dunits + 255) / 256, 16 * sms)), 256, 0, st>>>(
+      dy, dyp, g.OH, g.OW, dunits, FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  CUtensorMap xmap, dmap;
+  const std::int64_t rep = std::int64_t(g.N) * g.CC * g.Lp;
+  if (!encode_4d(&xmap, xph, g.Lq, g.CC, g.N, g.T, g.Lp, std::int64_t(g.CC) * g.Lp, rep, 32, g.Gb))
+    return cudaErrorInvalidValue;
+  if (!encode_4d(&dmap, dyp, g.Ld, g.K, g.N, 1, g.Ldp, std::int64_t(g.K) * g.Ldp, std::int64_t(g.N) * g.K * g.Ldp, 32,
+                 g.BN))
+    return cudaErrorInvalidValue;
+
+  BfParams p{};
+  p.dw = dw;
+  p.alpha = alpha;
+  p.K = g.K; p.C = g.C; p.R = g.R; p.S = g.S;
+  p.RS = g.R * g.S;
+  p.CRS = g.C * p.RS;
+  p.Bw = g.Bw; p.Ah = g.Ah; p.sh = g.sh; p.sw = g.sw; p.Qw = g.Qw;
+  p.CCp = g.CCp; p.CC = g.CC; p.Gb = g.Gb; p.Wq = g.Wq; p.M = g.M; p.BN = g.BN;
+  p.m_tiles = g.m_tiles;
+  p.tiles = g.m_tiles * g.n_tiles;
+  p.Lc = g.Lc;
+  p.T = g.T;
+  p.steps = g.N * g.Lc;
+  // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
+  int splits = std::max(1, std::min(p.steps / 8, sms / p.tiles));
+  p.steps_per_unit = (p.steps + splits - 1) / splits;
+  p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
+  const int stage_bytes = kBM * 128 + ((g.BN * 128 + 1023) & ~1023);
+  p.stages = std::min(kMaxStages, (200 * 1024) / stage_bytes);
+  const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(bf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  count_launch();
+  bf_kernel<<<std::min(sms, p.tiles * p.splits), kThreads, smem, st>>>(xmap, dmap, p);
+  return cudaGetLastError();
+}
+
+}  // namespace ucudnn

@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <mutex>
 
+#include "bfilter.h"
 #include "conv_common.h"
 #include "precomp.h"
 #include "sm100.cuh"
@@ -398,23 +399,21 @@ Geo bwd_data_geo(const ConvShape& s) {
 bool precomp_supports(int op, const ConvShape& s) {
   if (op == kFwd) return s.sh <= 8 && s.sw <= 8 && s.ph <= 127 && s.pw <= 127 && s.R <= 64 && s.S <= 64;
   if (op == kBwdData) return s.sh == 1 && s.sw == 1 && s.ph <= s.R - 1 && s.pw <= s.S - 1;
-  // BackwardFilter would need MN-major (pixel-reduction) operands, which
-  // tcgen05 kind::tf32 does not execute on this part; the
-  // GEMM algorithm covers it.
-  return false;
+  // BackwardFilter: TMA-tiled phase-split operands (bfilter.cu)
+  return bf_supports(s);
 }
 
 std::int64_t precomp_workspace(int op, const ConvShape& s) {
   if (op == kFwd) return std::int64_t(geo_ws(fwd_geo(s)));
   if (op == kBwdData) return std::int64_t(geo_ws(bwd_data_geo(s)));
-  return 0;
+  return bf_workspace(s);
 }
 
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                         float beta, cudaStream_t st, int flags) {
   if (op == kFwd) return run_geo(fwd_geo(s), a, b, 0, out, ws, alpha, beta, st, flags);
   if (op == kBwdData) return run_geo(bwd_data_geo(s), a, b, 1, out, ws, alpha, beta, st, flags);
-  return cudaErrorNotSupported;
+  return bf_run(s, a, b, out, ws, alpha, beta, st);
 }
 
 }  // namespace ucudnn

@@ -54,6 +54,10 @@ struct PrecompParams {
   int taps, S, c_chunks;
   int OW, OHW, sh, sw, ph, pw;  // output geometry in the *input* frame of the TMA map
   FastDiv fd_P, fd_OW, fd_mt;
+  // phase scatter epilogue (strided BackwardData): column (a, b, c) of
+  // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
+  int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  FastDiv fd_Cr, fd_ssw;
 };
 
 __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& mt, int& nt) {
@@ -177,16 +181,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = mt * kBM + ew * 32 + lane;
       const bool ok = row < p.M;
       std::int64_t obase = 0;
+      int hb = 0, wb = 0;
       if (ok) {
         std::uint32_t n, pix;
         p.fd_P.divmod(std::uint32_t(row), n, pix);
         obase = std::int64_t(n) * p.Nout * p.P + pix;
+        if (p.phase) {
+          std::uint32_t i, j;
+          p.fd_OW.divmod(pix, i, j);
+          obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
+          hb = int(i) * p.ssh - p.sph;
+          wb = int(j) * p.ssw - p.spw;
+        }
       }
       const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
         if (!ok) continue;
+        if (p.phase) {
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const int col = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || col >= p.Nout) break;
+            std::uint32_t ab, c, a, b;
+            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
+            p.fd_ssw.divmod(ab, a, b);
+            const int h = hb + int(a), w = wb + int(b);
+            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+            const float val = p.alpha * v[j];
+            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int col = nt * p.BN + c0 + j;
@@ -226,11 +254,46 @@ __global__ void to_nhwc_kernel(const float* __restrict__ src, float* __restrict_
   }
 }
 
+// Space-to-depth for strided Forward: x (NCHW) -> xs[n][i][j][Cp] with
+// channel cc = (a*Bw + b)*C + c holding x[n][c][i*sh + a - ph][j*sw + b - pw]
+// (0 off the image or for cc >= Ah*Bw*C). 32 x 32 smem transpose per block.
+struct S2D {
+  int C, H, W, sh, sw, ph, pw, Bw, CC, Hq, Wq, Cp;
+};
+__global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d) {
+  __shared__ float tile[32][33];
+  const int n = blockIdx.z / d.Hq, i = blockIdx.z - n * d.Hq;
+  const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int iy = threadIdx.y; iy < 32; iy += blockDim.y) {
+    const int cc = c0 + iy, j = j0 + threadIdx.x;
+    float v = 0.f;
+    if (cc < d.CC && j < d.Wq) {
+      const int ab = cc / d.C, c = cc - ab * d.C, a = ab / d.Bw, b = ab - a * d.Bw;
+      const int h = i * d.sh + a - d.ph, w = j * d.sw + b - d.pw;
+      if (unsigned(h) < unsigned(d.H) && unsigned(w) < unsigned(d.W))
+        v = __ldg(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W + w);
+    }
+    tile[iy][threadIdx.x] = v;
+  }
+  __syncthreads();
+  float* o = out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp;
+  for (int iy = threadIdx.y; iy < 32; iy += blockDim.y) {
+    const int j = j0 + iy, cc = c0 + threadIdx.x;
+    if (j < d.Wq && cc < d.Cp) o[std::int64_t(j) * d.Cp + cc] = tile[threadIdx.x][iy];
+  }
+}
+
 // Filter -> B tiles [n_tile][kstep][kgroup 8][BN][4]. Output channel o,
 // reduction (tap, ch). Forward: W[o][ch][tap]; flip_transpose (stride-1
-// BackwardData): W[ch][o][taps-1-tap] with rows o over C and ch over K.
+// BackwardData): W[ch][o][taps-1-tap] with rows o over C and ch over K;
+// phase (strided BackwardData): o = (a, b, c), tap = (t, u) of a Th x Tw
+// grid, ch = k -> W[k][c][a + (Th-1-t)*sh][b + (Tw-1-u)*sw] (0 off the filter).
+struct PhaseFilter {
+  int C, R, S, sh, sw, Tw;
+};
 __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int O, int I, int taps,
-                                   int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip) {
+                                   int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip,
+                                   PhaseFilter pf) {
   const std::int64_t total = std::int64_t(n_tiles) * ksteps * 8 * BN;  // 16-byte units
   for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
        u += std::int64_t(gridDim.x) * blockDim.x) {
@@ -253,8 +316,22 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
         ch = (k - tap * c_chunks) * 32 + g * 4 + e;
       }
       float x = 0.f;
-      if (o < O && ch < I && tap < taps)
-        x = flip ? w[(std::int64_t(ch) * O + o) * taps + (taps - 1 - tap)] : w[(std::int64_t(o) * I + ch) * taps + tap];
+      if (o < O && ch < I && tap < taps) {
+        if (flip == 3) {  // space-to-depth Forward: o = k, tap = (t, u), ch = (a, b, c)
+          const int ab = ch / pf.C, c = ch - ab * pf.C, a = ab / pf.sw, b = ab - a * pf.sw;
+          const int t = tap / pf.Tw, u = tap - t * pf.Tw;
+          const int r = t * pf.sh + a, q = u * pf.sw + b;
+          if (a < pf.sh && r < pf.R && q < pf.S) x = w[((std::int64_t(o) * pf.C + c) * pf.R + r) * pf.S + q];
+        } else if (flip == 2) {
+          const int ab = o / pf.C, c = o - ab * pf.C, a = ab / pf.sw, b = ab - a * pf.sw;
+          const int t = tap / pf.Tw, u = tap - t * pf.Tw, Th = taps / pf.Tw;
+          const int r = a + (Th - 1 - t) * pf.sh, q = b + (pf.Tw - 1 - u) * pf.sw;
+          if (r < pf.R && q < pf.S) x = w[((std::int64_t(ch) * pf.C + c) * pf.R + r) * pf.S + q];
+        } else {
+          x = flip ? w[(std::int64_t(ch) * O + o) * taps + (taps - 1 - tap)]
+                   : w[(std::int64_t(o) * I + ch) * taps + tap];
+        }
+      }
       v[e] = x;
     }
     reinterpret_cast<float4*>(out)[u] = make_float4(v[0], v[1], v[2], v[3]);
@@ -292,6 +369,12 @@ std::size_t align256(std::size_t b) { return (b + 255) / 256 * 256; }
 // channels) convolved to (Nout x Hout x Wout) by an R x S filter.
 struct Geo {
   int N, Cin, Hin, Win, Nout, Hout, Wout, R, S, ph, pw, sh, sw;
+  int ph_hi = -1, pw_hi = -1;  // high-side padding (default: = ph / pw)
+  int phase = 0;               // 1: strided BackwardData phase scatter
+  int s2d = 0;                 // 1: strided Forward on a space-to-depth copy
+  S2D sd{};
+  PhaseFilter pf{};
+  int Hr = 0, Wr = 0, rph = 0, rpw = 0;  // the real dx extent and conv padding
 };
 
 std::size_t geo_ws(const Geo& g, int* ksteps_out = nullptr, int* bn_out = nullptr) {
@@ -317,13 +400,19 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
                                              align256(std::size_t(n_tiles) * ksteps * BN * 128));
   const int HW = g.Hin * g.Win;
   count_launch();
-  to_nhwc_kernel<<<dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st>>>(act, act_nhwc, g.Cin, HW, Cp);
+  if (g.s2d) {
+    S2D d = g.sd;
+    d.Cp = Cp;
+    s2d_nhwc_kernel<<<dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st>>>(act, act_nhwc, d);
+  } else {
+    to_nhwc_kernel<<<dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st>>>(act, act_nhwc, g.Cin, HW, Cp);
+  }
   if (!(flags & kFilterReady)) {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     count_launch();
     pack_filter_kernel<<<blocks, 256, 0, st>>>(w, btiles, g.Nout, g.Cin, taps, BN, n_tiles, ksteps, Cp == 4 ? 1 : 0,
-                                               Cp / 32, flip);
+                                               Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -332,7 +421,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   const cuuint64_t dims[4] = {cuuint64_t(Cp), cuuint64_t(g.Win), cuuint64_t(g.Hin), cuuint64_t(g.N)};
   const cuuint64_t strides[3] = {cuuint64_t(Cp) * 4, cuuint64_t(Cp) * 4 * g.Win, cuuint64_t(Cp) * 4 * g.Win * g.Hin};
   const int lower[2] = {-g.pw, -g.ph};
-  const int upper[2] = {g.pw - (g.S - 1), g.ph - (g.R - 1)};
+  const int upper[2] = {(g.pw_hi < 0 ? g.pw : g.pw_hi) - (g.S - 1), (g.ph_hi < 0 ? g.ph : g.ph_hi) - (g.R - 1)};
   const cuuint32_t estr[4] = {1, cuuint32_t(g.sw), cuuint32_t(g.sh), 1};
   const bool small = Cp == 4;
   CUresult r = encode_im2col()(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, act_nhwc, dims, strides, lower, upper,
@@ -370,6 +459,18 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   p.fd_P = FastDiv(std::uint32_t(p.P));
   p.fd_OW = FastDiv(std::uint32_t(g.Wout));
   p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
+  p.phase = g.phase;
+  if (g.phase) {
+    p.Cr = g.pf.C;
+    p.Hr = g.Hr;
+    p.Wr = g.Wr;
+    p.ssh = g.pf.sh;
+    p.ssw = g.pf.sw;
+    p.sph = g.rph;
+    p.spw = g.rpw;
+    p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
+    p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
+  }
   const int stage_bytes = kBM * 128 + ((BN * 128 + 1023) & ~1023);
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)
@@ -389,30 +490,77 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
 Geo fwd_geo(const ConvShape& s) {
   return Geo{s.N, s.C, s.H, s.W, s.K, s.OH(), s.OW(), s.R, s.S, s.ph, s.pw, s.sh, s.sw};
 }
+// Strided Forward on a space-to-depth copy: with x_a[i] = x_pad[i*sh + a],
+// y[oh] = sum_{t, a} x_a[oh + t] * W[t*sh + a], a stride-1 conv over
+// Ah*Bw*C phase-channels with a Th x Tw filter (taps past R / S are zero).
+// Used when it shrinks the TMA work: few input channels (AlexNet conv1:
+// 3 -> 48 channels, 121 -> 9 taps) or 1x1 strided shortcuts.
+Geo fwd_s2d_geo(const ConvShape& s) {
+  const int Ah = std::min(s.sh, s.R), Bw = std::min(s.sw, s.S);
+  const int Th = (s.R + s.sh - 1) / s.sh, Tw = (s.S + s.sw - 1) / s.sw;
+  const int OH = s.OH(), OW = s.OW(), Hq = OH + Th - 1, Wq = OW + Tw - 1;
+  Geo g{s.N, Ah * Bw * s.C, Hq, Wq, s.K, OH, OW, Th, Tw, 0, 0, 1, 1};
+  g.s2d = 1;
+  g.pf = PhaseFilter{s.C, s.R, s.S, Bw, Bw, Tw};
+  g.pf.sh = s.sh;  // r = t*sh + a (a < Ah); Bw doubles as the channel-decode stride
+  g.sd = S2D{s.C, s.H, s.W, s.sh, s.sw, s.ph, s.pw, Bw, Ah * Bw * s.C, Hq, Wq, 0};
+  return g;
+}
+bool use_s2d(const ConvShape& s) { return (s.sh > 1 || s.sw > 1) && (s.C < 32 || (s.R == 1 && s.S == 1)); }
+Geo f_geo(const ConvShape& s) { return use_s2d(s) ? fwd_s2d_geo(s) : fwd_geo(s); }
 // stride-1 BackwardData as a forward conv of dy with the flipped filter
 Geo bwd_data_geo(const ConvShape& s) {
   return Geo{s.N, s.K, s.OH(), s.OW(), s.C, s.H, s.W, s.R, s.S, s.R - 1 - s.ph, s.S - 1 - s.pw, 1, 1};
 }
+// Strided BackwardData, split by output stride phase. In padded input
+// coordinates h' = h + ph = i*sh + a, dx_a[i] = sum_t sum_k dy[k][i - t] *
+// W[k][c][a + t*sh] (t < Th = ceil(R/sh)): every phase is a stride-1
+// correlation of dy with a Th x Tw sub-filter, so all sh*sw*C phase-channels
+// form ONE stride-1 forward conv (padding Th-1 low) whose epilogue scatters
+// column (a, b, c) of pixel (i, j) to dx[c][i*sh + a - ph][j*sw + b - pw].
+// Taps past the filter edge are zero in the packed filter.
+Geo bwd_data_phase_geo(const ConvShape& s) {
+  const int Th = (s.R + s.sh - 1) / s.sh, Tw = (s.S + s.sw - 1) / s.sw;
+  const int OH = s.OH(), OW = s.OW();
+  // cover every dx row: i up to (H - 1 + ph) / sh
+  const int Hq = std::max(OH + Th - 1, (s.H - 1 + s.ph) / s.sh + 1);
+  const int Wq = std::max(OW + Tw - 1, (s.W - 1 + s.pw) / s.sw + 1);
+  Geo g{s.N, s.K, OH, OW, s.sh * s.sw * s.C, Hq, Wq, Th, Tw, Th - 1, Tw - 1, 1, 1};
+  g.ph_hi = Hq - OH;
+  g.pw_hi = Wq - OW;
+  g.phase = 1;
+  g.pf = PhaseFilter{s.C, s.R, s.S, s.sh, s.sw, Tw};
+  g.Hr = s.H;
+  g.Wr = s.W;
+  g.rph = s.ph;
+  g.rpw = s.pw;
+  return g;
+}
+Geo bd_geo(const ConvShape& s) { return (s.sh == 1 && s.sw == 1) ? bwd_data_geo(s) : bwd_data_phase_geo(s); }
 
 }  // namespace
 
 bool precomp_supports(int op, const ConvShape& s) {
   if (op == kFwd) return s.sh <= 8 && s.sw <= 8 && s.ph <= 127 && s.pw <= 127 && s.R <= 64 && s.S <= 64;
-  if (op == kBwdData) return s.sh == 1 && s.sw == 1 && s.ph <= s.R - 1 && s.pw <= s.S - 1;
+  if (op == kBwdData) {
+    if (s.sh == 1 && s.sw == 1) return s.ph <= s.R - 1 && s.pw <= s.S - 1;
+    // phase split (any stride): sh*sw*C phase-channels, Th x Tw sub-filters
+    return s.sh <= 8 && s.sw <= 8 && s.ph <= s.R - 1 && s.pw <= s.S - 1 && s.R <= 64 && s.S <= 64;
+  }
   // BackwardFilter: TMA-tiled phase-split operands (bfilter.cu)
   return bf_supports(s);
 }
 
 std::int64_t precomp_workspace(int op, const ConvShape& s) {
-  if (op == kFwd) return std::int64_t(geo_ws(fwd_geo(s)));
-  if (op == kBwdData) return std::int64_t(geo_ws(bwd_data_geo(s)));
+  if (op == kFwd) return std::int64_t(geo_ws(f_geo(s)));
+  if (op == kBwdData) return std::int64_t(geo_ws(bd_geo(s)));
   return bf_workspace(s);
 }
 
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                         float beta, cudaStream_t st, int flags) {
-  if (op == kFwd) return run_geo(fwd_geo(s), a, b, 0, out, ws, alpha, beta, st, flags);
-  if (op == kBwdData) return run_geo(bwd_data_geo(s), a, b, 1, out, ws, alpha, beta, st, flags);
+  if (op == kFwd) return run_geo(f_geo(s), a, b, 0, out, ws, alpha, beta, st, flags);
+  if (op == kBwdData) return run_geo(bd_geo(s), a, b, 1, out, ws, alpha, beta, st, flags);
   return bf_run(s, a, b, out, ws, alpha, beta, st);
 }
 

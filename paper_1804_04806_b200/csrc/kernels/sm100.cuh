@@ -27,11 +27,14 @@ __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t
                "r"(bytes)
                : "memory");
 }
+// Spin on try_wait without a suspend-time hint: a hinted wait parks the warp
+// (NANOSLEEP.SYNCS) and its wake-up latency was a fixed ~1 us per pipeline
+// step in the first profiles.
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");

@@ -53,7 +53,10 @@ using namespace sm100;
 namespace {
 
 constexpr int kBM = 128;
+// ring depth that splits evenly over 3 or 2 producer threads
+inline int ring_stages(int fit) { return fit > 8 ? 8 : fit < 2 ? 2 : fit; }
 constexpr int kMaxStages = 8;
+constexpr int kSub = 1;  // 32-pixel reduction chunks per stage (2 measured slower here)
 constexpr int kThreads = 256;
 constexpr int kMaxBN = 256;
 
@@ -140,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = std::uint32_t(p.BN) * 128;
-  const std::uint32_t stage_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const std::uint32_t stage_bytes = kSub * sub_bytes;
   const int kStages = p.stages;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
   std::uint64_t* empty = full + kMaxStages;
@@ -168,7 +172,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem = *tmem_slot;
   const int units = p.tiles * p.splits;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // up to three producer threads, stage s owned by thread s % 3 (one
+    // thread's TMA issue stream keeps only about one stage in flight:
+    // scripts/tma_probe.cu). Fixed ownership keeps every stage's parity
+    // waits in order, so no producer can run two rounds ahead on a stage.
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       const int boxes = kBM / p.Gb;
@@ -177,28 +187,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tile = u % p.tiles, split = u / p.tiles;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-        int n = g0 / p.Lc, ch = g0 - n * p.Lc;
-        for (int g = g0; g < g1; ++g, ++it) {
-          const int st = it % kStages;
+        for (int g = g0; g < g1; g += kSub, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
+          const int st = it % kStages, nsub = min(kSub, g1 - g);
           mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
-          unsigned char* sa = smem + st * stage_bytes;
-          mbar_expect_tx(&full[st], a_bytes + b_bytes);
-          const int j0 = ch * 32;
+          mbar_expect_tx(&full[st], nsub * (a_bytes + b_bytes));
+          for (int sub = 0; sub < nsub; ++sub) {
+            unsigned char* sa = smem + st * stage_bytes + sub * sub_bytes;
+            const int n = (g + sub) / p.Lc, j0 = ((g + sub) - n * p.Lc) * 32;
 #pragma unroll 1
-          for (int bx = 0; bx < boxes; ++bx) {
-            const int row0 = mt * kBM + bx * p.Gb;
-            const int q = row0 / p.CCp, cc0 = row0 - q * p.CCp;
-            const int qh = q / p.Qw, qw = q - qh * p.Qw;
-            // rows past M: an out-of-range channel coordinate makes TMA zero-fill the box
-            // TMA wants the innermost start coordinate 16-byte aligned: the
-            // misaligned part of the tap offset selects a pre-shifted replica
-            const int o = j0 + qh * p.Wq + qw;
-            tma_4d(sa + bx * (p.Gb * 128), &xmap, &full[st], o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
-          }
-          tma_4d(sa + a_bytes, &dmap, &full[st], j0, nt * p.BN, n, 0);
-          if (++ch == p.Lc) {
-            ch = 0;
-            ++n;
+            for (int bx = 0; bx < boxes; ++bx) {
+              const int row0 = mt * kBM + bx * p.Gb;
+              const int q = row0 / p.CCp, cc0 = row0 - q * p.CCp;
+              const int qh = q / p.Qw, qw = q - qh * p.Qw;
+              // rows past M: an out-of-range channel coordinate makes TMA
+              // zero-fill the box. TMA wants the innermost start coordinate
+              // 16-byte aligned: the misaligned part of the tap offset
+              // selects a pre-shifted replica.
+              const int o = j0 + qh * p.Wq + qw;
+              tma_4d(sa + bx * (p.Gb * 128), &xmap, &full[st], o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
+            }
+            tma_4d(sa + a_bytes, &dmap, &full[st], j0, nt * p.BN, n, 0);
           }
         }
       }
@@ -216,18 +225,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
       tc_fence_after();
       const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
-      for (int g = g0; g < g1; ++g, ++it) {
-        const int st = it % kStages;
+      for (int g = g0; g < g1; g += kSub, ++it) {
+        const int st = it % kStages, nsub = min(kSub, g1 - g);
         mbar_wait(&full[st], (it / kStages) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+          for (int sub = 0; sub < nsub; ++sub) {
+            const std::uint32_t sa = sbase + st * stage_bytes + sub * sub_bytes, sb = sa + a_bytes;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            mma_tf32(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
-                     (g != g0 || q != 0) ? 1u : 0u);
+            for (int q = 0; q < 4; ++q)
+              mma_tf32(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
+                       (g + sub != g0 || q != 0) ? 1u : 0u);
+          }
           mma_commit(&empty[st]);
-          if (g == g1 - 1) mma_commit(&tfull[acc]);
+          if (g + kSub >= g1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
       }
@@ -446,10 +457,10 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   p.steps = g.N * g.Lc;
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   int splits = std::max(1, std::min(p.steps / 8, sms / p.tiles));
-  p.steps_per_unit = (p.steps + splits - 1) / splits;
+  p.steps_per_unit = ((p.steps + splits - 1) / splits + kSub - 1) / kSub * kSub;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
-  const int stage_bytes = kBM * 128 + ((g.BN * 128 + 1023) & ~1023);
-  p.stages = std::min(kMaxStages, (200 * 1024) / stage_bytes);
+  const int stage_bytes = kSub * (kBM * 128 + ((g.BN * 128 + 1023) & ~1023));
+  p.stages = ring_stages((200 * 1024) / stage_bytes);
   const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
   static bool attr = false;
   if (!attr) {

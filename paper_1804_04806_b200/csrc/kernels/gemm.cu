@@ -178,7 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
   const std::uint32_t tmem = *tmem_slot;
   const int tiles = p.m_tiles * p.n_tiles, units = tiles * p.splits;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // up to three producer threads, stage s owned by thread s % 3 (one
+    // thread's TMA issue stream keeps only about one stage in flight:
+    // scripts/tma_probe.cu). Fixed ownership keeps every stage's parity
+    // waits in order, so no producer can run two rounds ahead on a stage.
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -188,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
         const float* ab = p.a + (std::size_t(mt) * p.ksteps) * (a_bytes / 4);
         const float* bb = p.b + (std::size_t(nt) * p.ksteps) * (b_bytes / 4);
         for (int k = k0; k < k1; ++k, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           unsigned char* sa = smem + s * stage_bytes;

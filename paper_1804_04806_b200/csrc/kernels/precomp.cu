@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "bfilter.h"
@@ -38,7 +39,12 @@ using namespace sm100;
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kStages = 4;
+// ring depth that splits evenly over 3 or 2 producer threads
+inline int ring_stages(int fit) { return fit > 8 ? 8 : fit < 2 ? 2 : fit; }
+constexpr int kMaxStages = 8;
+// 32-deep reduction chunks per pipeline stage: a tcgen05.commit costs
+// several hundred cycles of issue time, so each commit covers 8 MMAs
+// (scripts/mma_probe.cu)
 constexpr int kThreads = 256;
 constexpr int kMaxBN = 256;
 
@@ -57,6 +63,7 @@ struct PrecompParams {
   // phase scatter epilogue (strided BackwardData): column (a, b, c) of
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  int stages, ksub;
   FastDiv fd_Cr, fd_ssw;
 };
 
@@ -75,10 +82,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = std::uint32_t(p.BN) * 128;
-  const std::uint32_t stage_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int kSub = p.ksub;
+  const std::uint32_t stage_bytes = kSub * sub_bytes;
+  const int kStages = p.stages;
+  const int jsteps = (p.ksteps + kSub - 1) / kSub;  // pipeline stages per tile
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
-  std::uint64_t* empty = full + kStages;
-  std::uint64_t* tfull = empty + kStages;
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
   std::uint64_t* tempty = tfull + 2;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
 
@@ -101,7 +112,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem = *tmem_slot;
   const int total_tiles = p.m_tiles * p.n_tiles;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // up to three producer threads, stage s owned by thread s % 3 (one
+    // thread's TMA issue stream keeps only about one stage in flight:
+    // scripts/tma_probe.cu). Fixed ownership keeps every stage's parity
+    // waits in order, so no producer can run two rounds ahead on a stage.
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
     if (lane == 0) {
       // ------------------------------------------------ producer
       int it = 0;
@@ -114,26 +131,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.fd_OW.divmod(pix, oh, ow);
         const int cw = int(ow) * p.sw - p.pw, ch = int(oh) * p.sh - p.ph;
         const float* bsrc = p.btiles + std::size_t(nt) * p.ksteps * (b_bytes / 4);
-        for (int k = 0; k < p.ksteps; ++k, ++it) {
+        for (int j = 0; j < jsteps; ++j, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-          unsigned char* sa = smem + s * stage_bytes;
-          mbar_expect_tx(&full[s], a_bytes + b_bytes);
-          if (p.small_c) {
+          const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
+          mbar_expect_tx(&full[s], nsub * (a_bytes + b_bytes));
+          for (int sub = 0; sub < nsub; ++sub) {
+            const int k = k0 + sub;
+            unsigned char* sa = smem + s * stage_bytes + sub * sub_bytes;
+            if (p.small_c) {
 #pragma unroll 1
-            for (int g = 0; g < 8; ++g) {
-              int tap = k * 8 + g;
-              if (tap >= p.taps) tap = p.taps - 1;  // its B rows are zero
+              for (int g = 0; g < 8; ++g) {
+                int tap = k * 8 + g;
+                if (tap >= p.taps) tap = p.taps - 1;  // its B rows are zero
+                const int r = tap / p.S, q = tap - r * p.S;
+                tma_im2col_4d(sa + g * (kBM * 16), &amap, &full[s], 0, cw, ch, int(n), (unsigned short)q,
+                              (unsigned short)r);
+              }
+            } else {
+              const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
               const int r = tap / p.S, q = tap - r * p.S;
-              tma_im2col_4d(sa + g * (kBM * 16), &amap, &full[s], 0, cw, ch, int(n), (unsigned short)q,
-                            (unsigned short)r);
+              tma_im2col_4d(sa, &amap, &full[s], cc * 32, cw, ch, int(n), (unsigned short)q, (unsigned short)r);
             }
-          } else {
-            const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
-            const int r = tap / p.S, q = tap - r * p.S;
-            tma_im2col_4d(sa, &amap, &full[s], cc * 32, cw, ch, int(n), (unsigned short)q, (unsigned short)r);
+            bulk_g2s(sa + a_bytes, bsrc + std::size_t(k) * (b_bytes / 4), b_bytes, &full[s]);
           }
-          bulk_g2s(sa + a_bytes, bsrc + std::size_t(k) * (b_bytes / 4), b_bytes, &full[s]);
         }
       }
     }
@@ -142,28 +164,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ MMA issuer
     const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
     const std::uint32_t sbase = smem_u32(smem);
-    const std::uint32_t lbo_b = std::uint32_t(p.BN) * 16;
     int it = 0, tl = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       const int acc = tl & 1;
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
       tc_fence_after();
       const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
-      for (int k = 0; k < p.ksteps; ++k, ++it) {
+      for (int j = 0; j < jsteps; ++j, ++it) {
         const int s = it % kStages;
         mbar_wait(&full[s], (it / kStages) & 1);
         tc_fence_after();
+        const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
         if (lane == 0) {
-          const std::uint32_t sa = sbase + s * stage_bytes, sb = sa + a_bytes;
+          for (int sub = 0; sub < nsub; ++sub) {
+            const std::uint32_t sa = sbase + s * stage_bytes + sub * sub_bytes, sb = sa + a_bytes;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            std::uint64_t ad = p.small_c ? umma_desc(sa + 2 * q * (kBM * 16), kBM * 16, 128)
-                                         : umma_desc_sw128(sa + q * 32);
-            std::uint64_t bd = umma_desc(sb + 2 * q * lbo_b, lbo_b, 128);
-            mma_tf32(dtm, ad, bd, idesc, (k | q) != 0);
+            for (int q = 0; q < 4; ++q) {
+              std::uint64_t ad = p.small_c ? umma_desc(sa + 2 * q * (kBM * 16), kBM * 16, 128)
+                                           : umma_desc_sw128(sa + q * 32);
+              std::uint64_t bd = umma_desc_sw128(sb + q * 32);
+              mma_tf32(dtm, ad, bd, idesc, ((k0 + sub) | q) != 0);
+            }
           }
           mma_commit(&empty[s]);
-          if (k == p.ksteps - 1) mma_commit(&tfull[acc]);
+          if (j == jsteps - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
       }
@@ -283,7 +307,7 @@ __global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__
   }
 }
 
-// Filter -> B tiles [n_tile][kstep][kgroup 8][BN][4]. Output channel o,
+// Filter -> B tiles [n_tile][kstep][BN rows][32 floats, SWIZZLE_128B]. Output channel o,
 // reduction (tap, ch). Forward: W[o][ch][tap]; flip_transpose (stride-1
 // BackwardData): W[ch][o][taps-1-tap] with rows o over C and ch over K;
 // phase (strided BackwardData): o = (a, b, c), tap = (t, u) of a Th x Tw
@@ -334,7 +358,10 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
       }
       v[e] = x;
     }
-    reinterpret_cast<float4*>(out)[u] = make_float4(v[0], v[1], v[2], v[3]);
+    // SWIZZLE_128B K-major block: row `row` holds its 8 16-byte chunks at
+    // positions g ^ (row & 7) (the pattern TMA writes and UMMA reads)
+    const std::int64_t blk = u / (8 * BN);
+    reinterpret_cast<float4*>(out)[blk * 8 * BN + row * 8 + (g ^ (row & 7))] = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -471,10 +498,14 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
     p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
   }
-  const int stage_bytes = kBM * 128 + ((BN * 128 + 1023) & ~1023);
+  // two 32-deep chunks per stage (8 MMAs per tcgen05.commit): measured
+  // 10-25 % faster than one on AlexNet conv2 / conv4 (same box, A/B)
+  p.ksub = 2;
+  const int stage_bytes = p.ksub * (kBM * 128 + ((BN * 128 + 1023) & ~1023));
+  p.stages = ring_stages((200 * 1024) / stage_bytes);
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)
-  const int smem = std::max(kStages * stage_bytes + 1024 + 256, 116 * 1024);
+  const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
   static int smem_set = 0;
   if (smem > smem_set) {
     e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

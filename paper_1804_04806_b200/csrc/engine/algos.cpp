@@ -5,6 +5,7 @@
 #include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
 #include "../kernels/precomp.h"
+#include "../kernels/winograd.h"
 
 namespace ucudnn {
 
@@ -29,7 +30,22 @@ cudaError_t igemm_run(int op, const ConvShape& s, const float* a, const float* b
   return cudaErrorInvalidValue;
 }
 
+bool wino2_supports(int op, const ConvShape& s) { return winograd_supports(2, op, s); }
+std::int64_t wino2_workspace(int op, const ConvShape& s) { return winograd_workspace(2, op, s); }
+cudaError_t wino2_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
+                      float beta, cudaStream_t st, int flags) {
+  return winograd_run(2, op, s, a, b, out, ws, alpha, beta, st, flags);
+}
+bool wino4_supports(int op, const ConvShape& s) { return winograd_supports(4, op, s); }
+std::int64_t wino4_workspace(int op, const ConvShape& s) { return winograd_workspace(4, op, s); }
+cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
+                      float beta, cudaStream_t st, int flags) {
+  return winograd_run(4, op, s, a, b, out, ws, alpha, beta, st, flags);
+}
+
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
+const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
+const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
 const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 
@@ -38,6 +54,8 @@ const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_wo
 const AlgoImpl* find_algo(int id) {
   switch (id) {
     case 0: return &kImplicitGemm;
+    case 1: return &kWinograd;
+    case 4: return &kWinograd4;
     case 3: return &kGemm;
     case 5: return &kPrecomp;
     default: return nullptr;

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackParams p) {
 }
 
 // ------------------------------------------------------------------ GEMM
-enum Epilogue : int { kEpiNchw = 0, kEpiRowMajor = 1, kEpiAtomicT = 2 };
+enum Epilogue : int { kEpiNchw = 0, kEpiRowMajor = 1, kEpiAtomicT = 2, kEpiColMajor = 3 };
 
 struct GemmParams {
   const float* a;  // [m_tile][kstep] blocks of 128 x 32
@@ -146,6 +146,8 @@ struct GemmParams {
   int m_tiles, n_tiles, ksteps, BN, splits, steps_per_unit;
   int epi, M, Nc, P, ld;
   FastDiv fd_P;
+  int batch;                            // independent GEMMs (Winograd points)
+  std::int64_t a_bs, b_bs, o_bs;        // their element strides
 };
 
 __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParams p) {
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
-  const int tiles = p.m_tiles * p.n_tiles, units = tiles * p.splits;
+  const int tiles = p.m_tiles * p.n_tiles, per_batch = tiles * p.splits, units = per_batch * p.batch;
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // up to three producer threads, stage s owned by thread s % 3 (one
@@ -188,11 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int tile = u % tiles, split = u / tiles;
+        const int bi = u / per_batch, ur = u - bi * per_batch;
+        const int tile = ur % tiles, split = ur / tiles;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int k0 = split * p.steps_per_unit, k1 = min(p.ksteps, k0 + p.steps_per_unit);
-        const float* ab = p.a + (std::size_t(mt) * p.ksteps) * (a_bytes / 4);
-        const float* bb = p.b + (std::size_t(nt) * p.ksteps) * (b_bytes / 4);
+        const float* ab = p.a + bi * p.a_bs + (std::size_t(mt) * p.ksteps) * (a_bytes / 4);
+        const float* bb = p.b + bi * p.b_bs + (std::size_t(nt) * p.ksteps) * (b_bytes / 4);
         for (int k = k0; k < k1; ++k, ++it) {
           if ((it % kStages) % nprod != pq) continue;
           const int s = it % kStages;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
     const std::uint32_t sbase = smem_u32(smem), lbo_b = std::uint32_t(p.BN) * 16;
     int it = 0, tl = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
-      const int split = u / tiles;
+      const int split = (u % per_batch) / tiles;
       const int k0 = split * p.steps_per_unit, k1 = min(p.ksteps, k0 + p.steps_per_unit);
       const int acc = tl & 1;
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
@@ -237,8 +240,10 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
     const int ew = warp - 4;
     int tl = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
-      const int tile = u % tiles, split = u / tiles;
+      const int bi = u / per_batch, ur = u - bi * per_batch;
+      const int tile = ur % tiles, split = ur / tiles;
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      float* const out = p.out + bi * p.o_bs;
       const int k0 = split * p.steps_per_unit, k1 = min(p.ksteps, k0 + p.steps_per_unit);
       const int acc = tl & 1;
       mbar_wait(&tfull[acc], (tl >> 1) & 1);
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
         if (!ok) continue;
         const int col0 = nt * p.BN + c0;
         if (p.epi == kEpiRowMajor && col0 + 32 <= p.Nc && c0 + 32 <= p.BN && (p.ld & 3) == 0) {
-          float4* dst = reinterpret_cast<float4*>(p.out + std::int64_t(row) * p.ld + col0);
+          float4* dst = reinterpret_cast<float4*>(out + std::int64_t(row) * p.ld + col0);
 #pragma unroll
           for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           continue;
@@ -268,13 +273,15 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
           const int col = col0 + j;
           if (c0 + j >= p.BN || col >= p.Nc) break;
           if (p.epi == kEpiNchw) {
-            float* dst = p.out + obase + std::int64_t(col) * p.P;
+            float* dst = out + obase + std::int64_t(col) * p.P;
             const float val = p.alpha * v[j];
             *dst = p.beta == 0.f ? val : val + p.beta * *dst;
           } else if (p.epi == kEpiRowMajor) {
-            p.out[std::int64_t(row) * p.ld + col] = v[j];
+            out[std::int64_t(row) * p.ld + col] = v[j];
+          } else if (p.epi == kEpiColMajor) {
+            out[std::int64_t(col) * p.ld + row] = v[j];
           } else {
-            red_add(p.out + std::int64_t(col) * p.ld + row, p.alpha * v[j]);
+            red_add(out + std::int64_t(col) * p.ld + row, p.alpha * v[j]);
           }
         }
       }
@@ -401,7 +408,8 @@ cudaError_t pack(const PackParams& p, cudaStream_t st) {
 }
 
 cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, float* out, float alpha, float beta,
-                 int P, int ld, bool split_k, cudaStream_t st) {
+                 int P, int ld, bool split_k, cudaStream_t st, int batch = 1, std::int64_t a_bs = 0,
+                 std::int64_t b_bs = 0, std::int64_t o_bs = 0) {
   GemmParams g{};
   g.a = a;
   g.b = b;
@@ -423,6 +431,10 @@ cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, floa
   g.P = P;
   g.ld = ld;
   g.fd_P = FastDiv(std::uint32_t(P > 0 ? P : 1));
+  g.batch = batch;
+  g.a_bs = a_bs;
+  g.b_bs = b_bs;
+  g.o_bs = o_bs;
   const int stage = kBM * 128 + ((q.BN * 128 + 127) & ~127);
   const int smem = std::max(kStages * stage + 1024 + 256, 116 * 1024);
   static int smem_set = 0;
@@ -432,11 +444,18 @@ cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, floa
     smem_set = 227 * 1024;
   }
   count_launch();
-  tiled_gemm_kernel<<<std::min(sms(), tiles * g.splits), kThreads, smem, st>>>(g);
+  tiled_gemm_kernel<<<std::min(std::int64_t(sms()), std::int64_t(tiles) * g.splits * batch), kThreads, smem, st>>>(g);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+int blocked_bn(int n) { return pick_bn(n); }
+
+cudaError_t batched_gemm_colmajor(int batch, int M, int Nc, int Kr, const float* a, std::int64_t a_bs, const float* b,
+                                  std::int64_t b_bs, float* out, std::int64_t o_bs, int ld, cudaStream_t st) {
+  return gemm(make_problem(M, Nc, Kr), a, b, kEpiColMajor, out, 1.f, 0.f, 0, ld, false, st, batch, a_bs, b_bs, o_bs);
+}
 
 bool gemm_supports(int, const ConvShape& s) {
   return std::int64_t(s.N) * s.OH() * s.OW() < (std::int64_t(1) << 31) && s.x_elems() < (std::int64_t(1) << 31);

@@ -27,7 +27,12 @@ SHAPES = [
     ConvShape(2, 40, 6, 6, 300, 3, 3, 1, 1, 1, 1),        # ragged tiles
     ConvShape(3, 64, 7, 7, 64, 3, 3, 1, 1, 1, 1),         # ResNet l4-like spatial size
 ]
-ALGOS = [0, 3, 5]
+ALGOS = [0, 1, 3, 4, 5]
+# F(4x4,3x3) carries 1/6 and 1/24 in G: not exact in TF32 even on integer data,
+# and its transforms amplify TF32 rounding (measured ~3.3e-3 normwise on
+# Gaussian data), so it gets a 1e-2 bound instead of the GEMM-class 3e-3.
+INEXACT = {4}
+TOL = {4: 1e-2}
 
 
 def _sid(s):
@@ -55,6 +60,9 @@ def test_integer_bit_exact(cuda, algo, op, s):
     a, b = inputs_for(op, s, rng, integer=True)
     got = run_algo(Handle(), op, s, a, b, cuda, algo)
     ref = conv_ref(op, s, a, b)
+    if algo in INEXACT:
+        assert np.linalg.norm(got - ref) <= TOL[algo] * np.linalg.norm(ref)
+        return
     assert np.array_equal(got, ref), f"max abs diff {np.abs(got - ref).max()}"
 
 
@@ -67,7 +75,7 @@ def test_gaussian_tf32_tolerance(cuda, algo, op, s):
     got = run_algo(Handle(), op, s, a, b, cuda, algo)
     ref = conv_ref(op, s, a, b)
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
-    assert err <= 3e-3, err
+    assert err <= TOL.get(algo, 3e-3), err
 
 
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
@@ -79,4 +87,7 @@ def test_alpha_beta(cuda, algo, op):
     init = np.random.default_rng(4).integers(-3, 4, size=out_shape(op, s)).astype(np.float64)
     got = run_algo(Handle(), op, s, a, b, cuda, algo, alpha=2.0, beta=-1.0, init=init)
     ref = 2.0 * conv_ref(op, s, a, b) - init
+    if algo in INEXACT:
+        assert np.linalg.norm(got - ref) <= TOL[algo] * np.linalg.norm(ref)
+        return
     assert np.array_equal(got, ref)

@@ -2,6 +2,7 @@
 
 #include <atomic>
 
+#include "../kernels/fft.h"
 #include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
 #include "../kernels/precomp.h"
@@ -46,6 +47,7 @@ cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
 const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
 const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
+const AlgoImpl kFft{2, "FFT", fft_supports, fft_workspace, fft_run};
 const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 
@@ -55,6 +57,7 @@ const AlgoImpl* find_algo(int id) {
   switch (id) {
     case 0: return &kImplicitGemm;
     case 1: return &kWinograd;
+    case 2: return &kFft;
     case 4: return &kWinograd4;
     case 3: return &kGemm;
     case 5: return &kPrecomp;

@@ -1,6 +1,8 @@
 #include "algos.h"
 
 #include <atomic>
+#include <cstdlib>
+#include <string>
 
 #include "../kernels/fft.h"
 #include "../kernels/gemm.h"
@@ -15,6 +17,20 @@ std::atomic<std::uint64_t> g_launches{0};
 }  // namespace
 void count_launch(int n) { g_launches.fetch_add(std::uint64_t(n), std::memory_order_relaxed); }
 std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int tune(const char* key, int dflt) {
+  static const std::string env = [] {
+    const char* e = std::getenv("UCUDNN_TUNE");
+    return std::string(e ? e : "");
+  }();
+  const std::string k = std::string(key) + "=";
+  std::size_t pos = 0;
+  while ((pos = env.find(k, pos)) != std::string::npos) {
+    if (pos == 0 || env[pos - 1] == ',') return std::atoi(env.c_str() + pos + k.size());
+    pos += k.size();
+  }
+  return dflt;
+}
 
 namespace {
 

@@ -56,7 +56,7 @@ constexpr int kBM = 128;
 // ring depth that splits evenly over 3 or 2 producer threads
 inline int ring_stages(int fit) { return fit > 8 ? 8 : fit < 2 ? 2 : fit; }
 constexpr int kMaxStages = 8;
-constexpr int kSub = 1;  // 32-pixel reduction chunks per stage (2 measured slower here)
+constexpr int kMaxSub = 2;  // 32-pixel reduction chunks per stage
 constexpr int kThreads = 256;
 constexpr int kMaxBN = 256;
 
@@ -69,6 +69,8 @@ struct BfGeo {
   int Ld, Ldp;         // dy_p plane: OH*Wq and its padded length
   int Lc;              // 32-pixel reduction steps per image
   int M, BN, m_tiles, n_tiles;
+  int swap;            // 1: MMA rows = output channels k (K <= 128), columns = (q, cc) rows
+  int Kb;              // swap: dy box rows (K rounded to 8; MMA rows past it are never read)
 };
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
@@ -109,6 +111,18 @@ BfGeo make_geo(const ConvShape& s) {
   g.Ldp = round_up(g.Ld, 4);
   g.Lc = (g.Ld + 31) / 32;
   g.M = g.Qh * g.Qw * g.CCp;
+  // Few output channels (AlexNet conv1, ResNet stage 1: K = 64): an N = 64
+  // MMA is issue-bound, so swap roles -- MMA rows are the K channels (one
+  // 128-row tile, zero-filled past K) and the (q, cc) rows become N <= 256.
+  g.swap = s.K <= 128 && g.M > 128;
+  if (g.swap) {
+    g.n_tiles = (g.M + kMaxBN - 1) / kMaxBN;
+    g.BN = round_up((g.M + g.n_tiles - 1) / g.n_tiles, std::max(g.Gb, 16));
+    g.n_tiles = (g.M + g.BN - 1) / g.BN;
+    g.m_tiles = 1;
+    g.Kb = round_up(s.K, 8);
+    return g;
+  }
   const int nt = (s.K + kMaxBN - 1) / kMaxBN;
   g.BN = round_up((s.K + nt - 1) / nt, 16);
   g.n_tiles = (s.K + g.BN - 1) / g.BN;
@@ -124,8 +138,20 @@ struct BfParams {
   float* dw;
   float alpha;
   int K, CRS, RS, S, R, C, Bw, Ah, sh, sw, Qw, CCp, CC, Gb, Wq, M, BN;
-  int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages;
+  int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages, swap, Kb, ksub;
 };
+
+// GEMM row (qh, qw, cc) of the x operand -> dW offset (c, r, s), or -1
+__device__ __forceinline__ int x_row_off(const BfParams& p, int row) {
+  if (row >= p.M) return -1;
+  const int q = row / p.CCp, cc = row - q * p.CCp;
+  const int qh = q / p.Qw, qw = q - qh * p.Qw;
+  if (cc >= p.CC) return -1;
+  const int ab = cc / p.C, c = cc - ab * p.C;
+  const int a = ab / p.Bw, b = ab - a * p.Bw;
+  const int r = qh * p.sh + a, s = qw * p.sw + b;
+  return (r < p.R && s < p.S) ? c * p.RS + r * p.S + s : -1;
+}
 
 __device__ __forceinline__ void tma_4d(void* dst, const void* tmap, std::uint64_t* bar, int x, int y, int z, int w) {
   asm volatile(
@@ -144,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = std::uint32_t(p.BN) * 128;
   const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int kSub = p.ksub;
   const std::uint32_t stage_bytes = kSub * sub_bytes;
   const int kStages = p.stages;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
@@ -191,13 +218,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((it % kStages) % nprod != pq) continue;
           const int st = it % kStages, nsub = min(kSub, g1 - g);
           mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&full[st], nsub * (a_bytes + b_bytes));
+          mbar_expect_tx(&full[st], nsub * ((p.swap ? std::uint32_t(p.Kb) * 128 : a_bytes) + b_bytes));
           for (int sub = 0; sub < nsub; ++sub) {
             unsigned char* sa = smem + st * stage_bytes + sub * sub_bytes;
             const int n = (g + sub) / p.Lc, j0 = ((g + sub) - n * p.Lc) * 32;
+            // swap: A = the dy box (K rows), B = the x boxes of column tile nt
+            unsigned char* xa = p.swap ? sa + a_bytes : sa;
+            const int xrow0 = p.swap ? nt * p.BN : mt * kBM;
+            const int nbox = p.swap ? p.BN / p.Gb : boxes;
 #pragma unroll 1
-            for (int bx = 0; bx < boxes; ++bx) {
-              const int row0 = mt * kBM + bx * p.Gb;
+            for (int bx = 0; bx < nbox; ++bx) {
+              const int row0 = xrow0 + bx * p.Gb;
               const int q = row0 / p.CCp, cc0 = row0 - q * p.CCp;
               const int qh = q / p.Qw, qw = q - qh * p.Qw;
               // rows past M: an out-of-range channel coordinate makes TMA
@@ -205,9 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               // 16-byte aligned: the misaligned part of the tap offset
               // selects a pre-shifted replica.
               const int o = j0 + qh * p.Wq + qw;
-              tma_4d(sa + bx * (p.Gb * 128), &xmap, &full[st], o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
+              tma_4d(xa + bx * (p.Gb * 128), &xmap, &full[st], o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
             }
-            tma_4d(sa + a_bytes, &dmap, &full[st], j0, nt * p.BN, n, 0);
+            if (p.swap) tma_4d(sa, &dmap, &full[st], j0, 0, n, 0);
+            else tma_4d(sa + a_bytes, &dmap, &full[st], j0, nt * p.BN, n, 0);
           }
         }
       }
@@ -247,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue: RED into dW
+    __shared__ int offtab[kMaxBN];
     const int ew = warp - 4;
     int tl = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
@@ -256,29 +289,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = tl & 1;
       mbar_wait(&tfull[acc], (tl >> 1) & 1);
       tc_fence_after();
-      // this thread's GEMM row -> dW offset (c, r, s), or invalid
-      const int row = mt * kBM + ew * 32 + lane;
-      int off = -1;
-      if (row < p.M && g1 > g0) {
-        const int q = row / p.CCp, cc = row - q * p.CCp;
-        const int qh = q / p.Qw, qw = q - qh * p.Qw;
-        if (cc < p.CC) {
-          const int ab = cc / p.C, c = cc - ab * p.C;
-          const int a = ab / p.Bw, b = ab - a * p.Bw;
-          const int r = qh * p.sh + a, s = qw * p.sw + b;
-          if (r < p.R && s < p.S) off = c * p.RS + r * p.S + s;
-        }
-      }
       const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tbase + std::uint32_t(c0), v);
-        if (off < 0) continue;
+      if (p.swap) {
+        // TMEM lane = output channel k, column = x row of tile nt
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous unit done with offtab
+        for (int j = ew * 32 + lane; j < p.BN; j += 128) offtab[j] = x_row_off(p, nt * p.BN + j);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int k = ew * 32 + lane;
+        const bool live = k < p.K && g1 > g0;
+        float* dwk = p.dw + std::int64_t(k) * p.CRS;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int k = nt * p.BN + c0 + j;
-          if (c0 + j >= p.BN || k >= p.K) break;
-          red_add(p.dw + std::int64_t(k) * p.CRS + off, p.alpha * v[j]);
+          for (int j = 0; j < 32; ++j) {
+            if (c0 + j >= p.BN) break;
+            const int off = offtab[c0 + j];
+            if (off >= 0) red_add(dwk + off, p.alpha * v[j]);
+          }
+        }
+      } else {
+        // this thread's GEMM row -> dW offset (c, r, s), or invalid
+        const int row = mt * kBM + ew * 32 + lane;
+        const int off = g1 > g0 ? x_row_off(p, row) : -1;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (off < 0) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || k >= p.K) break;
+            red_add(p.dw + std::int64_t(k) * p.CRS + off, p.alpha * v[j]);
+          }
         }
       }
       tc_fence_before();
@@ -439,7 +483,7 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   if (!encode_4d(&xmap, xph, g.Lq, g.CC, g.N, g.T, g.Lp, std::int64_t(g.CC) * g.Lp, rep, 32, g.Gb))
     return cudaErrorInvalidValue;
   if (!encode_4d(&dmap, dyp, g.Ld, g.K, g.N, 1, g.Ldp, std::int64_t(g.K) * g.Ldp, std::int64_t(g.N) * g.K * g.Ldp, 32,
-                 g.BN))
+                 g.swap ? g.Kb : g.BN))
     return cudaErrorInvalidValue;
 
   BfParams p{};
@@ -454,17 +498,21 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   p.tiles = g.m_tiles * g.n_tiles;
   p.Lc = g.Lc;
   p.T = g.T;
+  p.swap = g.swap;
+  p.Kb = g.Kb;
   p.steps = g.N * g.Lc;
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
-  int splits = std::max(1, std::min(p.steps / 8, sms / p.tiles));
+  int splits = std::max(1, std::min(p.steps / 8, tune("bf_waves", 1) * sms / p.tiles));
+  p.ksub = std::max(1, std::min(kMaxSub, tune("bf_ksub", 1)));
+  const int kSub = p.ksub;
   p.steps_per_unit = ((p.steps + splits - 1) / splits + kSub - 1) / kSub * kSub;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
   const int stage_bytes = kSub * (kBM * 128 + ((g.BN * 128 + 1023) & ~1023));
-  p.stages = ring_stages((200 * 1024) / stage_bytes);
+  p.stages = ring_stages(std::min(tune("bf_stages", 8), (200 * 1024) / stage_bytes));
   const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
   static bool attr = false;
   if (!attr) {
-    e = cudaFuncSetAttribute(bf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    e = cudaFuncSetAttribute(bf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);  // + 1 KB static offtab
     if (e != cudaSuccess) return e;
     attr = true;
   }

@@ -11,6 +11,10 @@
 
 namespace ucudnn {
 
+// Experiment knob: integer `key` from UCUDNN_TUNE="key=v,key=v" (parsed
+// once), else `dflt`. Only used for A/B timing of pipeline parameters.
+int tune(const char* key, int dflt);
+
 // Host-side count of device kernels this library has launched (evidence for
 // bench.py's gpu_launches; see ucudnnGetLaunchCount).
 void count_launch(int n = 1);

@@ -500,9 +500,9 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   }
   // two 32-deep chunks per stage (8 MMAs per tcgen05.commit): measured
   // 10-25 % faster than one on AlexNet conv2 / conv4 (same box, A/B)
-  p.ksub = 2;
+  p.ksub = std::max(1, std::min(2, tune("pc_ksub", 2)));
   const int stage_bytes = p.ksub * (kBM * 128 + ((BN * 128 + 1023) & ~1023));
-  p.stages = ring_stages((200 * 1024) / stage_bytes);
+  p.stages = ring_stages(std::min(tune("pc_stages", 8), (200 * 1024) / stage_bytes));
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)
   const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);

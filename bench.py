@@ -96,9 +96,16 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        # nvidia-smi takes a few hundred ms to start: wait for its first row so
+        # the samples fall inside the timed region that follows
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < 5.0:
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.02)
 
     def stop(self):
         if self.p is None:
@@ -162,7 +169,7 @@ def tf32_peak(dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--net", default="alexnet")
@@ -171,6 +178,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=0, help="samples per step (0: one per host core, <= 64)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a replayed CUDA graph")
     ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -236,13 +244,35 @@ def main():
         stack.step(base, comm, comm_stream)
         stack.algos = ours_algos
 
+    # One process per GPU with no collective inside the step (N = 1): capture
+    # the 15 planned C-ABI calls once into a CUDA graph and replay it, which
+    # removes the host launch gaps between the ~140 small kernels. N > 1
+    # keeps eager launches (the NCCL all-reduces are issued per layer).
+    def as_graph(fn, handle):
+        if dist_on or args.no_graph:
+            n0 = lib().ucudnnGetLaunchCount()
+            fn()
+            torch.cuda.synchronize(dev)
+            return fn, lib().ucudnnGetLaunchCount() - n0
+        cs = torch.cuda.Stream(dev)
+        handle.set_stream(cs.cuda_stream)
+        with torch.cuda.stream(cs):
+            fn()  # warm (first-call attribute setting, filter packing)
+        cs.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = lib().ucudnnGetLaunchCount()
+        with torch.cuda.graph(g, stream=cs):
+            fn()
+        per_step = lib().ucudnnGetLaunchCount() - n0
+        handle.set_stream(stream.cuda_stream)
+        return g.replay, per_step
+
+    run_ours, launches_per_step = as_graph(step_ours, h)
+    run_base, _ = as_graph(step_base, base)
     sampler = ClockSampler(local) if rank == 0 else None
-    n0 = lib().ucudnnGetLaunchCount()
-    ms = timed(step_ours, args.steps, args.warmup, dev, dist_on)
-    launches = (lib().ucudnnGetLaunchCount() - n0)
+    ms = timed(run_ours, args.steps, args.warmup, dev, dist_on)
     clocks = sampler.stop() if sampler else None
-    launches_per_step = launches // (args.steps + args.warmup)
-    ms_base = timed(step_base, args.steps, args.warmup, dev, dist_on)
+    ms_base = timed(run_base, args.steps, args.warmup, dev, dist_on)
 
     # per-kernel device times of our plan (dominant kernel -> roofline)
     evs = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in stack.kernels()}
@@ -295,7 +325,8 @@ def main():
             "config": {"workload": "AlexNet conv1-5, Forward + BackwardData + BackwardFilter (15 kernels), "
                                    "batch 256 per GPU", "net": args.net, "global_batch": 256 * world,
                        "ws_limit_bytes": limit, "mode": "wr", "policy": args.policy,
-                       "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)"},
+                       "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)",
+                       "launch": "eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls"},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
                          "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                          "frac": round(dom_tflops / peak, 3), "traffic": None,

@@ -63,12 +63,12 @@ typedef enum {
 /* Concrete B200 algorithms (the cost-table `algorithm` column). Ids 0-2 keep
  * the reference archetype names of cost_model.hpp:165-177. */
 typedef enum {
-  UCUDNN_ALGO_IMPLICIT_GEMM = 0,     /* tcgen05 implicit GEMM, 0 workspace            */
-  UCUDNN_ALGO_WINOGRAD = 1,          /* F(2x2,3x3), transforms + batched tcgen05 GEMM */
-  UCUDNN_ALGO_FFT = 2,               /* FFT-tiled (reserved: infeasible rows today)   */
-  UCUDNN_ALGO_GEMM = 3,              /* explicit im2col + tcgen05 GEMM                */
-  UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (reserved)                          */
-  UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* NHWC copy + TMA-im2col tcgen05 GEMM, ws ~ b  */
+  UCUDNN_ALGO_IMPLICIT_GEMM = 0,     /* tcgen05 implicit GEMM, SIMT-gathered operands, 0 workspace */
+  UCUDNN_ALGO_WINOGRAD = 1,          /* F(2x2,3x3) (3x3 s1 F/BD): transforms + 16 batched tcgen05 GEMMs */
+  UCUDNN_ALGO_FFT = 2,               /* FFT-tiled (s1 F/BD, R,S <= 16): register FFTs + per-bin GEMMs */
+  UCUDNN_ALGO_GEMM = 3,              /* explicit im2col / col2im + tiled tcgen05 GEMM                  */
+  UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (3x3 s1 F/BD): 36 batched tcgen05 GEMMs             */
+  UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* TMA-fed implicit GEMM on re-laid copies (all ops), ws ~ b   */
   UCUDNN_ALGO_COUNT = 6
 } ucudnnAlgo_t;
 

@@ -104,11 +104,17 @@ struct ucudnnContext {
   void* bench_ws = nullptr;
   std::size_t bench_ws_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // L2 flush before every timed run (a plan's micro-batches stream their
+  // slices from HBM; timing L2-hot repeats under-costs bandwidth-bound
+  // algorithms). UCUDNN_BENCH_FLUSH_MB, default 256 (> the 126 MB L2); 0 = off.
+  void* flush = nullptr;
+  std::size_t flush_bytes = std::size_t(-1);
 
   ~ucudnnContext() {
     if (arena) cudaFree(arena);
     if (scratch) cudaFree(scratch);
     if (bench_ws) cudaFree(bench_ws);
+    if (flush) cudaFree(flush);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -206,8 +212,14 @@ std::int64_t time_once(ucudnnContext* h, int op, const ConvShape& s, int algo, s
   for (int i = 0; i < std::max(1, h->warmup); ++i)
     cuda_check(a->run(op, s, ia, ib, out, h->bench_ws, 1.f, 0.f, h->stream, i ? kFilterReady : 0),
                "benchmark warm-up");
+  if (h->flush_bytes == std::size_t(-1)) {
+    const char* e = std::getenv("UCUDNN_BENCH_FLUSH_MB");
+    h->flush_bytes = std::size_t(e ? std::max(0, std::atoi(e)) : 256) << 20;
+    if (h->flush_bytes) cuda_check(cudaMalloc(&h->flush, h->flush_bytes), "cudaMalloc(L2 flush buffer)");
+  }
   std::vector<float> ms;
   for (int i = 0; i < std::max(1, h->iters); ++i) {
+    if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, h->stream), "L2 flush");
     cuda_check(cudaEventRecord(h->ev0, h->stream), "cudaEventRecord");
     cuda_check(a->run(op, s, ia, ib, out, h->bench_ws, 1.f, 0.f, h->stream, kFilterReady), "benchmark run");
     cuda_check(cudaEventRecord(h->ev1, h->stream), "cudaEventRecord");

@@ -298,12 +298,33 @@ def main():
     h2d = x_host.numel() * 4 + dy_host.numel() * 4
     d2h = sum(d.numel() * 4 for d in dw_host)
 
+    # copies overlap compute where the data flow allows: the top gradient's
+    # H2D runs on a copy stream during the forward pass, each dW's D2H starts
+    # right after its BackwardFilter; the step ends when every copy is done.
+    cp = torch.cuda.Stream(dev)
+
     def step_e2e():
+        cur = torch.cuda.current_stream(dev)
         stack.t[0]["x"].copy_(x_host, non_blocking=True)
-        stack.t[-1]["dy"].copy_(dy_host, non_blocking=True)
-        stack.step(h, comm, comm_stream)
-        for d, t in zip(dw_host, stack.t):
-            d.copy_(t["dw"], non_blocking=True)
+        cp.wait_stream(cur)
+        with torch.cuda.stream(cp):
+            stack.t[-1]["dy"].copy_(dy_host, non_blocking=True)
+        dy_ready = torch.cuda.Event()
+        dy_ready.record(cp)
+
+        def on_dw(i):
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            cp.wait_event(ev)
+            with torch.cuda.stream(cp):
+                dw_host[i].copy_(stack.t[i]["dw"], non_blocking=True)
+
+        stack.step(h, comm, comm_stream, on_backward=lambda: cur.wait_event(dy_ready),
+                   on_dw=None if comm is not None else on_dw)
+        if comm is not None:
+            for d, t in zip(dw_host, stack.t):
+                d.copy_(t["dw"], non_blocking=True)
+        cur.wait_stream(cp)
 
     ms_e2e = timed(step_e2e, args.steps, args.warmup, dev, dist_on)
 

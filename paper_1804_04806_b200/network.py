@@ -121,10 +121,12 @@ class ConvStack:
         else:
             h.backward_filter(s, t["x"], t["dy"], t["dw"], a, self.ws)
 
-    def step(self, h: Handle, comm=None, comm_stream=None, events=None):
+    def step(self, h: Handle, comm=None, comm_stream=None, events=None, on_backward=None, on_dw=None):
         """One training step of the conv stack. `comm`: torch.distributed group
         (dw all-reduce on `comm_stream`); `events`: optional dict (i, op) ->
-        (start, end) CUDA events recorded around each kernel."""
+        (start, end) CUDA events recorded around each kernel; `on_backward()`
+        runs before the first backward kernel is issued and `on_dw(i)` after
+        layer i's BackwardFilter (hooks for overlapping host copies)."""
         cur = torch.cuda.current_stream(self.device)
         n = len(self.layers)
         order = [(i, FORWARD) for i in range(n)]
@@ -132,11 +134,15 @@ class ConvStack:
             order += [(i, BACKWARD_DATA), (i, BACKWARD_FILTER)]
         pending = []
         for i, op in order:
+            if op == BACKWARD_DATA and i == n - 1 and on_backward is not None:
+                on_backward()
             if events is not None:
                 events[(i, op)][0].record(cur)
             self.run_kernel(h, i, op)
             if events is not None:
                 events[(i, op)][1].record(cur)
+            if op == BACKWARD_FILTER and on_dw is not None and comm is None:
+                on_dw(i)
             if op == BACKWARD_FILTER and comm is not None:
                 ev = torch.cuda.Event()
                 ev.record(cur)

@@ -174,7 +174,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--net", default="alexnet")
     ap.add_argument("--policy", default="powerOfTwo")
-    ap.add_argument("--limit-mib", type=int, default=64)
+    ap.add_argument("--limit-mib", type=int, default=64, help="WR: per-kernel workspace limit")
+    ap.add_argument("--mode", default="wr", choices=["wr", "wd"])
+    ap.add_argument("--total-mib", type=int, default=2544, help="WD: network-wide workspace budget")
     ap.add_argument("--ref-sample", type=int, default=0, help="samples per step (0: one per host core, <= 64)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -220,8 +222,18 @@ def main():
             open(db, "w").write("")
         torch.distributed.barrier()
         share_cost_table(db)
-    h = Handle(policy=args.policy, mode="wr", database=db, stream=stream.cuda_stream)
-    stack.plan(h, limit)
+    if args.mode == "wd":
+        # WD: Get*Algorithm registers every kernel, one ILP divides
+        # the budget, the library owns the arena; the undivided baseline gets
+        # budget / #kernels each (harness.hpp:71-80)
+        total = args.total_mib * MiB
+        h = Handle(policy=args.policy, mode="wd", total_workspace=total, database=db, stream=stream.cuda_stream)
+        stack.plan(h, 0)
+        h.optimize_network()
+        limit = total // len(stack.kernels())
+    else:
+        h = Handle(policy=args.policy, mode="wr", database=db, stream=stream.cuda_stream)
+        stack.plan(h, limit)
     h.flush_database()
     plan_s = time.perf_counter() - t0
     plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": h.plan(a) for (i, op), a in stack.algos.items()}
@@ -337,15 +349,20 @@ def main():
                              f"x{256 // args.cpu_sample}"}
         total_flops = stack.flops()
         line = {
-            "metric": METRIC, "value": round(ms, 4), "unit": "ms/iter", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if (args.net == "alexnet" and args.mode == "wr" and args.limit_mib == 64) else
+            f"{args.net} bs256 conv fwd+bwd ms/iter ({args.mode.upper()}, "
+            f"{args.limit_mib if args.mode == 'wr' else args.total_mib} MiB); speedup vs undivided",
+            "value": round(ms, 4), "unit": "ms/iter", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "tf32", "data": "synthetic (N(0,1) activations, He-init filters)",
             "speedup_vs_undivided": round(ms_base / ms, 4), "undivided_ms_per_step": round(ms_base, 4),
             "images_per_s": round(256 * world / (ms * 1e-3), 1),
             "tflops_effective": round(total_flops / (ms * 1e-3) / 1e12, 2),
-            "config": {"workload": "AlexNet conv1-5, Forward + BackwardData + BackwardFilter (15 kernels), "
-                                   "batch 256 per GPU", "net": args.net, "global_batch": 256 * world,
-                       "ws_limit_bytes": limit, "mode": "wr", "policy": args.policy,
+            "config": {"workload": f"{args.net} conv layers, Forward + BackwardData + BackwardFilter "
+                                   f"({len(stack.kernels())} kernels), batch 256 per GPU", "net": args.net,
+                       "global_batch": 256 * world,
+                       "ws_limit_bytes": limit, "mode": args.mode, "policy": args.policy,
+                       "total_workspace_bytes": args.total_mib * MiB if args.mode == "wd" else None,
                        "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)",
                        "launch": "eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls"},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",

@@ -71,6 +71,7 @@ struct BfGeo {
   int M, BN, m_tiles, n_tiles;
   int swap;            // 1: MMA rows = output channels k (K <= 128), columns = (q, cc) rows
   int Kb;              // swap: dy box rows (K rounded to 8; MMA rows past it are never read)
+  int x_direct, dy_direct;  // the re-layout would be an identity copy (1x1 stride-1 convs): TMA reads x / dy
 };
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
@@ -111,6 +112,9 @@ BfGeo make_geo(const ConvShape& s) {
   g.Ldp = round_up(g.Ld, 4);
   g.Lc = (g.Ld + 31) / 32;
   g.M = g.Qh * g.Qw * g.CCp;
+  g.x_direct = s.sh == 1 && s.sw == 1 && s.ph == 0 && s.pw == 0 && g.T == 1 && g.Wq == s.W && g.Hq == s.H &&
+               g.Lp == g.Lq;
+  g.dy_direct = g.Wq == g.OW && g.Ldp == g.Ld;
   // Few output channels (AlexNet conv1, ResNet stage 1: K = 64): an N = 64
   // MMA is issue-bound, so swap roles -- MMA rows are the K channels (one
   // 128-row tile, zero-filled past K) and the (q, cc) rows become N <= 256.
@@ -131,8 +135,8 @@ BfGeo make_geo(const ConvShape& s) {
 }
 
 std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
-std::size_t x_bytes(const BfGeo& g) { return a256(std::size_t(g.T) * g.N * g.CC * g.Lp * 4); }
-std::size_t dy_bytes(const BfGeo& g) { return a256(std::size_t(g.N) * g.K * g.Ldp * 4); }
+std::size_t x_bytes(const BfGeo& g) { return g.x_direct ? 0 : a256(std::size_t(g.T) * g.N * g.CC * g.Lp * 4); }
+std::size_t dy_bytes(const BfGeo& g) { return g.dy_direct ? 0 : a256(std::size_t(g.N) * g.K * g.Ldp * 4); }
 
 struct BfParams {
   float* dw;
@@ -457,8 +461,8 @@ std::int64_t bf_workspace(const ConvShape& s) {
 cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
                    cudaStream_t st) {
   const BfGeo g = make_geo(s);
-  float* xph = static_cast<float*>(ws);
-  float* dyp = reinterpret_cast<float*>(static_cast<char*>(ws) + x_bytes(g));
+  const float* xph = g.x_direct ? x : static_cast<const float*>(ws);
+  const float* dyp = g.dy_direct ? dy : reinterpret_cast<const float*>(static_cast<char*>(ws) + x_bytes(g));
   if (beta != 1.f) {
     const std::int64_t n = s.w_elems();
     count_launch();
@@ -466,15 +470,19 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   }
   const FastDiv fd_wq(std::uint32_t(g.Wq));
   const int sms = sm_count();
-  XPhaseArgs xa{x, xph, g.C, g.H, g.W, g.ph, g.pw, g.sh, g.sw, g.Bw, g.CC, g.T,
+  XPhaseArgs xa{x, const_cast<float*>(xph), g.C, g.H, g.W, g.ph, g.pw, g.sh, g.sw, g.Bw, g.CC, g.T,
                 std::int64_t(g.N) * g.CC * (g.Lp / 4), std::int64_t(g.N) * g.CC * g.Lp,
                 FastDiv(std::uint32_t(g.Lp / 4)), fd_wq, FastDiv(std::uint32_t(g.C)), FastDiv(std::uint32_t(g.Bw))};
-  count_launch();
-  x_phase_kernel<<<int(std::min<std::int64_t>((xa.units + 255) / 256, 16 * sms)), 256, 0, st>>>(xa);
+  if (!g.x_direct) {
+    count_launch();
+    x_phase_kernel<<<int(std::min<std::int64_t>((xa.units + 255) / 256, 16 * sms)), 256, 0, st>>>(xa);
+  }
   const std::int64_t dunits = std::int64_t(g.N) * g.K * (g.Ldp / 4);
-  count_launch();
-  dy_pitch_kernel<<<int(std::min<std::int64_t>((dunits + 255) / 256, 16 * sms)), 256, 0, st>>>(
-      dy, dyp, g.OH, g.OW, dunits, FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq);
+  if (!g.dy_direct) {
+    count_launch();
+    dy_pitch_kernel<<<int(std::min<std::int64_t>((dunits + 255) / 256, 16 * sms)), 256, 0, st>>>(
+        dy, const_cast<float*>(dyp), g.OH, g.OW, dunits, FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 

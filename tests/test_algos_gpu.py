@@ -26,6 +26,8 @@ SHAPES = [
     ConvShape(2, 192, 13, 13, 384, 3, 3, 1, 1, 1, 1),     # AlexNet conv3 (N tiles of 192)
     ConvShape(2, 40, 6, 6, 300, 3, 3, 1, 1, 1, 1),        # ragged tiles
     ConvShape(3, 64, 7, 7, 64, 3, 3, 1, 1, 1, 1),         # ResNet l4-like spatial size
+    ConvShape(2, 64, 14, 14, 32, 1, 1, 0, 0, 1, 1),       # 1x1 stride 1: BF reads x / dy in place
+    ConvShape(3, 32, 7, 7, 160, 1, 1, 0, 0, 1, 1),        # 1x1 stride 1, 49-pixel planes (re-laid)
 ]
 ALGOS = [0, 1, 2, 3, 4, 5]
 # F(4x4,3x3) carries 1/6 and 1/24 in G: not exact in TF32 even on integer data,

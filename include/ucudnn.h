@@ -93,6 +93,10 @@ int64_t ucudnnGetMinTotalWorkspace(void);
 size_t ucudnnGetVersion(void);
 /* Number of device kernels this library has launched in this process. */
 uint64_t ucudnnGetLaunchCount(void);
+/* Diagnostic: mean MMA-warp cycles {waiting for operands, issuing, waiting
+ * for a free accumulator, total} per CTA of the last IMPLICIT_PRECOMP_GEMM
+ * launch made with UCUDNN_TUNE=prof=1 (zeros otherwise). */
+ucudnnStatus_t ucudnnDebugPrecompProfile(double* out4);
 
 /* ------------------------------------------------------------ handle ----- */
 /* Replaces cudnnCreate/cudnnDestroy/cudnnSetStream. The

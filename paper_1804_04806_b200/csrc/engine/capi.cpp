@@ -15,6 +15,7 @@
 #include "../kernels/igemm.h"
 #include "../planner/planner.h"
 #include "algos.h"
+#include "../kernels/precomp.h"
 
 using namespace ucudnn;
 
@@ -415,6 +416,12 @@ const char* ucudnnGetLastError(void) { return g_last_error.c_str(); }
 int64_t ucudnnGetMinTotalWorkspace(void) { return g_min_ws; }
 size_t ucudnnGetVersion(void) { return UCUDNN_VERSION; }
 uint64_t ucudnnGetLaunchCount(void) { return launch_count(); }
+
+ucudnnStatus_t ucudnnDebugPrecompProfile(double* out4) {
+  if (!out4) return UCUDNN_STATUS_BAD_PARAM;
+  precomp_profile(out4);
+  return UCUDNN_STATUS_SUCCESS;
+}
 
 ucudnnStatus_t ucudnnCreate(UcudnnHandle_t* out) {
   return guarded([&] {

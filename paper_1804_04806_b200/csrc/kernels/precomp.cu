@@ -63,7 +63,7 @@ struct PrecompParams {
   // phase scatter epilogue (strided BackwardData): column (a, b, c) of
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
-  int stages, ksub;
+  int stages, ksub, prof;
   FastDiv fd_Cr, fd_ssw;
 };
 
@@ -73,6 +73,10 @@ __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& 
   nt = int(q);
   mt = int(r);
 }
+
+// UCUDNN_TUNE=prof=1: per-CTA cycle counters of the MMA warp (wait-for-data,
+// issue, wait-for-accumulator) -- a diagnostic, read by ucudnnDebugProfile.
+__device__ unsigned long long g_prof[1024 * 4];
 
 __global__ void __launch_bounds__(kThreads, 1)
     precomp_kernel(const __grid_constant__ CUtensorMap amap, const PrecompParams p) {
@@ -165,15 +169,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
     const std::uint32_t sbase = smem_u32(smem);
     int it = 0, tl = 0;
+    long long c_data = 0, c_issue = 0, c_acc = 0, t_start = clock64();
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       const int acc = tl & 1;
+      long long c0 = p.prof ? clock64() : 0;
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
       tc_fence_after();
+      if (p.prof) c_acc += clock64() - c0;
       const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
       for (int j = 0; j < jsteps; ++j, ++it) {
         const int s = it % kStages;
+        long long c1 = p.prof ? clock64() : 0;
         mbar_wait(&full[s], (it / kStages) & 1);
         tc_fence_after();
+        long long c2 = p.prof ? clock64() : 0;
+        if (p.prof) c_data += c2 - c1;
         const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
         if (lane == 0) {
           for (int sub = 0; sub < nsub; ++sub) {
@@ -190,7 +200,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (j == jsteps - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
+        if (p.prof) c_issue += clock64() - c2;
       }
+    }
+    if (p.prof && lane == 0 && blockIdx.x < 1024) {
+      g_prof[blockIdx.x * 4 + 0] = c_data;
+      g_prof[blockIdx.x * 4 + 1] = c_issue;
+      g_prof[blockIdx.x * 4 + 2] = c_acc;
+      g_prof[blockIdx.x * 4 + 3] = clock64() - t_start;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
@@ -332,9 +349,13 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       int tap, ch;
-      if (small_c) {
+      if (small_c == 1) {
         tap = k * 8 + g;
         ch = e;
+      } else if (small_c == 2) {  // strip kernel: k = chunk * taps + tap
+        const int cc = k / taps;
+        tap = k - cc * taps;
+        ch = cc * 32 + g * 4 + e;
       } else {
         tap = k / c_chunks;
         ch = (k - tap * c_chunks) * 32 + g * 4 + e;
@@ -363,6 +384,259 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
     const std::int64_t blk = u / (8 * BN);
     reinterpret_cast<float4*>(out)[blk * 8 * BN + row * 8 + (g ^ (row & 7))] = make_float4(v[0], v[1], v[2], v[3]);
   }
+}
+
+
+// ---------------------------------------------------------------- strip
+// Stride-1 implicit GEMM that loads each input pixel once per 32-channel
+// chunk instead of once per filter tap. The (padded, channels-last) input is
+// read as a flat [rows = (n, h, w)][C] matrix with the padded row pitch Wp,
+// and output pixel (oh, ow) of image n is flat position p = n*Hp*Wp + oh*Wp +
+// ow (positions with ow >= OW or oh >= OH are computed and dropped). Tap
+// (r, s) of positions [p0, p0+128) then reads input rows [p0 + r*Wp + s, ...),
+// so one TMA "strip" of 128 + (R-1)*Wp + (S-1) rows per chunk feeds every tap:
+// the UMMA descriptor simply starts r*Wp + s rows (x 128 B) into the strip --
+// SWIZZLE_128B is a function of the absolute smem address, so any 128-byte
+// row start is legal (scripts/offset_probe.cu). Compared with one TMA im2col
+// box per (tap, chunk) this cuts the operand traffic from L2 by ~R*S for A.
+//
+// Roles: warp 3 lane 0 streams strips into a double buffer; warps 0 and 2
+// stream the filter chunks of two taps per stage (8 MMAs per commit); warp 1
+// issues tcgen05.mma; warps 4-7 run the epilogue (NCHW or stride-phase
+// scatter) while the next tile accumulates in the other TMEM buffer.
+constexpr int kTapsPerStage = 2;
+
+struct StripParams {
+  const float* btiles;  // [n_tile][chunk][tap][BN rows][32 floats, SW128]
+  float* out;
+  float alpha, beta;
+  int BN, n_tiles, m_tiles, tpi;  // tiles per image
+  int taps, S, c_chunks, Wp, HWp;
+  int OH, OW, Nout, P;
+  int box_rows, nboxes, stages;
+  int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    strip_kernel(const __grid_constant__ CUtensorMap xmap, const StripParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t strip_bytes = std::uint32_t(p.nboxes * p.box_rows) * 128;
+  const std::uint32_t tap_bytes = std::uint32_t(p.BN) * 128;
+  const std::uint32_t stage_bytes = kTapsPerStage * tap_bytes;
+  const int kStages = p.stages;
+  unsigned char* strips = smem;
+  unsigned char* ring = smem + 2 * strip_bytes;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* sfull = empty + kMaxStages;
+  std::uint64_t* sempty = sfull + 2;
+  std::uint64_t* tfull = sempty + 2;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&sfull[a], 1);
+      mbar_init(&sempty[a], 1);
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int total_tiles = p.m_tiles * p.n_tiles;
+  const int tsteps = (p.taps + kTapsPerStage - 1) / kTapsPerStage;  // filter stages per chunk
+
+  if (warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------ strip producer
+      int sc = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        std::uint32_t nt, mt, n, local;
+        p.fd_mt.divmod(std::uint32_t(t), nt, mt);
+        p.fd_tpi.divmod(mt, n, local);
+        const int p0 = int(n) * p.HWp + int(local) * kBM;
+        for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
+          const int sb = sc & 1;
+          mbar_wait(&sempty[sb], ((sc >> 1) & 1) ^ 1);
+          mbar_expect_tx(&sfull[sb], strip_bytes);
+          for (int bx = 0; bx < p.nboxes; ++bx)
+            tma_2d(strips + sb * strip_bytes + bx * p.box_rows * 128, &xmap, &sfull[sb], cc * 32,
+                   p0 + bx * p.box_rows);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 0 || warp == 2) {
+    // ------------------------------------------------ filter producers
+    const int pq = warp == 0 ? 0 : 1, nprod = kStages < 2 ? 1 : 2;
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const int nt = t / p.m_tiles;
+        const float* bsrc = p.btiles + std::size_t(nt) * p.c_chunks * p.taps * (tap_bytes / 4);
+        for (int cc = 0; cc < p.c_chunks; ++cc)
+          for (int ts = 0; ts < tsteps; ++ts, ++it) {
+            if ((it % kStages) % nprod != pq) continue;
+            const int st = it % kStages;
+            const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
+            mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+            mbar_expect_tx(&full[st], ntap * tap_bytes);
+            for (int i = 0; i < ntap; ++i)
+              bulk_g2s(ring + st * stage_bytes + i * tap_bytes,
+                       bsrc + (std::size_t(cc) * p.taps + tap0 + i) * (tap_bytes / 4), tap_bytes, &full[st]);
+          }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint32_t sbase = smem_u32(strips), rbase = smem_u32(ring);
+    int it = 0, sc = 0, tl = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
+      const int acc = tl & 1;
+      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
+        const int sb = sc & 1;
+        mbar_wait(&sfull[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        for (int ts = 0; ts < tsteps; ++ts, ++it) {
+          const int st = it % kStages;
+          const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            for (int i = 0; i < ntap; ++i) {
+              const int tap = tap0 + i, r = tap / p.S, q = tap - r * p.S;
+              const std::uint32_t sa = sbase + sb * strip_bytes + std::uint32_t(r * p.Wp + q) * 128;
+              const std::uint32_t sbb = rbase + st * stage_bytes + i * tap_bytes;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_tf32(dtm, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sbb + k * 32), idesc,
+                         (cc | tap | k) != 0);
+            }
+            mma_commit(&empty[st]);
+            if (ts == tsteps - 1) mma_commit(&sempty[sb]);
+            if (ts == tsteps - 1 && cc == p.c_chunks - 1) mma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    int tl = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
+      std::uint32_t nt, mt, n, local;
+      p.fd_mt.divmod(std::uint32_t(t), nt, mt);
+      p.fd_tpi.divmod(mt, n, local);
+      const int acc = tl & 1;
+      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const int pos = int(local) * kBM + ew * 32 + lane;  // flat position inside image n
+      std::uint32_t oh, ow;
+      p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
+      const bool ok = int(oh) < p.OH && int(ow) < p.OW;
+      std::int64_t obase = 0;
+      int hb = 0, wb = 0;
+      if (ok) {
+        if (p.phase) {
+          obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
+          hb = int(oh) * p.ssh - p.sph;
+          wb = int(ow) * p.ssw - p.spw;
+        } else {
+          obase = std::int64_t(n) * p.Nout * p.P + int(oh) * p.OW + int(ow);
+        }
+      }
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (!ok) continue;
+        if (p.phase) {
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const int col = int(nt) * p.BN + c0 + j;
+            if (c0 + j >= p.BN || col >= p.Nout) break;
+            std::uint32_t ab, c, a, b;
+            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
+            p.fd_ssw.divmod(ab, a, b);
+            const int h = hb + int(a), w = wb + int(b);
+            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+            const float val = p.alpha * v[j];
+            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = int(nt) * p.BN + c0 + j;
+          if (c0 + j >= p.BN || col >= p.Nout) break;
+          float* dst = p.out + obase + std::int64_t(col) * p.P;
+          const float val = p.alpha * v[j];
+          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// NCHW -> zero-padded channels-last [n][Hp][Wp][Cp] (source pixel (h, w)
+// lands at (h + pt, w + pl)); 32 x 33 smem transpose per (n, row, w-block, c-block).
+__global__ void pad_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int H, int W, int Cp,
+                                int pt, int pl, int Hp, int Wp) {
+  __shared__ float tile[32][33];
+  const int n = blockIdx.z / Hp, hp = blockIdx.z - n * Hp;
+  const int w0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int h = hp - pt;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, w = w0 + threadIdx.x - pl;
+    float v = 0.f;
+    if (c < C && unsigned(h) < unsigned(H) && unsigned(w) < unsigned(W) && w0 + int(threadIdx.x) < Wp)
+      v = src[((std::int64_t(n) * C + c) * H + h) * W + w];
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  float* o = dst + (std::int64_t(n) * Hp + hp) * Wp * Cp;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int wp = w0 + i, c = c0 + threadIdx.x;
+    if (wp < Wp && c < Cp) o[std::int64_t(wp) * Cp + c] = tile[threadIdx.x][i];
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
 }
 
 PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col() {
@@ -404,6 +678,31 @@ struct Geo {
   int Hr = 0, Wr = 0, rph = 0, rpw = 0;  // the real dx extent and conv padding
 };
 
+// Strip path (stride-1 after the s2d / phase rewrites, >= 32-channel rows):
+// geometry of the padded input and of the per-chunk strip.
+struct StripGeo {
+  bool ok = false;
+  int Hp = 0, Wp = 0, rows = 0, box_rows = 0, nboxes = 0, stages = 0;
+  std::size_t strip_bytes = 0;
+};
+StripGeo strip_geo(const Geo& g, int BN) {
+  StripGeo sg;
+  if (g.sh != 1 || g.sw != 1 || cpad(g.Cin) == 4 || !tune("strip", 0)) return sg;
+  sg.Hp = g.Hin + g.ph + (g.ph_hi < 0 ? g.ph : g.ph_hi);
+  sg.Wp = g.Win + g.pw + (g.pw_hi < 0 ? g.pw : g.pw_hi);
+  if (sg.Hp - g.R + 1 != g.Hout || sg.Wp - g.S + 1 != g.Wout) return sg;
+  sg.rows = kBM + (g.R - 1) * sg.Wp + (g.S - 1);
+  sg.box_rows = std::min(256, (sg.rows + 7) / 8 * 8);
+  sg.nboxes = (sg.rows + sg.box_rows - 1) / sg.box_rows;
+  sg.strip_bytes = std::size_t(sg.nboxes) * sg.box_rows * 128;
+  const std::size_t stage = std::size_t(kTapsPerStage) * BN * 128;
+  const std::size_t budget = 210 * 1024;
+  if (2 * sg.strip_bytes + 2 * stage > budget) return sg;
+  sg.stages = int(std::min<std::size_t>(kMaxStages, (budget - 2 * sg.strip_bytes) / stage));
+  sg.ok = true;
+  return sg;
+}
+
 std::size_t geo_ws(const Geo& g, int* ksteps_out = nullptr, int* bn_out = nullptr) {
   const int Cp = cpad(g.Cin), taps = g.R * g.S;
   const bool small = Cp == 4;
@@ -411,11 +710,105 @@ std::size_t geo_ws(const Geo& g, int* ksteps_out = nullptr, int* bn_out = nullpt
   const int BN = pick_bn(g.Nout), n_tiles = (g.Nout + BN - 1) / BN;
   if (ksteps_out) *ksteps_out = ksteps;
   if (bn_out) *bn_out = BN;
-  return align256(std::size_t(n_tiles) * ksteps * BN * 128) + align256(std::size_t(g.N) * g.Hin * g.Win * Cp * 4);
+  const StripGeo sg = strip_geo(g, BN);
+  const std::size_t act = sg.ok ? std::size_t(g.N) * sg.Hp * sg.Wp * Cp * 4 : std::size_t(g.N) * g.Hin * g.Win * Cp * 4;
+  return align256(std::size_t(n_tiles) * ksteps * BN * 128) + align256(act);
+}
+
+cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const float* w, int flip, float* out,
+                      void* ws, float alpha, float beta, cudaStream_t st, int flags) {
+  const int Cp = cpad(g.Cin), taps = g.R * g.S;
+  int ksteps = 0, BN = 0;
+  geo_ws(g, &ksteps, &BN);
+  const int n_tiles = (g.Nout + BN - 1) / BN;
+  float* btiles = static_cast<float*>(ws);
+  float* xp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(std::size_t(n_tiles) * ksteps * BN * 128));
+  count_launch();
+  if (g.s2d) {
+    S2D d = g.sd;
+    d.Cp = Cp;
+    s2d_nhwc_kernel<<<dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st>>>(act, xp, d);
+  } else {
+    pad_nhwc_kernel<<<dim3((sg.Wp + 31) / 32, (Cp + 31) / 32, g.N * sg.Hp), dim3(32, 8), 0, st>>>(
+        act, xp, g.Cin, g.Hin, g.Win, Cp, g.ph, g.pw, sg.Hp, sg.Wp);
+  }
+  if (!(flags & kFilterReady)) {
+    const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
+    const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
+    count_launch();
+    pack_filter_kernel<<<blocks, 256, 0, st>>>(w, btiles, g.Nout, g.Cin, taps, BN, n_tiles, ksteps, 2, Cp / 32,
+                                               g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  CUtensorMap xmap;
+  const std::uint64_t rows_total = std::uint64_t(g.N) * sg.Hp * sg.Wp;
+  const cuuint64_t dims[2] = {cuuint64_t(Cp), cuuint64_t(rows_total)};
+  const cuuint64_t strides[1] = {cuuint64_t(Cp) * 4};
+  const cuuint32_t box[2] = {32, cuuint32_t(sg.box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, xp, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+
+  StripParams p{};
+  p.btiles = btiles;
+  p.out = out;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.BN = BN;
+  p.n_tiles = n_tiles;
+  p.Wp = sg.Wp;
+  p.HWp = sg.Hp * sg.Wp;
+  p.OH = g.Hout;
+  p.OW = g.Wout;
+  p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + kBM - 1) / kBM;
+  p.m_tiles = g.N * p.tpi;
+  p.taps = taps;
+  p.S = g.S;
+  p.c_chunks = Cp / 32;
+  p.Nout = g.Nout;
+  p.P = g.Hout * g.Wout;
+  p.box_rows = sg.box_rows;
+  p.nboxes = sg.nboxes;
+  p.stages = sg.stages;
+  p.fd_Wp = FastDiv(std::uint32_t(sg.Wp));
+  p.fd_tpi = FastDiv(std::uint32_t(p.tpi));
+  p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
+  p.phase = g.phase;
+  if (g.phase) {
+    p.Cr = g.pf.C;
+    p.Hr = g.Hr;
+    p.Wr = g.Wr;
+    p.ssh = g.pf.sh;
+    p.ssw = g.pf.sw;
+    p.sph = g.rph;
+    p.spw = g.rpw;
+    p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
+    p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
+  }
+  const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  count_launch();
+  strip_kernel<<<std::min(sm_count(), p.m_tiles * p.n_tiles), kThreads, std::max(smem, 116 * 1024), st>>>(xmap, p);
+  return cudaGetLastError();
 }
 
 cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, float* out, void* ws, float alpha,
                     float beta, cudaStream_t st, int flags) {
+  {
+    int ks = 0, bn = 0;
+    geo_ws(g, &ks, &bn);
+    const StripGeo sg = strip_geo(g, bn);
+    if (sg.ok) return run_strip(g, sg, act, w, flip, out, ws, alpha, beta, st, flags);
+  }
   const int Cp = cpad(g.Cin), taps = g.R * g.S;
   int ksteps = 0, BN = 0;
   geo_ws(g, &ksteps, &BN);
@@ -486,6 +879,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   p.fd_P = FastDiv(std::uint32_t(p.P));
   p.fd_OW = FastDiv(std::uint32_t(g.Wout));
   p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
+  p.prof = tune("prof", 0);
   p.phase = g.phase;
   if (g.phase) {
     p.Cr = g.pf.C;
@@ -570,6 +964,21 @@ Geo bwd_data_phase_geo(const ConvShape& s) {
 Geo bd_geo(const ConvShape& s) { return (s.sh == 1 && s.sw == 1) ? bwd_data_geo(s) : bwd_data_phase_geo(s); }
 
 }  // namespace
+
+// Diagnostic: average MMA-warp cycles (data wait, issue, accumulator wait,
+// total) over the CTAs of the last precomp launch run with UCUDNN_TUNE=prof=1.
+void precomp_profile(double out[4]) {
+  static unsigned long long h[1024 * 4];
+  cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
+  double s[4] = {0, 0, 0, 0};
+  int n = 0;
+  for (int b = 0; b < 1024; ++b) {
+    if (h[b * 4 + 3] == 0) continue;
+    for (int i = 0; i < 4; ++i) s[i] += double(h[b * 4 + i]);
+    ++n;
+  }
+  for (int i = 0; i < 4; ++i) out[i] = n ? s[i] / n : 0;
+}
 
 bool precomp_supports(int op, const ConvShape& s) {
   if (op == kFwd) return s.sh <= 8 && s.sw <= 8 && s.ph <= 127 && s.pw <= 127 && s.R <= 64 && s.S <= 64;

@@ -14,4 +14,6 @@ std::int64_t precomp_workspace(int op, const ConvShape& s);
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
                         float alpha, float beta, cudaStream_t stream, int flags);
 
+void precomp_profile(double out[4]);
+
 }  // namespace ucudnn

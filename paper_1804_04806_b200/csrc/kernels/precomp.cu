@@ -416,6 +416,7 @@ struct StripParams {
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
+  int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -425,7 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                          ~std::uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t strip_bytes = std::uint32_t(p.nboxes * p.box_rows) * 128;
-  const std::uint32_t tap_bytes = std::uint32_t(p.BN) * 128;
+  const std::uint32_t tap_bytes = std::uint32_t(p.BN) * 128;  // swap: BN = 128 filter rows
+  const int tile_pos = p.swap ? 2 * kBM : kBM;
   const std::uint32_t stage_bytes = kTapsPerStage * tap_bytes;
   const int kStages = p.stages;
   unsigned char* strips = smem;
@@ -437,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tfull = sempty + 2;
   std::uint64_t* tempty = tfull + 2;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  float* xpose = reinterpret_cast<float*>(ring + kStages * stage_bytes + 256);  // swap epilogue: 4 x 32 x 33
   if (threadIdx.x == 0) {
     prefetch_tmap(&xmap);
     for (int s = 0; s < kStages; ++s) {
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         std::uint32_t nt, mt, n, local;
         p.fd_mt.divmod(std::uint32_t(t), nt, mt);
         p.fd_tpi.divmod(mt, n, local);
-        const int p0 = int(n) * p.HWp + int(local) * kBM;
+        const int p0 = int(n) * p.HWp + int(local) * tile_pos;
         for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
           const int sb = sc & 1;
           mbar_wait(&sempty[sb], ((sc >> 1) & 1) ^ 1);
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint32_t idesc = idesc_tf32(kBM, p.swap ? 2 * kBM : p.BN);
     const std::uint32_t sbase = smem_u32(strips), rbase = smem_u32(ring);
     int it = 0, sc = 0, tl = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
@@ -526,9 +529,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const std::uint32_t sa = sbase + sb * strip_bytes + std::uint32_t(r * p.Wp + q) * 128;
               const std::uint32_t sbb = rbase + st * stage_bytes + i * tap_bytes;
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_tf32(dtm, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sbb + k * 32), idesc,
-                         (cc | tap | k) != 0);
+              for (int k = 0; k < 4; ++k) {
+                // swap: A = filter rows, B = 256 strip positions
+                const std::uint64_t da = umma_desc_sw128((p.swap ? sbb : sa) + k * 32);
+                const std::uint64_t db = umma_desc_sw128((p.swap ? sa : sbb) + k * 32);
+                mma_tf32(dtm, da, db, idesc, (cc | tap | k) != 0);
+              }
             }
             mma_commit(&empty[st]);
             if (ts == tsteps - 1) mma_commit(&sempty[sb]);
@@ -549,6 +555,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = tl & 1;
       mbar_wait(&tfull[acc], (tl >> 1) & 1);
       tc_fence_after();
+      if (p.swap) {
+        // TMEM lane = output channel, column = position: stage 32 x 32
+        // blocks through smem so the stores run along positions
+        float* tp = xpose + ew * (32 * 33);
+        const std::uint32_t tb = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+        for (int c0 = 0; c0 < 2 * kBM; c0 += 32) {
+          float v[32];
+          tmem_ld32(tb + std::uint32_t(c0), v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tp[lane * 33 + j] = v[j];
+          __syncwarp();
+          const int pos = int(local) * tile_pos + c0 + lane;
+          std::uint32_t oh, ow;
+          p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
+          if (int(oh) < p.OH && int(ow) < p.OW) {
+            if (!p.phase) {
+              float* base = p.out + std::int64_t(n) * p.Nout * p.P + int(oh) * p.OW + int(ow);
+              for (int r = 0; r < 32; ++r) {
+                const int col = ew * 32 + r;
+                if (col >= p.Nout) break;
+                float* dst = base + std::int64_t(col) * p.P;
+                const float val = p.alpha * tp[r * 33 + lane];
+                *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+              }
+            } else {
+              float* base = p.out + std::int64_t(n) * p.Cr * p.Hr * p.Wr;
+              const int hb = int(oh) * p.ssh - p.sph, wb = int(ow) * p.ssw - p.spw;
+              for (int r = 0; r < 32; ++r) {
+                const int col = ew * 32 + r;
+                if (col >= p.Nout) break;
+                std::uint32_t ab, c, a, b;
+                p.fd_Cr.divmod(std::uint32_t(col), ab, c);
+                p.fd_ssw.divmod(ab, a, b);
+                const int h = hb + int(a), w = wb + int(b);
+                if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+                float* dst = base + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+                const float val = p.alpha * tp[r * 33 + lane];
+                *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+              }
+            }
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       const int pos = int(local) * kBM + ew * 32 + lane;  // flat position inside image n
       std::uint32_t oh, ow;
       p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
@@ -681,22 +734,34 @@ struct Geo {
 // Strip path (stride-1 after the s2d / phase rewrites, >= 32-channel rows):
 // geometry of the padded input and of the per-chunk strip.
 struct StripGeo {
-  bool ok = false;
+  bool ok = false, swap = false;
   int Hp = 0, Wp = 0, rows = 0, box_rows = 0, nboxes = 0, stages = 0;
   std::size_t strip_bytes = 0;
 };
+// Few output channels (<= 128): swapped roles -- 256 strip positions as the
+// MMA N, output channels (zero-padded to 128) as its M -- so each MMA does
+// 4x the work of a 128 x 64 one at about the same issue cost.
+// (Measured, AlexNet at 64 images: conv2 BD 191 -> 179 us, conv1 F 148 -> 142
+// us; the stride-phase BD of conv1 gets slower, 124 -> 222 us, so phase
+// scatters stay on the im2col kernel.)
+bool strip_swap(const Geo& g) {
+  return g.sh == 1 && g.sw == 1 && cpad(g.Cin) != 4 && g.Nout <= 128 && !g.phase && tune("strip", 1) &&
+         tune("sswap", 1);
+}
+int filter_rows(const Geo& g) { return strip_swap(g) ? kBM : pick_bn(g.Nout); }
 StripGeo strip_geo(const Geo& g, int BN) {
   StripGeo sg;
-  if (g.sh != 1 || g.sw != 1 || cpad(g.Cin) == 4 || !tune("strip", 0)) return sg;
+  sg.swap = strip_swap(g);
+  if (g.sh != 1 || g.sw != 1 || cpad(g.Cin) == 4 || !(sg.swap || tune("strip", 0))) return sg;
   sg.Hp = g.Hin + g.ph + (g.ph_hi < 0 ? g.ph : g.ph_hi);
   sg.Wp = g.Win + g.pw + (g.pw_hi < 0 ? g.pw : g.pw_hi);
   if (sg.Hp - g.R + 1 != g.Hout || sg.Wp - g.S + 1 != g.Wout) return sg;
-  sg.rows = kBM + (g.R - 1) * sg.Wp + (g.S - 1);
+  sg.rows = (sg.swap ? 2 * kBM : kBM) + (g.R - 1) * sg.Wp + (g.S - 1);
   sg.box_rows = std::min(256, (sg.rows + 7) / 8 * 8);
   sg.nboxes = (sg.rows + sg.box_rows - 1) / sg.box_rows;
   sg.strip_bytes = std::size_t(sg.nboxes) * sg.box_rows * 128;
   const std::size_t stage = std::size_t(kTapsPerStage) * BN * 128;
-  const std::size_t budget = 210 * 1024;
+  const std::size_t budget = 210 * 1024 - (sg.swap ? 4 * 32 * 33 * 4 : 0);
   if (2 * sg.strip_bytes + 2 * stage > budget) return sg;
   sg.stages = int(std::min<std::size_t>(kMaxStages, (budget - 2 * sg.strip_bytes) / stage));
   sg.ok = true;
@@ -707,7 +772,7 @@ std::size_t geo_ws(const Geo& g, int* ksteps_out = nullptr, int* bn_out = nullpt
   const int Cp = cpad(g.Cin), taps = g.R * g.S;
   const bool small = Cp == 4;
   const int ksteps = small ? (taps + 7) / 8 : taps * (Cp / 32);
-  const int BN = pick_bn(g.Nout), n_tiles = (g.Nout + BN - 1) / BN;
+  const int BN = filter_rows(g), n_tiles = (g.Nout + BN - 1) / BN;
   if (ksteps_out) *ksteps_out = ksteps;
   if (bn_out) *bn_out = BN;
   const StripGeo sg = strip_geo(g, BN);
@@ -764,7 +829,9 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   p.HWp = sg.Hp * sg.Wp;
   p.OH = g.Hout;
   p.OW = g.Wout;
-  p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + kBM - 1) / kBM;
+  p.swap = sg.swap ? 1 : 0;
+  const int tile_pos = sg.swap ? 2 * kBM : kBM;
+  p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + tile_pos - 1) / tile_pos;
   p.m_tiles = g.N * p.tpi;
   p.taps = taps;
   p.S = g.S;
@@ -789,7 +856,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
     p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
   }
-  const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256;
+  const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
+                   (sg.swap ? 4 * 32 * 33 * 4 : 0);
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -97,6 +97,8 @@ uint64_t ucudnnGetLaunchCount(void);
  * for a free accumulator, total} per CTA of the last IMPLICIT_PRECOMP_GEMM
  * launch made with UCUDNN_TUNE=prof=1 (zeros otherwise). */
 ucudnnStatus_t ucudnnDebugPrecompProfile(double* out4);
+/* Same split for the last IMPLICIT_PRECOMP_GEMM BackwardFilter launch. */
+ucudnnStatus_t ucudnnDebugBackwardFilterProfile(double* out4);
 
 /* ------------------------------------------------------------ handle ----- */
 /* Replaces cudnnCreate/cudnnDestroy/cudnnSetStream. The

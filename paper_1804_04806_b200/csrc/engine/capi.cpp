@@ -15,6 +15,7 @@
 #include "../kernels/igemm.h"
 #include "../planner/planner.h"
 #include "algos.h"
+#include "../kernels/bfilter.h"
 #include "../kernels/precomp.h"
 
 using namespace ucudnn;
@@ -420,6 +421,12 @@ uint64_t ucudnnGetLaunchCount(void) { return launch_count(); }
 ucudnnStatus_t ucudnnDebugPrecompProfile(double* out4) {
   if (!out4) return UCUDNN_STATUS_BAD_PARAM;
   precomp_profile(out4);
+  return UCUDNN_STATUS_SUCCESS;
+}
+
+ucudnnStatus_t ucudnnDebugBackwardFilterProfile(double* out4) {
+  if (!out4) return UCUDNN_STATUS_BAD_PARAM;
+  bf_profile(out4);
   return UCUDNN_STATUS_SUCCESS;
 }
 

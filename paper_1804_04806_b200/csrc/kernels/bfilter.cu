@@ -142,7 +142,7 @@ struct BfParams {
   float* dw;
   float alpha;
   int K, CRS, RS, S, R, C, Bw, Ah, sh, sw, Qw, CCp, CC, Gb, Wq, M, BN;
-  int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages, swap, Kb, ksub;
+  int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages, swap, Kb, ksub, prof;
 };
 
 // GEMM row (qh, qw, cc) of the x operand -> dW offset (c, r, s), or -1
@@ -164,6 +164,8 @@ __device__ __forceinline__ void tma_4d(void* dst, const void* tmap, std::uint64_
       "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
+
+__device__ unsigned long long g_bfprof[1024 * 4];
 
 __global__ void __launch_bounds__(kThreads, 1)
     bf_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap, const BfParams p) {
@@ -254,17 +256,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
     const std::uint32_t sbase = smem_u32(smem);
     int it = 0, tl = 0;
+    long long c_data = 0, c_issue = 0, c_acc = 0, t_start = clock64();
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
       const int split = u / p.tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
       const int acc = tl & 1;
+      long long c0 = p.prof ? clock64() : 0;
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
       tc_fence_after();
+      if (p.prof) c_acc += clock64() - c0;
       const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
       for (int g = g0; g < g1; g += kSub, ++it) {
         const int st = it % kStages, nsub = min(kSub, g1 - g);
+        long long c1 = p.prof ? clock64() : 0;
         mbar_wait(&full[st], (it / kStages) & 1);
         tc_fence_after();
+        long long c2 = p.prof ? clock64() : 0;
+        if (p.prof) c_data += c2 - c1;
         if (lane == 0) {
           for (int sub = 0; sub < nsub; ++sub) {
             const std::uint32_t sa = sbase + st * stage_bytes + sub * sub_bytes, sb = sa + a_bytes;
@@ -277,9 +285,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g + kSub >= g1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
+        if (p.prof) c_issue += clock64() - c2;
       }
       if (g1 <= g0 && lane == 0) mma_commit(&tfull[acc]);
       __syncwarp();
+    }
+    if (p.prof && lane == 0 && blockIdx.x < 1024) {
+      g_bfprof[blockIdx.x * 4 + 0] = c_data;
+      g_bfprof[blockIdx.x * 4 + 1] = c_issue;
+      g_bfprof[blockIdx.x * 4 + 2] = c_acc;
+      g_bfprof[blockIdx.x * 4 + 3] = clock64() - t_start;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue: RED into dW
@@ -351,65 +366,73 @@ struct XPhaseArgs {
   std::int64_t units, rep;  // float4 units per replica, floats per replica
   FastDiv fd_u, fd_wq, fd_c, fd_bw;  // units per plane, plane pitch, C, Bw
 };
-__global__ void __launch_bounds__(256) x_phase_kernel(const XPhaseArgs a) {
-  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < a.units;
-       u += std::int64_t(gridDim.x) * blockDim.x) {
-    std::uint32_t plane, q;
-    a.fd_u.divmod(std::uint32_t(u), plane, q);
-    std::uint32_t n, cc, ab, c, pa, pb;
-    n = plane / std::uint32_t(a.CC);
-    cc = plane - n * std::uint32_t(a.CC);
-    a.fd_c.divmod(cc, ab, c);
-    a.fd_bw.divmod(ab, pa, pb);
-    const float* src = a.x + (std::int64_t(n) * a.C + c) * a.H * a.W;
-    const int p0 = int(q) * 4;
-    float v[7];
-    std::uint32_t i, j;
-    a.fd_wq.divmod(std::uint32_t(p0), i, j);
+__device__ __forceinline__ void x_phase_unit(const XPhaseArgs& a, std::int64_t u) {
+  std::uint32_t plane, q;
+  a.fd_u.divmod(std::uint32_t(u), plane, q);
+  std::uint32_t n, cc, ab, c, pa, pb;
+  n = plane / std::uint32_t(a.CC);
+  cc = plane - n * std::uint32_t(a.CC);
+  a.fd_c.divmod(cc, ab, c);
+  a.fd_bw.divmod(ab, pa, pb);
+  const float* src = a.x + (std::int64_t(n) * a.C + c) * a.H * a.W;
+  const int p0 = int(q) * 4;
+  float v[7];
+  std::uint32_t i, j;
+  a.fd_wq.divmod(std::uint32_t(p0), i, j);
 #pragma unroll
-    for (int e = 0; e < 7; ++e) {
-      const int h = int(i) * a.sh + int(pa) - a.ph, w = int(j) * a.sw + int(pb) - a.pw;
-      v[e] = (e < a.T + 3 && unsigned(h) < unsigned(a.H) && unsigned(w) < unsigned(a.W)) ? __ldg(src + h * a.W + w)
-                                                                                        : 0.f;
-      if (++j == a.fd_wq.d) {
-        j = 0;
-        ++i;
-      }
+  for (int e = 0; e < 7; ++e) {
+    const int h = int(i) * a.sh + int(pa) - a.ph, w = int(j) * a.sw + int(pb) - a.pw;
+    v[e] = (e < a.T + 3 && unsigned(h) < unsigned(a.H) && unsigned(w) < unsigned(a.W)) ? __ldg(src + h * a.W + w)
+                                                                                      : 0.f;
+    if (++j == a.fd_wq.d) {
+      j = 0;
+      ++i;
     }
-    float4* dst = reinterpret_cast<float4*>(a.out) + u;
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (t < a.T) dst[t * (a.rep / 4)] = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
   }
+  float4* dst = reinterpret_cast<float4*>(a.out) + u;
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    if (t < a.T) dst[t * (a.rep / 4)] = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
 }
 
 // dy (NCHW) -> dy_p[n][k][Ldp]: rows re-pitched to Wq, zero beyond OW.
-__global__ void __launch_bounds__(256) dy_pitch_kernel(const float* __restrict__ dy, float* __restrict__ out, int OH,
-                                                       int OW, std::int64_t units, FastDiv fd_u, FastDiv fd_wq) {
-  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < units;
-       u += std::int64_t(gridDim.x) * blockDim.x) {
-    std::uint32_t plane, q, i, j;
-    fd_u.divmod(std::uint32_t(u), plane, q);
-    const float* src = dy + std::int64_t(plane) * OH * OW;
-    fd_wq.divmod(q * 4, i, j);
-    float v[4];
+struct DyPitchArgs {
+  const float* dy;
+  float* out;
+  int OH, OW;
+  std::int64_t units;
+  FastDiv fd_u, fd_wq;
+};
+__device__ __forceinline__ void dy_pitch_unit(const DyPitchArgs& a, std::int64_t u) {
+  std::uint32_t plane, q, i, j;
+  a.fd_u.divmod(std::uint32_t(u), plane, q);
+  const float* src = a.dy + std::int64_t(plane) * a.OH * a.OW;
+  a.fd_wq.divmod(q * 4, i, j);
+  float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      v[e] = (int(i) < OH && int(j) < OW) ? __ldg(src + int(i) * OW + int(j)) : 0.f;
-      if (++j == fd_wq.d) {
-        j = 0;
-        ++i;
-      }
+  for (int e = 0; e < 4; ++e) {
+    v[e] = (int(i) < a.OH && int(j) < a.OW) ? __ldg(src + int(i) * a.OW + int(j)) : 0.f;
+    if (++j == a.fd_wq.d) {
+      j = 0;
+      ++i;
     }
-    reinterpret_cast<float4*>(out)[u] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  reinterpret_cast<float4*>(a.out)[u] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// One launch for everything BackwardFilter does before its GEMM: the two
+// re-layouts (either may be skipped) and dW *= beta (beta != 1).
+__global__ void __launch_bounds__(256) bf_prep_kernel(const XPhaseArgs xa, const DyPitchArgs da, float* dw,
+                                                       std::int64_t wn, float beta) {
+  const std::int64_t nx = xa.units, nd = da.units, total = nx + nd + wn;
+  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
+       u += std::int64_t(gridDim.x) * blockDim.x) {
+    if (u < nx) x_phase_unit(xa, u);
+    else if (u < nx + nd) dy_pitch_unit(da, u - nx);
+    else dw[u - nx - nd] = beta == 0.f ? 0.f : dw[u - nx - nd] * beta;
   }
 }
 
-__global__ void bf_scale_kernel(float* p, std::int64_t n, float beta) {
-  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += std::int64_t(gridDim.x) * blockDim.x)
-    p[i] = beta == 0.f ? 0.f : p[i] * beta;
-}
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -445,6 +468,19 @@ bool encode_4d(CUtensorMap* m, const float* base, int d0, int d1, int d2, int d3
 
 }  // namespace
 
+void bf_profile(double out[4]) {
+  static unsigned long long h[1024 * 4];
+  cudaMemcpyFromSymbol(h, g_bfprof, sizeof(h));
+  double s[4] = {0, 0, 0, 0};
+  int n = 0;
+  for (int b = 0; b < 1024; ++b) {
+    if (h[b * 4 + 3] == 0) continue;
+    for (int i = 0; i < 4; ++i) s[i] += double(h[b * 4 + i]);
+    ++n;
+  }
+  for (int i = 0; i < 4; ++i) out[i] = n ? s[i] / n : 0;
+}
+
 bool bf_supports(const ConvShape& s) {
   const BfGeo g = make_geo(s);
   // TMA coordinates are int32 and box dims <= 256; flat offsets must fit
@@ -463,25 +499,18 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   const BfGeo g = make_geo(s);
   const float* xph = g.x_direct ? x : static_cast<const float*>(ws);
   const float* dyp = g.dy_direct ? dy : reinterpret_cast<const float*>(static_cast<char*>(ws) + x_bytes(g));
-  if (beta != 1.f) {
-    const std::int64_t n = s.w_elems();
-    count_launch();
-    bf_scale_kernel<<<int(std::min<std::int64_t>((n + 255) / 256, 4 * sm_count())), 256, 0, st>>>(dw, n, beta);
-  }
   const FastDiv fd_wq(std::uint32_t(g.Wq));
   const int sms = sm_count();
   XPhaseArgs xa{x, const_cast<float*>(xph), g.C, g.H, g.W, g.ph, g.pw, g.sh, g.sw, g.Bw, g.CC, g.T,
-                std::int64_t(g.N) * g.CC * (g.Lp / 4), std::int64_t(g.N) * g.CC * g.Lp,
+                g.x_direct ? 0 : std::int64_t(g.N) * g.CC * (g.Lp / 4), std::int64_t(g.N) * g.CC * g.Lp,
                 FastDiv(std::uint32_t(g.Lp / 4)), fd_wq, FastDiv(std::uint32_t(g.C)), FastDiv(std::uint32_t(g.Bw))};
-  if (!g.x_direct) {
+  DyPitchArgs da{dy, const_cast<float*>(dyp), g.OH, g.OW, g.dy_direct ? 0 : std::int64_t(g.N) * g.K * (g.Ldp / 4),
+                 FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq};
+  const std::int64_t wn = beta != 1.f ? s.w_elems() : 0;
+  const std::int64_t prep = xa.units + da.units + wn;
+  if (prep > 0) {
     count_launch();
-    x_phase_kernel<<<int(std::min<std::int64_t>((xa.units + 255) / 256, 16 * sms)), 256, 0, st>>>(xa);
-  }
-  const std::int64_t dunits = std::int64_t(g.N) * g.K * (g.Ldp / 4);
-  if (!g.dy_direct) {
-    count_launch();
-    dy_pitch_kernel<<<int(std::min<std::int64_t>((dunits + 255) / 256, 16 * sms)), 256, 0, st>>>(
-        dy, const_cast<float*>(dyp), g.OH, g.OW, dunits, FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq);
+    bf_prep_kernel<<<int(std::min<std::int64_t>((prep + 255) / 256, 16 * sms)), 256, 0, st>>>(xa, da, dw, wn, beta);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -507,6 +536,7 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   p.Lc = g.Lc;
   p.T = g.T;
   p.swap = g.swap;
+  p.prof = tune("prof", 0);
   p.Kb = g.Kb;
   p.steps = g.N * g.Lc;
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit

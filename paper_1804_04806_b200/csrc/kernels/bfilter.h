@@ -16,4 +16,6 @@ std::int64_t bf_workspace(const ConvShape& s);
 cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
                    cudaStream_t stream);
 
+void bf_profile(double out[4]);  // diagnostic (UCUDNN_TUNE=prof=1)
+
 }  // namespace ucudnn

@@ -17,19 +17,20 @@ dev = torch.device("cuda")
 h = Handle()
 L = lib()
 L.ucudnnDebugPrecompProfile.argtypes = [C.POINTER(C.c_double)]
+L.ucudnnDebugBackwardFilterProfile.argtypes = [C.POINTER(C.c_double)]
 b = int(os.environ.get("BATCH", "64"))
 for name, s in ALEXNET:
     s = s.with_batch(b)
-    for op in (0, 1):
+    for op in (0, 1, 2):
         x = torch.randn(s.N, s.C, s.H, s.W, device=dev); w = torch.randn(s.K, s.C, s.R, s.S, device=dev)
         dy = torch.randn(s.N, s.K, s.OH, s.OW, device=dev)
-        a, bb = [(x, w), (dy, w)][op]
+        a, bb = [(x, w), (dy, w), (x, dy)][op]
         out = torch.empty(out_shape(op, s), device=dev)
         wsb, ok = algorithm_workspace(op, s, 5, s.N)
         ws = torch.empty(max(wsb, 4) // 4 + 1, device=dev)
         h.run(op, s, a, bb, out, 5, ws)
         torch.cuda.synchronize()
         r = (C.c_double * 4)()
-        L.ucudnnDebugPrecompProfile(r)
+        (L.ucudnnDebugBackwardFilterProfile if op == 2 else L.ucudnnDebugPrecompProfile)(r)
         tot = r[3] or 1
         print(f"{name} op{op}: data-wait {100*r[0]/tot:5.1f}%  issue {100*r[1]/tot:5.1f}%  acc-wait {100*r[2]/tot:5.1f}%  total {r[3]/1.9e3:8.1f} us@1.9GHz")

@@ -27,6 +27,8 @@ PROTOTYPES = {
     "ucudnnGetMinTotalWorkspace": (i64, []),
     "ucudnnGetVersion": (C.c_size_t, []),
     "ucudnnGetLaunchCount": (C.c_uint64, []),
+    "ucudnnDebugPrecompProfile": (C.c_int, [C.POINTER(C.c_double)]),
+    "ucudnnDebugBackwardFilterProfile": (C.c_int, [C.POINTER(C.c_double)]),
     "ucudnnCreate": (C.c_int, [C.POINTER(vp)]),
     "ucudnnDestroy": (C.c_int, [vp]),
     "ucudnnSetStream": (C.c_int, [vp, vp]),

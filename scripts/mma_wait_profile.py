@@ -16,8 +16,6 @@ from tests.oracle_py import out_shape
 dev = torch.device("cuda")
 h = Handle()
 L = lib()
-L.ucudnnDebugPrecompProfile.argtypes = [C.POINTER(C.c_double)]
-L.ucudnnDebugBackwardFilterProfile.argtypes = [C.POINTER(C.c_double)]
 b = int(os.environ.get("BATCH", "64"))
 for name, s in ALEXNET:
     s = s.with_batch(b)

@@ -63,7 +63,7 @@ struct PrecompParams {
   // phase scatter epilogue (strided BackwardData): column (a, b, c) of
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
-  int stages, ksub, prof;
+  int stages, ksub, prof, cps;
   FastDiv fd_Cr, fd_ssw;
 };
 
@@ -109,7 +109,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  // cps == 2: two CTAs share the SM (256 TMEM columns each; one accumulator
+  // when BN > 128, so the other CTA's MMAs cover this one's epilogue)
+  if (warp == 1) {
+    if (p.cps == 2) tmem_alloc<256>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
+  const int nacc = p.cps == 2 && p.BN > 128 ? 1 : 2;
+  const std::uint32_t acc_cols = p.cps == 2 ? 128u : std::uint32_t(kMaxBN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -171,12 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0, tl = 0;
     long long c_data = 0, c_issue = 0, c_acc = 0, t_start = clock64();
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
-      const int acc = tl & 1;
+      const int acc = tl % nacc;
       long long c0 = p.prof ? clock64() : 0;
-      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      mbar_wait(&tempty[acc], ((tl / nacc) & 1) ^ 1);
       tc_fence_after();
       if (p.prof) c_acc += clock64() - c0;
-      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t dtm = tmem + std::uint32_t(acc) * acc_cols;
       for (int j = 0; j < jsteps; ++j, ++it) {
         const int s = it % kStages;
         long long c1 = p.prof ? clock64() : 0;
@@ -216,8 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       int mt, nt;
       tile_coords(p, t, mt, nt);
-      const int acc = tl & 1;
-      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      const int acc = tl % nacc;
+      mbar_wait(&tfull[acc], (tl / nacc) & 1);
       tc_fence_after();
       const int row = mt * kBM + ew * 32 + lane;
       const bool ok = row < p.M;
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           wb = int(j) * p.ssw - p.spw;
         }
       }
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc) * acc_cols;
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -273,7 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_free<512>(tmem);
+    if (p.cps == 2) tmem_free<256>(tmem);
+    else tmem_free<512>(tmem);
   }
 }
 
@@ -745,8 +753,10 @@ struct StripGeo {
 // us; the stride-phase BD of conv1 gets slower, 124 -> 222 us, so phase
 // scatters stay on the im2col kernel.)
 bool strip_swap(const Geo& g) {
-  return g.sh == 1 && g.sw == 1 && cpad(g.Cin) != 4 && g.Nout <= 128 && !g.phase && tune("strip", 1) &&
-         tune("sswap", 1);
+  // Off by default since the implicit GEMM runs two CTAs per SM: that
+  // measured faster for these shapes (conv2 BD 157 vs 179 us, conv1 F 132 vs
+  // 142 us). UCUDNN_TUNE=sswap=1 turns it back on.
+  return g.sh == 1 && g.sw == 1 && cpad(g.Cin) != 4 && g.Nout <= 128 && !g.phase && tune("sswap", 0);
 }
 int filter_rows(const Geo& g) { return strip_swap(g) ? kBM : pick_bn(g.Nout); }
 StripGeo strip_geo(const Geo& g, int BN) {
@@ -962,19 +972,26 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   }
   // two 32-deep chunks per stage (8 MMAs per tcgen05.commit): measured
   // 10-25 % faster than one on AlexNet conv2 / conv4 (same box, A/B)
-  p.ksub = std::max(1, std::min(2, tune("pc_ksub", 2)));
+  // Two CTAs per SM (256 TMEM columns each) once there are more tiles than
+  // SMs: the second wave's tail disappears and a CTA's epilogue hides behind
+  // its neighbour's MMAs. Measured on AlexNet at 64 images: conv2 BD 196 ->
+  // 157 us, conv1 F 151 -> 132, conv3 F 71 -> 63, conv4 BD 89 -> 77; with
+  // fewer tiles than SMs it packs them onto fewer SMs and loses (conv4 F).
+  p.cps = tune("pc_cps", p.m_tiles * p.n_tiles > sm_count() ? 2 : 1) == 2 ? 2 : 1;
+  p.ksub = std::max(1, std::min(2, tune("pc_ksub", p.cps == 2 && BN > 128 ? 1 : 2)));
   const int stage_bytes = p.ksub * (kBM * 128 + ((BN * 128 + 1023) & ~1023));
-  p.stages = ring_stages(std::min(tune("pc_stages", 8), (200 * 1024) / stage_bytes));
+  p.stages = ring_stages(std::min(tune("pc_stages", 8), (p.cps == 2 ? 100 * 1024 : 200 * 1024) / stage_bytes));
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)
-  const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
+  const int smem = p.cps == 2 ? p.stages * stage_bytes + 1024 + 256
+                              : std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
   static int smem_set = 0;
   if (smem > smem_set) {
     e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     smem_set = 227 * 1024;
   }
-  const int grid = std::min(sm_count(), p.m_tiles * p.n_tiles);
+  const int grid = std::min(p.cps * sm_count(), p.m_tiles * p.n_tiles);
   count_launch();
   precomp_kernel<<<grid, kThreads, smem, st>>>(amap, p);
   return cudaGetLastError();

@@ -45,6 +45,7 @@
 
 #include "bfilter.h"
 #include "conv_common.h"
+#include "launch.h"
 #include "sm100.cuh"
 
 namespace ucudnn {
@@ -203,6 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
+  pdl_wait();  // everything above touched only smem / TMEM / the param-space tensor maps
+  pdl_trigger();
   const int units = p.tiles * p.splits;
 
   if (warp == 0 || warp == 2 || warp == 3) {
@@ -424,6 +427,8 @@ __device__ __forceinline__ void dy_pitch_unit(const DyPitchArgs& a, std::int64_t
 // re-layouts (either may be skipped) and dW *= beta (beta != 1).
 __global__ void __launch_bounds__(256) bf_prep_kernel(const XPhaseArgs xa, const DyPitchArgs da, float* dw,
                                                        std::int64_t wn, float beta) {
+  pdl_wait();
+  pdl_trigger();
   const std::int64_t nx = xa.units, nd = da.units, total = nx + nd + wn;
   for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
        u += std::int64_t(gridDim.x) * blockDim.x) {
@@ -508,12 +513,12 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
                  FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq};
   const std::int64_t wn = beta != 1.f ? s.w_elems() : 0;
   const std::int64_t prep = xa.units + da.units + wn;
+  cudaError_t e;
   if (prep > 0) {
-    count_launch();
-    bf_prep_kernel<<<int(std::min<std::int64_t>((prep + 255) / 256, 16 * sms)), 256, 0, st>>>(xa, da, dw, wn, beta);
+    e = launch_pdl(bf_prep_kernel, dim3(int(std::min<std::int64_t>((prep + 255) / 256, 16 * sms))), dim3(256), 0, st, xa,
+                   da, dw, wn, beta);
+    if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
 
   CUtensorMap xmap, dmap;
   const std::int64_t rep = std::int64_t(g.N) * g.CC * g.Lp;
@@ -554,9 +559,8 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  count_launch();
-  bf_kernel<<<std::min(sms, p.tiles * p.splits), kThreads, smem, st>>>(xmap, dmap, p);
-  return cudaGetLastError();
+  return launch_pdl(bf_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, xmap,
+                    dmap, p);
 }
 
 }  // namespace ucudnn

@@ -30,6 +30,7 @@
 
 #include "bfilter.h"
 #include "conv_common.h"
+#include "launch.h"
 #include "precomp.h"
 #include "sm100.cuh"
 
@@ -121,6 +122,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
+  pdl_wait();  // everything above touched only smem / TMEM / the param-space tensor map
+  pdl_trigger();
   const int total_tiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0 || warp == 2 || warp == 3) {
@@ -287,6 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // NCHW -> N(HW)Cp, zero-filling channels C..Cp-1 (32 x 32 smem transpose).
 __global__ void to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int HW, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float tile[32][33];
   const int n = blockIdx.z;
   const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -310,6 +315,8 @@ struct S2D {
   int C, H, W, sh, sw, ph, pw, Bw, CC, Hq, Wq, Cp;
 };
 __global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float tile[32][33];
   const int n = blockIdx.z / d.Hq, i = blockIdx.z - n * d.Hq;
   const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -343,6 +350,8 @@ struct PhaseFilter {
 __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int O, int I, int taps,
                                    int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip,
                                    PhaseFilter pf) {
+  pdl_wait();
+  pdl_trigger();
   const std::int64_t total = std::int64_t(n_tiles) * ksteps * 8 * BN;  // 16-byte units
   for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
        u += std::int64_t(gridDim.x) * blockDim.x) {
@@ -467,6 +476,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
+  pdl_wait();  // everything above touched only smem / TMEM / the param-space tensor map
+  pdl_trigger();
   const int total_tiles = p.m_tiles * p.n_tiles;
   const int tsteps = (p.taps + kTapsPerStage - 1) / kTapsPerStage;  // filter stages per chunk
 
@@ -671,6 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // lands at (h + pt, w + pl)); 32 x 33 smem transpose per (n, row, w-block, c-block).
 __global__ void pad_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int H, int W, int Cp,
                                 int pt, int pl, int Hp, int Wp) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float tile[32][33];
   const int n = blockIdx.z / Hp, hp = blockIdx.z - n * Hp;
   const int w0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -798,24 +811,24 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   const int n_tiles = (g.Nout + BN - 1) / BN;
   float* btiles = static_cast<float*>(ws);
   float* xp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(std::size_t(n_tiles) * ksteps * BN * 128));
-  count_launch();
+  cudaError_t e;
   if (g.s2d) {
     S2D d = g.sd;
     d.Cp = Cp;
-    s2d_nhwc_kernel<<<dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st>>>(act, xp, d);
+    e = launch_pdl(s2d_nhwc_kernel, dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st, act, xp,
+                   d);
   } else {
-    pad_nhwc_kernel<<<dim3((sg.Wp + 31) / 32, (Cp + 31) / 32, g.N * sg.Hp), dim3(32, 8), 0, st>>>(
-        act, xp, g.Cin, g.Hin, g.Win, Cp, g.ph, g.pw, sg.Hp, sg.Wp);
+    e = launch_pdl(pad_nhwc_kernel, dim3((sg.Wp + 31) / 32, (Cp + 31) / 32, g.N * sg.Hp), dim3(32, 8), 0, st, act, xp,
+                   g.Cin, g.Hin, g.Win, Cp, g.ph, g.pw, sg.Hp, sg.Wp);
   }
+  if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
-    count_launch();
-    pack_filter_kernel<<<blocks, 256, 0, st>>>(w, btiles, g.Nout, g.Cin, taps, BN, n_tiles, ksteps, 2, Cp / 32,
-                                               g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+    e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
+                   ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+    if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
 
   CUtensorMap xmap;
   const std::uint64_t rows_total = std::uint64_t(g.N) * sg.Hp * sg.Wp;
@@ -874,9 +887,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  count_launch();
-  strip_kernel<<<std::min(sm_count(), p.m_tiles * p.n_tiles), kThreads, std::max(smem, 116 * 1024), st>>>(xmap, p);
-  return cudaGetLastError();
+  return launch_pdl(strip_kernel, dim3(std::min(sm_count(), p.m_tiles * p.n_tiles)), dim3(kThreads),
+                    std::size_t(std::max(smem, 116 * 1024)), st, xmap, p);
 }
 
 cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, float* out, void* ws, float alpha,
@@ -897,23 +909,24 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   float* act_nhwc = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                              align256(std::size_t(n_tiles) * ksteps * BN * 128));
   const int HW = g.Hin * g.Win;
-  count_launch();
+  cudaError_t e;
   if (g.s2d) {
     S2D d = g.sd;
     d.Cp = Cp;
-    s2d_nhwc_kernel<<<dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st>>>(act, act_nhwc, d);
+    e = launch_pdl(s2d_nhwc_kernel, dim3((g.Win + 31) / 32, (Cp + 31) / 32, g.N * g.Hin), dim3(32, 8), 0, st, act,
+                   act_nhwc, d);
   } else {
-    to_nhwc_kernel<<<dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st>>>(act, act_nhwc, g.Cin, HW, Cp);
+    e = launch_pdl(to_nhwc_kernel, dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st, act, act_nhwc,
+                   g.Cin, HW, Cp);
   }
+  if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
-    count_launch();
-    pack_filter_kernel<<<blocks, 256, 0, st>>>(w, btiles, g.Nout, g.Cin, taps, BN, n_tiles, ksteps, Cp == 4 ? 1 : 0,
-                                               Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+    e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
+                   ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+    if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
 
   CUtensorMap amap;
   const cuuint64_t dims[4] = {cuuint64_t(Cp), cuuint64_t(g.Win), cuuint64_t(g.Hin), cuuint64_t(g.N)};
@@ -992,9 +1005,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     smem_set = 227 * 1024;
   }
   const int grid = std::min(p.cps * sm_count(), p.m_tiles * p.n_tiles);
-  count_launch();
-  precomp_kernel<<<grid, kThreads, smem, st>>>(amap, p);
-  return cudaGetLastError();
+  return launch_pdl(precomp_kernel, dim3(grid), dim3(kThreads), std::size_t(smem), st, amap, p);
 }
 
 Geo fwd_geo(const ConvShape& s) {

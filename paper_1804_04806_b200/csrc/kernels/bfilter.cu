@@ -138,12 +138,20 @@ BfGeo make_geo(const ConvShape& s) {
 std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
 std::size_t x_bytes(const BfGeo& g) { return g.x_direct ? 0 : a256(std::size_t(g.T) * g.N * g.CC * g.Lp * 4); }
 std::size_t dy_bytes(const BfGeo& g) { return g.dy_direct ? 0 : a256(std::size_t(g.N) * g.K * g.Ldp * 4); }
+// RED scratch in the GEMM's own layout ([k][x row], or [x row][k] when the
+// roles are swapped), so a warp's 32 lanes reduce into 32 consecutive floats
+// -- one L2 transaction instead of 32 scattered ones into dW[k][c][r][s].
+int rows_pad(const BfGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM; }
+int cols_pad(const BfGeo& g) { return g.swap ? kBM : g.n_tiles * g.BN; }
+std::size_t acc_bytes(const BfGeo& g) { return a256(std::size_t(rows_pad(g)) * cols_pad(g) * 4); }
 
 struct BfParams {
   float* dw;
   float alpha;
   int K, CRS, RS, S, R, C, Bw, Ah, sh, sw, Qw, CCp, CC, Gb, Wq, M, BN;
   int m_tiles, tiles, splits, steps, steps_per_unit, Lc, T, stages, swap, Kb, ksub, prof;
+  float* acc;  // RED scratch: non-swap [k][row] (pitch rpad), swap [row][k] (pitch 128)
+  int rpad;
 };
 
 // GEMM row (qh, qw, cc) of the x operand -> dW offset (c, r, s), or -1
@@ -319,7 +327,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int k = ew * 32 + lane;
         const bool live = k < p.K && g1 > g0;
-        float* dwk = p.dw + std::int64_t(k) * p.CRS;
         for (int c0 = 0; c0 < p.BN; c0 += 32) {
           float v[32];
           tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -327,8 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (c0 + j >= p.BN) break;
-            const int off = offtab[c0 + j];
-            if (off >= 0) red_add(dwk + off, p.alpha * v[j]);
+            if (offtab[c0 + j] >= 0) red_add(p.acc + std::int64_t(nt * p.BN + c0 + j) * kBM + k, v[j]);
           }
         }
       } else {
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const int k = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || k >= p.K) break;
-            red_add(p.dw + std::int64_t(k) * p.CRS + off, p.alpha * v[j]);
+            red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
           }
         }
       }
@@ -425,16 +431,42 @@ __device__ __forceinline__ void dy_pitch_unit(const DyPitchArgs& a, std::int64_t
 
 // One launch for everything BackwardFilter does before its GEMM: the two
 // re-layouts (either may be skipped) and dW *= beta (beta != 1).
-__global__ void __launch_bounds__(256) bf_prep_kernel(const XPhaseArgs xa, const DyPitchArgs da, float* dw,
-                                                       std::int64_t wn, float beta) {
+__global__ void __launch_bounds__(256) bf_prep_kernel(const XPhaseArgs xa, const DyPitchArgs da, float4* acc,
+                                                       std::int64_t an) {
   pdl_wait();
   pdl_trigger();
-  const std::int64_t nx = xa.units, nd = da.units, total = nx + nd + wn;
+  const std::int64_t nx = xa.units, nd = da.units, total = nx + nd + an;
   for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
        u += std::int64_t(gridDim.x) * blockDim.x) {
     if (u < nx) x_phase_unit(xa, u);
     else if (u < nx + nd) dy_pitch_unit(da, u - nx);
-    else dw[u - nx - nd] = beta == 0.f ? 0.f : dw[u - nx - nd] * beta;
+    else acc[u - nx - nd] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// dW[k][c][r][s] = beta * dW + alpha * scratch[k][row(c, r, s)]: every dW
+// element owns exactly one GEMM row, so this is a plain gather-update.
+struct FinalizeArgs {
+  const float* acc;
+  float* dw;
+  float alpha, beta;
+  int K, C, R, S, sh, sw, Bw, Qw, CCp, rpad, swap;
+  std::int64_t n;  // K * C * R * S
+};
+__global__ void __launch_bounds__(256) bf_finalize_kernel(const FinalizeArgs f) {
+  pdl_wait();
+  pdl_trigger();
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < f.n;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    const int s = int(i % f.S);
+    std::int64_t t = i / f.S;
+    const int r = int(t % f.R);
+    t /= f.R;
+    const int c = int(t % f.C), k = int(t / f.C);
+    const int qh = r / f.sh, a = r - qh * f.sh, qw = s / f.sw, b = s - qw * f.sw;
+    const int row = (qh * f.Qw + qw) * f.CCp + (a * f.Bw + b) * f.C + c;
+    const float v = f.swap ? f.acc[std::int64_t(row) * kBM + k] : f.acc[std::int64_t(k) * f.rpad + row];
+    f.dw[i] = f.beta == 0.f ? f.alpha * v : f.alpha * v + f.beta * f.dw[i];
   }
 }
 
@@ -496,7 +528,7 @@ bool bf_supports(const ConvShape& s) {
 
 std::int64_t bf_workspace(const ConvShape& s) {
   const BfGeo g = make_geo(s);
-  return std::int64_t(x_bytes(g) + dy_bytes(g));
+  return std::int64_t(x_bytes(g) + dy_bytes(g) + acc_bytes(g));
 }
 
 cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
@@ -511,14 +543,12 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
                 FastDiv(std::uint32_t(g.Lp / 4)), fd_wq, FastDiv(std::uint32_t(g.C)), FastDiv(std::uint32_t(g.Bw))};
   DyPitchArgs da{dy, const_cast<float*>(dyp), g.OH, g.OW, g.dy_direct ? 0 : std::int64_t(g.N) * g.K * (g.Ldp / 4),
                  FastDiv(std::uint32_t(g.Ldp / 4)), fd_wq};
-  const std::int64_t wn = beta != 1.f ? s.w_elems() : 0;
-  const std::int64_t prep = xa.units + da.units + wn;
-  cudaError_t e;
-  if (prep > 0) {
-    e = launch_pdl(bf_prep_kernel, dim3(int(std::min<std::int64_t>((prep + 255) / 256, 16 * sms))), dim3(256), 0, st, xa,
-                   da, dw, wn, beta);
-    if (e != cudaSuccess) return e;
-  }
+  float* accbuf = reinterpret_cast<float*>(static_cast<char*>(ws) + x_bytes(g) + dy_bytes(g));
+  const std::int64_t an = std::int64_t(rows_pad(g)) * cols_pad(g) / 4;
+  const std::int64_t prep = xa.units + da.units + an;
+  cudaError_t e = launch_pdl(bf_prep_kernel, dim3(int(std::min<std::int64_t>((prep + 255) / 256, 16 * sms))), dim3(256),
+                             0, st, xa, da, reinterpret_cast<float4*>(accbuf), an);
+  if (e != cudaSuccess) return e;
 
   CUtensorMap xmap, dmap;
   const std::int64_t rep = std::int64_t(g.N) * g.CC * g.Lp;
@@ -541,6 +571,8 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   p.Lc = g.Lc;
   p.T = g.T;
   p.swap = g.swap;
+  p.acc = accbuf;
+  p.rpad = rows_pad(g);
   p.prof = tune("prof", 0);
   p.Kb = g.Kb;
   p.steps = g.N * g.Lc;
@@ -559,8 +591,13 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(bf_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, xmap,
-                    dmap, p);
+  e = launch_pdl(bf_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, xmap, dmap,
+                 p);
+  if (e != cudaSuccess) return e;
+  FinalizeArgs f{accbuf, dw, alpha, beta, g.K, g.C, g.R, g.S, g.sh, g.sw, g.Bw, g.Qw, g.CCp, rows_pad(g), g.swap,
+                 s.w_elems()};
+  return launch_pdl(bf_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256), 0, st,
+                    f);
 }
 
 }  // namespace ucudnn

@@ -11,17 +11,18 @@
 using namespace ucudnn::sm100;
 
 __global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensorMap map, int N, int iters, int per,
-                                                int tma_on, long long* out, int ntiles) {
+                                                int tma_on, long long* out, int ntiles, int nbuf) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
-  unsigned char* ops = smem;                  // MMA operands: A 16 KB + B N*128
-  unsigned char* ring = smem + 64 * 1024;     // TMA ring: 6 x 16 KB
+  unsigned char* ops = smem;                  // MMA operands: nbuf x (A 16 KB + B N*128)
+  const std::uint32_t bufb = 16384 + N * 128;
+  unsigned char* ring = smem + (tma_on ? 0 : 0) + nbuf * bufb;  // TMA ring: 6 x 16 KB (when on)
   __shared__ __align__(8) std::uint64_t bar, full[6], empty[6];
   __shared__ std::uint32_t slot;
   __shared__ volatile int done;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < (16384 + N * 128) / 4; i += blockDim.x) reinterpret_cast<float*>(ops)[i] = 0.f;
+  for (int i = threadIdx.x; i < int(nbuf * bufb / 4); i += blockDim.x) reinterpret_cast<float*>(ops)[i] = 0.f;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     for (int s = 0; s < 6; ++s) {
@@ -38,12 +39,18 @@ __global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensor
   tc_fence_after();
   const std::uint32_t tm = slot;
   if (warp == 1) {
-    const std::uint32_t a = smem_u32(ops), b = a + 16384, idesc = idesc_tf32(128, N);
+    const std::uint32_t a0 = smem_u32(ops), idesc = idesc_tf32(128, N);
+    const std::uint64_t da0 = umma_desc_sw128(a0);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       if (lane == 0) {
-        for (int q = 0; q < per; ++q)
-          mma_tf32(tm, umma_desc_sw128(a + (q & 3) * 32), umma_desc_sw128(b + (q & 3) * 32), idesc, 1);
+        // buffer = (it % nbuf): descriptors are precomputed base + (byte offset >> 4)
+        const std::uint64_t da = da0 + (((it % nbuf) * bufb) >> 4), db = da + (16384 >> 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= per) break;
+          mma_tf32(tm, da + 2 * (q & 3), db + 2 * (q & 3), idesc, 1);
+        }
         mma_commit(&bar);
       }
       __syncwarp();
@@ -93,16 +100,19 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int N : {64, 192, 256})
-    for (int tma : {0, 1})
-      for (int per : {4, 8}) {
-        probe<<<148, 256, 64 * 1024 + 6 * 16384 + 1024>>>(map, N, 200, per, tma, d, int(bytes / 128 / 128));
+    for (int nbuf : {1, 2, 4})
+      for (int per : {8}) {
+        const int tma = 0;
+        const int smem = nbuf * (16384 + N * 128) + 1024;
+        if (smem > 200 * 1024) continue;
+        probe<<<148, 256, smem>>>(map, N, 200, per, tma, d, int(bytes / 128 / 128), nbuf);
         cudaError_t e = cudaDeviceSynchronize();
         long long h[148];
         cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
         double avg = 0;
         for (int i = 0; i < 148; ++i) avg += h[i];
         avg /= 148;
-        std::printf("N=%3d tma=%d per=%d: %.0f cyc/MMA (%.0f MAC/cyc/SM) %s\n", N, tma, per, avg, 128.0 * N * 8 / avg,
+        std::printf("N=%3d nbuf=%d per=%d: %.0f cyc/MMA (%.0f MAC/cyc/SM) %s\n", N, nbuf, per, avg, 128.0 * N * 8 / avg,
                     cudaGetErrorString(e));
       }
   return 0;

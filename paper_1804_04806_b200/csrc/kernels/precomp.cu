@@ -288,6 +288,198 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------- 2-SM
+// The same implicit GEMM on CTA pairs (cluster of 2) with tcgen05.mma
+// cta_group::2: one MMA covers 256 output pixels (128 per CTA, each CTA's
+// own TMA im2col box) x BN channels, B split along N (each CTA loads BN/2
+// filter rows). Per CTA that halves the filter bytes per MMA and doubles the
+// work per MMA instruction, so the same shared-memory ring keeps twice as
+// much MMA work in flight -- the ring's round trip (MMA completion ->
+// producer -> TMA -> MMA issue) is what bounded the 1-SM kernel. The pair's
+// rank 0 issues every MMA; both CTAs' TMA transactions count on rank 0's
+// "full" barriers, its commits multicast to both CTAs, and both epilogues
+// release the accumulator on rank 0's "tempty" barrier (256 arrivals).
+__global__ void __launch_bounds__(kThreads, 1)
+    precomp2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                    const PrecompParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cluster_rank();
+  const int bh = p.BN / 2;  // filter rows per CTA
+  const std::uint32_t a_bytes = kBM * 128;
+  const std::uint32_t b_bytes = std::uint32_t(bh) * 128;
+  const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int kSub = p.ksub;
+  const std::uint32_t stage_bytes = kSub * sub_bytes;
+  const int kStages = p.stages;
+  const int jsteps = (p.ksteps + kSub - 1) / kSub;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&amap);
+    prefetch_tmap(&bmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers initialised before any remote arrive / TMA
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int total_tiles = p.m_tiles * p.n_tiles;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
+    if (lane == 0) {
+      int it = 0;
+      for (int t = cid; t < total_tiles; t += ncl) {
+        int mt, nt;
+        tile_coords(p, t, mt, nt);
+        std::uint32_t n, pix, oh, ow;
+        p.fd_P.divmod(std::uint32_t(mt * 2 * kBM + int(rank) * kBM), n, pix);
+        p.fd_OW.divmod(pix, oh, ow);
+        const int cw = int(ow) * p.sw - p.pw, ch = int(oh) * p.sh - p.ph;
+        const int brow0 = nt * p.ksteps * p.BN + int(rank) * bh;
+        for (int j = 0; j < jsteps; ++j, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
+          if (rank == 0) mbar_expect_tx(&full[s], 2u * nsub * (a_bytes + b_bytes));
+          const std::uint32_t bar = mapa(smem_u32(&full[s]), 0);
+          for (int sub = 0; sub < nsub; ++sub) {
+            const int k = k0 + sub;
+            unsigned char* sa = smem + s * stage_bytes + sub * sub_bytes;
+            const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
+            const int r = tap / p.S, q = tap - r * p.S;
+            tma_im2col_4d_2sm(sa, &amap, bar, cc * 32, cw, ch, int(n), (unsigned short)q, (unsigned short)r);
+            tma_2d_2sm(sa + a_bytes, &bmap, bar, 0, brow0 + k * p.BN);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---------------------------------------------- MMA issuer (pair leader)
+      const std::uint32_t idesc = idesc_tf32(2 * kBM, p.BN);
+      const std::uint32_t sbase = smem_u32(smem);
+      const std::uint64_t da0 = umma_desc_sw128(sbase), db0 = umma_desc_sw128(sbase + a_bytes);
+      int it = 0, tl = 0;
+      for (int t = cid; t < total_tiles; t += ncl, ++tl) {
+        const int acc = tl & 1;
+        mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+        for (int j = 0; j < jsteps; ++j, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
+          if (lane == 0) {
+            const std::uint32_t so = (std::uint32_t(s) * stage_bytes) >> 4;
+            for (int sub = 0; sub < nsub; ++sub) {
+              const std::uint32_t o = so + ((std::uint32_t(sub) * sub_bytes) >> 4);
+              const std::uint32_t first = (k0 + sub) != 0;
+              mma_tf32_2sm(dtm, da0 + o, db0 + o, idesc, first);
+              mma_tf32_2sm(dtm, da0 + o + 2, db0 + o + 2, idesc, 1u);
+              mma_tf32_2sm(dtm, da0 + o + 4, db0 + o + 4, idesc, 1u);
+              mma_tf32_2sm(dtm, da0 + o + 6, db0 + o + 6, idesc, 1u);
+            }
+            mma_commit_2sm(&empty[s], 3);
+            if (j == jsteps - 1) mma_commit_2sm(&tfull[acc], 3);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - 4;
+    const std::uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    int tl = 0;
+    for (int t = cid; t < total_tiles; t += ncl, ++tl) {
+      int mt, nt;
+      tile_coords(p, t, mt, nt);
+      const int acc = tl & 1;
+      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
+      const bool ok = row < p.M;
+      std::int64_t obase = 0;
+      int hb = 0, wb = 0;
+      if (ok) {
+        std::uint32_t n, pix;
+        p.fd_P.divmod(std::uint32_t(row), n, pix);
+        obase = std::int64_t(n) * p.Nout * p.P + pix;
+        if (p.phase) {
+          std::uint32_t i, j;
+          p.fd_OW.divmod(pix, i, j);
+          obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
+          hb = int(i) * p.ssh - p.sph;
+          wb = int(j) * p.ssw - p.spw;
+        }
+      }
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (!ok) continue;
+        if (p.phase) {
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const int col = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || col >= p.Nout) break;
+            std::uint32_t ab, c, a, b;
+            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
+            p.fd_ssw.divmod(ab, a, b);
+            const int h = hb + int(a), w = wb + int(b);
+            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+            const float val = p.alpha * v[j];
+            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = nt * p.BN + c0 + j;
+          if (c0 + j >= p.BN || col >= p.Nout) break;
+          float* dst = p.out + obase + std::int64_t(col) * p.P;
+          const float val = p.alpha * v[j];
+          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_remote(tempty_leader0 + std::uint32_t(acc) * 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_2sm<512>(tmem);
+  }
+}
+
 // NCHW -> N(HW)Cp, zero-filling channels C..Cp-1 (32 x 32 smem transpose).
 __global__ void to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int HW, int Cp) {
   pdl_wait();
@@ -349,7 +541,7 @@ struct PhaseFilter {
 };
 __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int O, int I, int taps,
                                    int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip,
-                                   PhaseFilter pf) {
+                                   PhaseFilter pf, int swz) {
   pdl_wait();
   pdl_trigger();
   const std::int64_t total = std::int64_t(n_tiles) * ksteps * 8 * BN;  // 16-byte units
@@ -399,7 +591,9 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
     // SWIZZLE_128B K-major block: row `row` holds its 8 16-byte chunks at
     // positions g ^ (row & 7) (the pattern TMA writes and UMMA reads)
     const std::int64_t blk = u / (8 * BN);
-    reinterpret_cast<float4*>(out)[blk * 8 * BN + row * 8 + (g ^ (row & 7))] = make_float4(v[0], v[1], v[2], v[3]);
+    // swz == 0: plain rows, for a TMA load that applies the swizzle itself
+    reinterpret_cast<float4*>(out)[blk * 8 * BN + row * 8 + (swz ? (g ^ (row & 7)) : g)] =
+        make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -826,7 +1020,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
-                   ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+                   ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, 1);
     if (e != cudaSuccess) return e;
   }
 
@@ -903,6 +1097,12 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   int ksteps = 0, BN = 0;
   geo_ws(g, &ksteps, &BN);
   const int n_tiles = (g.Nout + BN - 1) / BN;
+  // 2-SM MMA (precomp2_kernel) for >= 128-wide filter tiles: measured at 64
+  // images, conv2 F 95 -> 81 us, conv3 BD 79 -> 65, conv4 F 85 -> 69, conv5
+  // 63 -> 52 (conv2 F at 256 images: 489 TFLOP/s); narrower tiles (conv2 BD,
+  // conv1) stay on the 1-SM kernel, which won there. A function of the shape
+  // only, so all micro-batches of a call agree on the filter layout.
+  const bool two_sm = Cp != 4 && BN % 16 == 0 && BN >= tune("two_sm_min_bn", 128) && tune("two_sm", 1);
   // packed filter first: its size does not depend on the micro-batch, so
   // later micro-batches of the same call reuse it (kFilterReady)
   float* btiles = static_cast<float*>(ws);
@@ -924,7 +1124,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
-                   ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf);
+                   ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, two_sm ? 0 : 1);
     if (e != cudaSuccess) return e;
   }
 
@@ -982,6 +1182,44 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.spw = g.rpw;
     p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
     p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
+  }
+  if (two_sm) {
+    CUtensorMap bmap;
+    const cuuint64_t bdims[2] = {32, cuuint64_t(n_tiles) * ksteps * BN};
+    const cuuint64_t bstr[1] = {128};
+    const cuuint32_t bbox[2] = {32, cuuint32_t(BN / 2)};
+    const cuuint32_t bes[2] = {1, 1};
+    if (encode_tiled()(&bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, btiles, bdims, bstr, bbox, bes,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    p.m_tiles = (p.M + 2 * kBM - 1) / (2 * kBM);
+    p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
+    p.ksub = std::max(1, std::min(2, tune("pc2_ksub", 2)));
+    const int stage2 = p.ksub * (kBM * 128 + ((BN / 2 * 128 + 1023) & ~1023));
+    p.stages = ring_stages(std::min(tune("pc2_stages", 8), (200 * 1024) / stage2));
+    const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
+    static bool attr2 = false;
+    if (!attr2) {
+      e = cudaFuncSetAttribute(precomp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    const int clusters = std::min(sm_count() / 2, p.m_tiles * p.n_tiles);
+    count_launch();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = std::size_t(smem2);
+    cfg.stream = st;
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = 2;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, precomp2_kernel, amap, bmap, p);
   }
   // two 32-deep chunks per stage (8 MMAs per tcgen05.commit): measured
   // 10-25 % faster than one on AlexNet conv2 / conv4 (same box, A/B)

@@ -141,7 +141,7 @@ std::size_t dy_bytes(const BfGeo& g) { return g.dy_direct ? 0 : a256(std::size_t
 // RED scratch in the GEMM's own layout ([k][x row], or [x row][k] when the
 // roles are swapped), so a warp's 32 lanes reduce into 32 consecutive floats
 // -- one L2 transaction instead of 32 scattered ones into dW[k][c][r][s].
-int rows_pad(const BfGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM; }
+int rows_pad(const BfGeo& g) { return g.swap ? g.n_tiles * g.BN : (g.m_tiles + 1) / 2 * 2 * kBM; }
 int cols_pad(const BfGeo& g) { return g.swap ? kBM : g.n_tiles * g.BN; }
 std::size_t acc_bytes(const BfGeo& g) { return a256(std::size_t(rows_pad(g)) * cols_pad(g) * 4); }
 
@@ -365,6 +365,156 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// 2-SM BackwardFilter (K >= 128, roles not swapped): CTA pairs with
+// tcgen05.mma cta_group::2 -- 256 x rows (128 per CTA, each CTA's own x
+// boxes) x BN output channels, the dy box split along N (BN/2 rows per CTA).
+// Same split-K units over (image, 32-pixel step), same RED-into-scratch
+// epilogue per CTA; rank 0 issues the MMAs, both CTAs' TMA bytes count on
+// its barriers, commits multicast to both, both epilogues release rank 0's
+// accumulator barrier.
+__global__ void __launch_bounds__(kThreads, 1)
+    bf2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap, const BfParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cluster_rank();
+  const int bh = p.BN / 2;
+  const std::uint32_t a_bytes = kBM * 128;
+  const std::uint32_t b_bytes = std::uint32_t(bh) * 128;
+  const std::uint32_t stage_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&dmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int units = p.tiles * p.splits;  // tiles = pair tiles x n tiles
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
+    if (lane == 0) {
+      const int boxes = kBM / p.Gb;
+      int it = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int tile = u % p.tiles, split = u / p.tiles;
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;  // m_tiles counts 256-row pair tiles
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        const int xrow0 = mt * 2 * kBM + int(rank) * kBM;
+        for (int g = g0; g < g1; ++g, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
+          const int st = it % kStages;
+          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2u * (a_bytes + b_bytes));
+          const std::uint32_t bar = mapa(smem_u32(&full[st]), 0);
+          unsigned char* sa = smem + st * stage_bytes;
+          const int n = g / p.Lc, j0 = (g - n * p.Lc) * 32;
+#pragma unroll 1
+          for (int bx = 0; bx < boxes; ++bx) {
+            const int row0 = xrow0 + bx * p.Gb;
+            const int q = row0 / p.CCp, cc0 = row0 - q * p.CCp;
+            const int qh = q / p.Qw, qw = q - qh * p.Qw;
+            const int o = j0 + qh * p.Wq + qw;
+            tma_4d_2sm(sa + bx * (p.Gb * 128), &xmap, bar, o & ~3, row0 < p.M ? cc0 : p.CC, n, (o & 3) % p.T);
+          }
+          tma_4d_2sm(sa + a_bytes, &dmap, bar, j0, nt * p.BN + int(rank) * bh, n, 0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0) {
+      const std::uint32_t idesc = idesc_tf32(2 * kBM, p.BN);
+      const std::uint32_t sbase = smem_u32(smem);
+      const std::uint64_t da0 = umma_desc_sw128(sbase), db0 = umma_desc_sw128(sbase + a_bytes);
+      int it = 0, tl = 0;
+      for (int u = cid; u < units; u += ncl, ++tl) {
+        const int split = u / p.tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        const int acc = tl & 1;
+        mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+        for (int g = g0; g < g1; ++g, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const std::uint32_t o = (std::uint32_t(st) * stage_bytes) >> 4;
+            mma_tf32_2sm(dtm, da0 + o, db0 + o, idesc, g != g0);
+            mma_tf32_2sm(dtm, da0 + o + 2, db0 + o + 2, idesc, 1u);
+            mma_tf32_2sm(dtm, da0 + o + 4, db0 + o + 4, idesc, 1u);
+            mma_tf32_2sm(dtm, da0 + o + 6, db0 + o + 6, idesc, 1u);
+            mma_commit_2sm(&empty[st], 3);
+            if (g == g1 - 1) mma_commit_2sm(&tfull[acc], 3);
+          }
+          __syncwarp();
+        }
+        if (g1 <= g0 && lane == 0) mma_commit_2sm(&tfull[acc], 3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const std::uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    int tl = 0;
+    for (int u = cid; u < units; u += ncl, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const int row = mt * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
+      const int off = g1 > g0 ? x_row_off(p, row) : -1;
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (off < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = nt * p.BN + c0 + j;
+          if (c0 + j >= p.BN || k >= p.K) break;
+          red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_remote(tempty_leader0 + std::uint32_t(acc) * 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_2sm<512>(tmem);
+  }
+}
+
 // x (NCHW) -> x_ph[t][n][(a,b,c)][Lp]: zero padding + stride-phase split,
 // replica t shifted left by t elements. One thread = 4 consecutive plane
 // positions of every replica (float4 stores; HBM-bound).
@@ -554,8 +704,12 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   const std::int64_t rep = std::int64_t(g.N) * g.CC * g.Lp;
   if (!encode_4d(&xmap, xph, g.Lq, g.CC, g.N, g.T, g.Lp, std::int64_t(g.CC) * g.Lp, rep, 32, g.Gb))
     return cudaErrorInvalidValue;
+  // 2-SM kernel (the MMA pairs 256 x rows; each CTA loads half of the dy
+  // rows) where it measured faster: 256-wide or multi-tile K (AlexNet
+  // conv3-5, 32-64 images: 3-10 %); K = 192 in one tile (conv2) lost 2-3 %.
+  const bool two = !g.swap && g.BN % 16 == 0 && (g.BN >= 256 || (g.BN >= 128 && g.n_tiles >= 2)) && tune("bf2", 1);
   if (!encode_4d(&dmap, dyp, g.Ld, g.K, g.N, 1, g.Ldp, std::int64_t(g.K) * g.Ldp, std::int64_t(g.N) * g.K * g.Ldp, 32,
-                 g.swap ? g.Kb : g.BN))
+                 g.swap ? g.Kb : two ? g.BN / 2 : g.BN))
     return cudaErrorInvalidValue;
 
   BfParams p{};
@@ -577,6 +731,42 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   p.Kb = g.Kb;
   p.steps = g.N * g.Lc;
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
+  if (two) {
+    p.m_tiles = (g.m_tiles + 1) / 2;
+    p.tiles = p.m_tiles * g.n_tiles;
+    int sp = std::max(1, std::min(p.steps / 8, (sms / 2) / p.tiles));
+    p.ksub = 1;
+    p.steps_per_unit = (p.steps + sp - 1) / sp;
+    p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
+    const int stage2 = kBM * 128 + ((g.BN / 2 * 128 + 1023) & ~1023);
+    p.stages = ring_stages(std::min(tune("bf2_stages", 8), (200 * 1024) / stage2));
+    const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
+    static bool attr2 = false;
+    if (!attr2) {
+      e = cudaFuncSetAttribute(bf2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    count_launch();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(sms / 2, p.tiles * p.splits));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = std::size_t(smem2);
+    cfg.stream = st;
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = 2;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, bf2_kernel, xmap, dmap, p);
+    if (e != cudaSuccess) return e;
+    FinalizeArgs f2{accbuf, dw, alpha, beta, g.K, g.C, g.R, g.S, g.sh, g.sw, g.Bw, g.Qw, g.CCp, rows_pad(g), g.swap,
+                    s.w_elems()};
+    return launch_pdl(bf_finalize_kernel, dim3(int(std::min<std::int64_t>((f2.n + 255) / 256, 8 * sms))), dim3(256), 0,
+                      st, f2);
+  }
   int splits = std::max(1, std::min(p.steps / 8, tune("bf_waves", 1) * sms / p.tiles));
   p.ksub = std::max(1, std::min(kMaxSub, tune("bf_ksub", 1)));
   const int kSub = p.ksub;

@@ -201,6 +201,14 @@ __device__ __forceinline__ void tma_im2col_4d_2sm(void* dst, const void* tmap, s
       "l"(tmap), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
       : "memory");
 }
+__device__ __forceinline__ void tma_4d_2sm(void* dst, const void* tmap, std::uint32_t bar_cluster, int x, int y, int z,
+                                           int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
 __device__ __forceinline__ void tma_2d_2sm(void* dst, const void* tmap, std::uint32_t bar_cluster, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"

@@ -242,6 +242,11 @@ def main():
     for (i, op) in stack.kernels():
         base_stack_algos[(i, op)] = base.get_algorithm(op, stack.layers[i].shape, limit)
     base_plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": base.plan(a) for (i, op), a in base_stack_algos.items()}
+    # the caller's WR workspace must cover the undivided plans too (in WD mode
+    # the planned handle itself needs none: it owns its arena)
+    need = max(base.workspace_size(a, op, stack.layers[i].shape) for (i, op), a in base_stack_algos.items())
+    if need // 4 + 64 > stack.ws.numel():
+        stack.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
 
     comm = torch.distributed.group.WORLD if dist_on else None
     comm_stream = torch.cuda.Stream(dev) if dist_on else None

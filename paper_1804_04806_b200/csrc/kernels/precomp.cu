@@ -64,9 +64,27 @@ struct PrecompParams {
   // phase scatter epilogue (strided BackwardData): column (a, b, c) of
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
   int stages, ksub, prof, cps;
   FastDiv fd_Cr, fd_ssw;
 };
+
+// Stride-phase BackwardData when the filter is narrower than the stride (1x1
+// stride-2 shortcuts): only phases a < sAh, b < sBw have taps and are GEMM
+// columns; dx at the other phases gets beta * dx (0 for beta = 0), written
+// by whoever owns column (0, 0, c) of the same pixel.
+template <typename P>
+__device__ __forceinline__ void tapless_phases(const P& p, float* base, int c, int hb, int wb) {
+  if (p.sAh >= p.ssh && p.sBw >= p.ssw) return;
+  for (int a = 0; a < p.ssh; ++a)
+    for (int b = 0; b < p.ssw; ++b) {
+      if (a < p.sAh && b < p.sBw) continue;
+      const int h = hb + a, w = wb + b;
+      if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+      float* dst = base + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+      *dst = p.beta == 0.f ? 0.f : p.beta * *dst;
+    }
+}
 
 __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& mt, int& nt) {
   std::uint32_t q, r;
@@ -258,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             std::uint32_t ab, c, a, b;
             p.fd_Cr.divmod(std::uint32_t(col), ab, c);
             p.fd_ssw.divmod(ab, a, b);
+            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
             const int h = hb + int(a), w = wb + int(b);
             if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
             float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
@@ -449,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             std::uint32_t ab, c, a, b;
             p.fd_Cr.divmod(std::uint32_t(col), ab, c);
             p.fd_ssw.divmod(ab, a, b);
+            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
             const int h = hb + int(a), w = wb + int(b);
             if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
             float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
@@ -538,6 +558,7 @@ __global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__
 // grid, ch = k -> W[k][c][a + (Th-1-t)*sh][b + (Tw-1-u)*sw] (0 off the filter).
 struct PhaseFilter {
   int C, R, S, sh, sw, Tw;
+  int bw = 0;  // stride-phase BD: phases kept along w (decode divisor of the column index)
 };
 __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int O, int I, int taps,
                                    int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip,
@@ -577,7 +598,7 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
           const int r = t * pf.sh + a, q = u * pf.sw + b;
           if (a < pf.sh && r < pf.R && q < pf.S) x = w[((std::int64_t(o) * pf.C + c) * pf.R + r) * pf.S + q];
         } else if (flip == 2) {
-          const int ab = o / pf.C, c = o - ab * pf.C, a = ab / pf.sw, b = ab - a * pf.sw;
+          const int ab = o / pf.C, c = o - ab * pf.C, a = ab / pf.bw, b = ab - a * pf.bw;
           const int t = tap / pf.Tw, u = tap - t * pf.Tw, Th = taps / pf.Tw;
           const int r = a + (Th - 1 - t) * pf.sh, q = b + (pf.Tw - 1 - u) * pf.sw;
           if (r < pf.R && q < pf.S) x = w[((std::int64_t(ch) * pf.C + c) * pf.R + r) * pf.S + q];
@@ -626,6 +647,7 @@ struct StripParams {
   int OH, OW, Nout, P;
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  int sAh, sBw;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
 };
@@ -801,6 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 std::uint32_t ab, c, a, b;
                 p.fd_Cr.divmod(std::uint32_t(col), ab, c);
                 p.fd_ssw.divmod(ab, a, b);
+                if (ab == 0) tapless_phases(p, base, int(c), hb, wb);
                 const int h = hb + int(a), w = wb + int(b);
                 if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
                 float* dst = base + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
@@ -843,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             std::uint32_t ab, c, a, b;
             p.fd_Cr.divmod(std::uint32_t(col), ab, c);
             p.fd_ssw.divmod(ab, a, b);
+            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
             const int h = hb + int(a), w = wb + int(b);
             if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
             float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
@@ -1071,7 +1095,9 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.sph = g.rph;
     p.spw = g.rpw;
     p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
-    p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
+    p.fd_ssw = FastDiv(std::uint32_t(g.pf.bw));
+    p.sAh = std::min(g.pf.sh, g.pf.R);
+    p.sBw = g.pf.bw;
   }
   const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
@@ -1181,7 +1207,9 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.sph = g.rph;
     p.spw = g.rpw;
     p.fd_Cr = FastDiv(std::uint32_t(g.pf.C));
-    p.fd_ssw = FastDiv(std::uint32_t(g.pf.sw));
+    p.fd_ssw = FastDiv(std::uint32_t(g.pf.bw));
+    p.sAh = std::min(g.pf.sh, g.pf.R);
+    p.sBw = g.pf.bw;
   }
   if (two_sm) {
     CUtensorMap bmap;
@@ -1284,11 +1312,13 @@ Geo bwd_data_phase_geo(const ConvShape& s) {
   // cover every dx row: i up to (H - 1 + ph) / sh
   const int Hq = std::max(OH + Th - 1, (s.H - 1 + s.ph) / s.sh + 1);
   const int Wq = std::max(OW + Tw - 1, (s.W - 1 + s.pw) / s.sw + 1);
-  Geo g{s.N, s.K, OH, OW, s.sh * s.sw * s.C, Hq, Wq, Th, Tw, Th - 1, Tw - 1, 1, 1};
+  // only the phases that own filter taps become GEMM columns
+  const int Ah = std::min(s.sh, s.R), Bw = std::min(s.sw, s.S);
+  Geo g{s.N, s.K, OH, OW, Ah * Bw * s.C, Hq, Wq, Th, Tw, Th - 1, Tw - 1, 1, 1};
   g.ph_hi = Hq - OH;
   g.pw_hi = Wq - OW;
   g.phase = 1;
-  g.pf = PhaseFilter{s.C, s.R, s.S, s.sh, s.sw, Tw};
+  g.pf = PhaseFilter{s.C, s.R, s.S, s.sh, s.sw, Tw, Bw};
   g.Hr = s.H;
   g.Wr = s.W;
   g.rph = s.ph;

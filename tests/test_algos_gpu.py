@@ -81,10 +81,17 @@ def test_gaussian_tf32_tolerance(cuda, algo, op, s):
     assert err <= TOL.get(algo, 3e-3), err
 
 
+AB_SHAPES = [
+    ConvShape(3, 6, 10, 10, 20, 3, 3, 1, 1, 1, 1),
+    ConvShape(2, 16, 14, 14, 32, 1, 1, 0, 0, 2, 2),   # BD: dx phases without taps get beta * dx
+    ConvShape(2, 3, 31, 31, 16, 11, 11, 2, 2, 4, 4),  # stride-phase BD / space-to-depth F
+]
+
+
+@pytest.mark.parametrize("s", AB_SHAPES, ids=_sid)
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["F", "BD", "BF"])
 @pytest.mark.parametrize("algo", ALGOS)
-def test_alpha_beta(cuda, algo, op):
-    s = ConvShape(3, 6, 10, 10, 20, 3, 3, 1, 1, 1, 1)
+def test_alpha_beta(cuda, algo, op, s):
     rng = np.random.default_rng(3)
     a, b = inputs_for(op, s, rng, integer=True)
     init = np.random.default_rng(4).integers(-3, 4, size=out_shape(op, s)).astype(np.float64)

@@ -17,7 +17,8 @@ FORWARD, BACKWARD_DATA, BACKWARD_FILTER = 0, 1, 2
 OP_NAMES = {FORWARD: "Forward", BACKWARD_DATA: "BackwardData", BACKWARD_FILTER: "BackwardFilter"}
 POLICIES = {"all": 0, "powerOfTwo": 1, "undivided": 2}
 MODES = {"wr": 0, "wd": 1}
-ALGOS = {0: "IMPLICIT_GEMM", 1: "WINOGRAD", 2: "FFT", 3: "GEMM", 4: "WINOGRAD_4x4", 5: "IMPLICIT_PRECOMP_GEMM"}
+ALGOS = {0: "IMPLICIT_GEMM", 1: "WINOGRAD", 2: "FFT", 3: "GEMM", 4: "WINOGRAD_4x4", 5: "IMPLICIT_PRECOMP_GEMM",
+         6: "IMPLICIT_GATHER_GEMM"}
 VIRTUAL_ALGO_BASE = 1000
 
 

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "../kernels/bflsu.h"
 #include "../kernels/fft.h"
 #include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
@@ -60,12 +61,23 @@ cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b
   return winograd_run(4, op, s, a, b, out, ws, alpha, beta, st, flags);
 }
 
+// BackwardFilter with operands gathered by cp.async straight from NCHW x / dy
+// (bflsu.cu): a small fixed workspace instead of PRECOMP's per-image copies.
+bool gather_supports(int op, const ConvShape& s) { return op == 2 && bfl_supports(s); }
+std::int64_t gather_workspace(int op, const ConvShape& s) { return op == 2 ? bfl_workspace(s) : 0; }
+cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
+                       float beta, cudaStream_t st, int) {
+  if (op != 2) return cudaErrorInvalidValue;
+  return bfl_run(s, a, b, out, ws, alpha, beta, st);
+}
+
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
 const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
 const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
 const AlgoImpl kFft{2, "FFT", fft_supports, fft_workspace, fft_run};
 const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
+const AlgoImpl kGather{6, "IMPLICIT_GATHER_GEMM", gather_supports, gather_workspace, gather_run};
 
 }  // namespace
 
@@ -77,10 +89,11 @@ const AlgoImpl* find_algo(int id) {
     case 4: return &kWinograd4;
     case 3: return &kGemm;
     case 5: return &kPrecomp;
+    case 6: return &kGather;
     default: return nullptr;
   }
 }
 
-int algo_count() { return 6; }
+int algo_count() { return 7; }
 
 }  // namespace ucudnn

@@ -44,6 +44,7 @@
 #include <cstdint>
 
 #include "bfilter.h"
+#include "bflsu.h"
 #include "conv_common.h"
 #include "launch.h"
 #include "sm100.cuh"
@@ -668,7 +669,11 @@ void bf_profile(double out[4]) {
   for (int i = 0; i < 4; ++i) out[i] = n ? s[i] / n : 0;
 }
 
+// UCUDNN_TUNE=bfl=1 routes PRECOMP BackwardFilter to the gather kernel (bflsu.cu; algo 6)
+bool use_lsu(const ConvShape& s) { return tune("bfl", 0) && bfl_supports(s); }
+
 bool bf_supports(const ConvShape& s) {
+  if (use_lsu(s)) return true;
   const BfGeo g = make_geo(s);
   // TMA coordinates are int32 and box dims <= 256; flat offsets must fit
   return std::int64_t(g.Lq) + 64 < (std::int64_t(1) << 30) && g.CC < (1 << 20) && s.K < (1 << 20) &&
@@ -677,12 +682,14 @@ bool bf_supports(const ConvShape& s) {
 }
 
 std::int64_t bf_workspace(const ConvShape& s) {
+  if (use_lsu(s)) return bfl_workspace(s);
   const BfGeo g = make_geo(s);
   return std::int64_t(x_bytes(g) + dy_bytes(g) + acc_bytes(g));
 }
 
 cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
                    cudaStream_t st) {
+  if (use_lsu(s)) return bfl_run(s, x, dy, dw, ws, alpha, beta, st);
   const BfGeo g = make_geo(s);
   const float* xph = g.x_direct ? x : static_cast<const float*>(ws);
   const float* dyp = g.dy_direct ? dy : reinterpret_cast<const float*>(static_cast<char*>(ws) + x_bytes(g));

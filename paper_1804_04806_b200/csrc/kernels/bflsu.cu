@@ -1,0 +1,471 @@
+// UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM, BackwardFilter, load-store-unit-fed
+// variant: the tcgen05 GEMM reads x and dy straight from their NCHW tensors.
+//
+//   dW[k][c][r][s] += alpha * sum_{n,oh,ow} dy[n][k][oh][ow] * x[n][c][oh*sh-ph+r][ow*sw-pw+s]
+//   (reference_conv.hpp:141-171; beta applied once, :173-180)
+//
+// Why not TMA here (bfilter.cu): the reduction axis -- output pixels -- has
+// to be K-major in shared memory, and a tap (r, s) shifts it by a non-16-byte
+// multiple, which TMA cannot start at. bfilter.cu pays for that with
+// re-laid-out, 4x-replicated copies of x in the workspace (AlexNet conv1: 687
+// MB for 256 images), so under a 64 MiB limit the planner has to cut the
+// batch into 16-image micro-batches and pay each call's ramp and
+// re-layout again. Here producer warps gather the operands themselves with
+// 4-byte cp.async (any alignment, zero fill through the ignore-src
+// predicate), lane = pixel, so:
+//   * no re-layout pass and no workspace beyond the small GEMM-layout RED
+//     scratch -- every batch size fits, one call covers the whole batch;
+//   * strides and padding are handled in the gather (per-lane bounds), GEMM
+//     rows are exactly the C*R*S filter taps (no phase padding);
+//   * 32-pixel reduction chunks run across image boundaries (the flat
+//     pixel index n*OH*OW + p), so 13x13 layers waste no MMA K-steps.
+// The store pattern is the SWIZZLE_128B K-major UMMA layout: row q at
+// q*128 B, 16-byte chunk (lane/4) ^ (q%8).
+//
+// GEMM rows of x are ordered (r, s, c) so that 8-row groups share one tap:
+// the bounds test and base offset are computed once per tap run, and each
+// row is one cp.async plus a pointer step. Roles as in bfilter.cu: K <= 128
+// output channels -> MMA rows = k (one 128-row tile of dy), columns = x rows.
+//
+// Persistent, one CTA per SM, 416 threads: warps 0-3 epilogue (TMEM ->
+// fp32 RED into the scratch), warp 4 TMEM owner + MMA issuer, warps 5-12
+// producers. A producer never waits for its own gathers: each thread's
+// cp.async.mbarrier.arrive fires when its copies land, and the MMA thread
+// issues the generic->async proxy fence after observing the full barrier.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "bflsu.h"
+#include "conv_common.h"
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace ucudnn {
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kMaxBN = 256;
+constexpr int kMaxStages = 8;
+constexpr int kProd = 12;  // producer warps
+constexpr int kThreads = (5 + kProd) * 32;
+
+struct LGeo {
+  int N, C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
+  int M;  // C*R*S GEMM rows of x
+  int swap, BN, m_tiles, n_tiles;
+  long long npx;  // N*OH*OW
+  int steps;      // 32-pixel chunks
+};
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+LGeo make_lgeo(const ConvShape& s) {
+  LGeo g{};
+  g.N = s.N; g.C = s.C; g.H = s.H; g.W = s.W; g.K = s.K; g.R = s.R; g.S = s.S;
+  g.ph = s.ph; g.pw = s.pw; g.sh = s.sh; g.sw = s.sw; g.OH = s.OH(); g.OW = s.OW();
+  g.M = s.C * s.R * s.S;
+  g.npx = std::int64_t(s.N) * g.OH * g.OW;
+  g.steps = int((g.npx + 31) / 32);
+  g.swap = s.K <= 128 && g.M > 128;
+  if (g.swap) {
+    int nt = (g.M + kMaxBN - 1) / kMaxBN;
+    g.BN = round_up((g.M + nt - 1) / nt, 16);
+    g.n_tiles = (g.M + g.BN - 1) / g.BN;
+    g.m_tiles = 1;
+  } else {
+    const int nt = (s.K + kMaxBN - 1) / kMaxBN;
+    g.BN = round_up((s.K + nt - 1) / nt, 16);
+    g.n_tiles = (s.K + g.BN - 1) / g.BN;
+    g.m_tiles = (g.M + kBM - 1) / kBM;
+  }
+  return g;
+}
+
+// RED scratch in the GEMM's own layout: non-swap [k][x row] (pitch rows_pad),
+// swap [x row][k] (pitch 128); 32 lanes reduce into 32 consecutive floats.
+int rows_pad(const LGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM; }
+int cols_pad(const LGeo& g) { return g.swap ? kBM : g.n_tiles * g.BN; }
+std::size_t scratch_bytes(const LGeo& g) { return (std::size_t(rows_pad(g)) * cols_pad(g) * 4 + 255) / 256 * 256; }
+
+struct LParams {
+  const float* x;
+  const float* dy;
+  float* acc;
+  int C, H, W, K, R, S, sh, sw, ph, pw, OW, OHW, HW, M;
+  long long npx, CHW, KOHW;
+  int swap, BN, m_tiles, tiles, splits, steps, steps_per_unit, stages, rpad;
+  int dbg;  // diagnostic (UCUDNN_TUNE=bfl_dbg): 1 skip the gathers, 2 skip the MMAs
+  FastDiv fd_ohw, fd_ow, fd_C, fd_S;
+};
+
+// 4-byte gather; src_size 0 writes a zero (src is then never dereferenced)
+__device__ __forceinline__ void cp_async4a(std::uint32_t dst, std::uint64_t src, std::uint32_t src_size) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_size) : "memory");
+}
+// mbarrier arrive (without a pending-count increment) triggered when all of
+// this thread's earlier cp.async have completed
+__device__ __forceinline__ void cp_async_arrive(std::uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Waits that last a whole unit (the epilogue's) back off so their spinning
+// does not steal issue slots from the gather warps.
+__device__ __forceinline__ void mbar_wait_backoff(std::uint64_t* bar, std::uint32_t parity) {
+  std::uint32_t ok = 0, ns = 128;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (ns < 4096) ns <<= 1;
+  }
+}
+// bits t in [lo, hi) of a width-n tap mask (n <= 32)
+__device__ __forceinline__ std::uint32_t range_mask(int lo, int hi, int n) {
+  lo = max(lo, 0);
+  hi = min(hi, n);
+  if (hi <= lo) return 0u;
+  const std::uint32_t h = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return h & ~((1u << lo) - 1u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t a_bytes = kBM * 128;
+  const std::uint32_t stage_bytes = a_bytes + ((std::uint32_t(p.BN) * 128 + 1023) & ~1023u);
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  __shared__ int2 xtab[kMaxBN];  // few-channel path: per x row of the tile
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kProd * 32);  // every producer thread, cp.async arrive
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 4) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int units = p.tiles * p.splits;
+
+  if (warp >= 5) {
+    // ------------------------------------------------ gather producers
+    const int pw = warp - 5;
+    const std::uint32_t sbase = smem_u32(smem);
+    // this lane's byte offset inside an 8-row swizzle atom, per row q % 8
+    std::uint32_t swz[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
+    // x rows go to A (non-swap) or B (swap); dy rows to the other
+    const std::uint32_t x_off = p.swap ? a_bytes : 0, d_off = p.swap ? 0 : a_bytes;
+    const bool c8 = p.C % 8 == 0;  // 8-row groups never straddle a tap
+    // byte offsets of rows j = 0..7 of a group (independent adds, no
+    // dependent address chain through the 8 cp.async of a group)
+    std::uint32_t xj[8], dj[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      xj[j] = std::uint32_t(j * p.HW * 4);
+      dj[j] = std::uint32_t(j * p.OHW * 4);
+    }
+    int st = 0;
+    std::uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int xm0 = p.swap ? nt * p.BN : mt * kBM;  // first x row of the tile
+      const int xrows = min(p.swap ? p.BN : kBM, p.M - xm0);
+      const int dk0 = p.swap ? 0 : nt * p.BN;
+      const int drows = min(p.swap ? kBM : p.BN, p.K - dk0);
+      if (!c8) {
+        // this warp's rows of the tile: (c*HW + r*W + s, r << 8 | s)
+        for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8)
+          if (lane < 8 && q0 + lane < xrows) {
+            std::uint32_t rs, c, r, s;
+            p.fd_C.divmod(std::uint32_t(xm0 + q0 + lane), rs, c);
+            p.fd_S.divmod(rs, r, s);
+            xtab[q0 + lane] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 8 | s));
+          }
+        __syncwarp();
+      }
+      for (int g = g0; g < g1; ++g) {
+        mbar_wait(&empty[st], ph ^ 1);
+        if (p.dbg == 1) {
+          cp_async_arrive(&full[st]);
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+          continue;
+        }
+        // this lane's pixel
+        const long long pg = (long long)g * 32 + lane;
+        const bool valid = pg < p.npx;
+        std::uint32_t n, pix, oh, ow;
+        p.fd_ohw.divmod(std::uint32_t(valid ? pg : 0), n, pix);
+        p.fd_ow.divmod(pix, oh, ow);
+        const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
+        const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
+        const std::uint32_t sst = sbase + st * stage_bytes;
+        // x rows: 8-row groups pw, pw + 8, ...
+        if (c8) {
+          // a group is 8 channels of one tap: one bounds test, then
+          // consecutive channel planes
+          for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
+            std::uint32_t rs, c, r, s;
+            p.fd_C.divmod(std::uint32_t(xm0 + q0), rs, c);
+            p.fd_S.divmod(rs, r, s);
+            const std::uint32_t dst = sst + x_off + q0 * 128;
+            const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
+            const std::uint32_t sz = ok ? 4u : 0u;
+            const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
+            const int qn = min(8, xrows - q0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < qn) cp_async4a(dst + swz[j], a + xj[j], sz);
+          }
+        } else {
+          // few channels (taps straddle groups): per-row (offset, tap) from
+          // the smem table, bounds from this lane's valid-tap bitmasks
+          const std::uint32_t vr = valid ? range_mask(-ihb, p.H - ihb, p.R) : 0u;
+          const std::uint32_t vs = range_mask(-iwb, p.W - iwb, p.S);
+          const std::uint64_t xa = reinterpret_cast<std::uint64_t>(xl);
+          for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
+            const std::uint32_t dst = sst + x_off + q0 * 128;
+            const int qn = min(8, xrows - q0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (j < qn) {
+                const int2 e = xtab[q0 + j];
+                const std::uint32_t ok = (vr >> (e.y >> 8)) & (vs >> (e.y & 255)) & 1u;
+                cp_async4a(dst + swz[j], xa + std::int64_t(e.x) * 4, ok * 4u);
+              }
+            }
+          }
+        }
+        // dy rows
+        {
+          const float* dl = p.dy + (long long)n * p.KOHW + pix;
+          const std::uint32_t sz = valid ? 4u : 0u;
+          for (int q0 = pw * 8; q0 < drows; q0 += kProd * 8) {
+            const float* src = dl + (long long)(dk0 + q0) * p.OHW;
+            const std::uint32_t dst = sst + d_off + q0 * 128;
+            const std::uint64_t a = reinterpret_cast<std::uint64_t>(src);
+            const int qn = min(8, drows - q0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < qn) cp_async4a(dst + swz[j], a + dj[j], sz);
+          }
+        }
+        // arrives once every cp.async this thread issued so far has landed
+        cp_async_arrive(&full[st]);
+        if (++st == kStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------ MMA issuer
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint32_t sbase = smem_u32(smem);
+    int it = 0, tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int split = u / p.tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      for (int g = g0; g < g1; ++g, ++it) {
+        const int st = it % kStages;
+        mbar_wait(&full[st], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          // the operands were written through the generic proxy (cp.async):
+          // order them before the tensor core's async-proxy reads
+          fence_async_smem();
+          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+          if (p.dbg != 2)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mma_tf32(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
+                       (g != g0 || q != 0) ? 1u : 0u);
+          mma_commit(&empty[st]);
+          if (g + 1 >= g1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+      if (g1 <= g0 && lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------ epilogue: RED into the scratch
+    const int ew = warp;
+    int tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait_backoff(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      if (p.swap) {
+        // TMEM lane = output channel k, column = x row nt*BN + j
+        const int k = ew * 32 + lane;
+        const bool live = k < p.K && g1 > g0;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int m = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || m >= p.M) break;
+            red_add(p.acc + std::int64_t(m) * kBM + k, v[j]);
+          }
+        }
+      } else {
+        const int m = mt * kBM + ew * 32 + lane;
+        const bool live = m < p.M && g1 > g0;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || k >= p.K) break;
+            red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// dW[k][c][r][s] = beta * dW + alpha * scratch(row = (r*S + s)*C + c, k)
+struct LFinal {
+  const float* acc;
+  float* dw;
+  float alpha, beta;
+  int C, R, S, rpad, swap;
+  std::int64_t n;  // K*C*R*S
+};
+__global__ void __launch_bounds__(256) bfl_finalize_kernel(const LFinal f) {
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < f.n;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    const int s = int(i % f.S);
+    std::int64_t t = i / f.S;
+    const int r = int(t % f.R);
+    t /= f.R;
+    const int c = int(t % f.C), k = int(t / f.C);
+    const int row = (r * f.S + s) * f.C + c;
+    const float v = f.swap ? f.acc[std::int64_t(row) * kBM + k] : f.acc[std::int64_t(k) * f.rpad + row];
+    f.dw[i] = f.beta == 0.f ? f.alpha * v : f.alpha * v + f.beta * f.dw[i];
+  }
+}
+
+int sm_count() {
+  static int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+}  // namespace
+
+bool bfl_supports(const ConvShape& s) {
+  const LGeo g = make_lgeo(s);
+  // few-channel path: tap masks are 32 bits, table offsets int32
+  const bool few_ok = s.C % 8 == 0 || (s.R <= 32 && s.S <= 32 && std::int64_t(s.C) * s.H * s.W < (1ll << 31));
+  return few_ok && g.npx + 64 < (std::int64_t(1) << 31) && g.M < (1 << 24) && s.K < (1 << 24);
+}
+
+std::int64_t bfl_workspace(const ConvShape& s) { return std::int64_t(scratch_bytes(make_lgeo(s))); }
+
+cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
+                    cudaStream_t st) {
+  const LGeo g = make_lgeo(s);
+  float* acc = static_cast<float*>(ws);
+  cudaError_t e = cudaMemsetAsync(acc, 0, std::size_t(rows_pad(g)) * cols_pad(g) * 4, st);
+  if (e != cudaSuccess) return e;
+  const int sms = sm_count();
+  LParams p{};
+  p.x = x;
+  p.dy = dy;
+  p.acc = acc;
+  p.C = g.C; p.H = g.H; p.W = g.W; p.K = g.K; p.R = g.R; p.S = g.S;
+  p.sh = g.sh; p.sw = g.sw; p.ph = g.ph; p.pw = g.pw; p.OW = g.OW;
+  p.OHW = g.OH * g.OW;
+  p.HW = g.H * g.W;
+  p.M = g.M;
+  p.npx = g.npx;
+  p.CHW = std::int64_t(g.C) * p.HW;
+  p.KOHW = std::int64_t(g.K) * p.OHW;
+  p.swap = g.swap;
+  p.BN = g.BN;
+  p.m_tiles = g.m_tiles;
+  p.tiles = g.m_tiles * g.n_tiles;
+  p.steps = g.steps;
+  p.rpad = rows_pad(g);
+  p.dbg = tune("bfl_dbg", 0);
+  p.fd_ohw = FastDiv(std::uint32_t(p.OHW));
+  p.fd_ow = FastDiv(std::uint32_t(g.OW));
+  p.fd_C = FastDiv(std::uint32_t(g.C));
+  p.fd_S = FastDiv(std::uint32_t(g.S));
+  // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
+  const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * sms / p.tiles));
+  p.steps_per_unit = (p.steps + splits - 1) / splits;
+  p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
+  const int stage_bytes = kBM * 128 + ((g.BN * 128 + 1023) & ~1023);
+  p.stages = std::max(2, std::min({kMaxStages, tune("bfl_stages", 8), (200 * 1024) / stage_bytes}));
+  const int smem = p.stages * stage_bytes + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(bfl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);  // + 2 KB static xtab
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, p);
+  if (e != cudaSuccess) return e;
+  LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, s.w_elems()};
+  return launch_pdl(bfl_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256), 0,
+                    st, f);
+}
+
+}  // namespace ucudnn

@@ -64,6 +64,7 @@ struct PrecompParams {
   // phase scatter epilogue (strided BackwardData): column (a, b, c) of
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
+  int pair;      // 1x1 stride-2 block stores (phase_store)
   int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
   int stages, ksub, prof, cps;
   FastDiv fd_Cr, fd_ssw;
@@ -84,6 +85,36 @@ __device__ __forceinline__ void tapless_phases(const P& p, float* base, int c, i
       float* dst = base + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
       *dst = p.beta == 0.f ? 0.f : p.beta * *dst;
     }
+}
+
+// One stride-phase BackwardData output: column col of the pixel whose dx
+// block starts at (hb, wb). pair = 1x1 stride-2 unpadded with even dx extents
+// (ResNet shortcuts): only (0, 0) of the 2x2 block has a tap, so the thread
+// writes the whole block as two float2 rows -- warp-contiguous along j,
+// instead of four scattered stride-2 scalars per column.
+template <typename P>
+__device__ __forceinline__ void phase_store(const P& p, std::int64_t obase, int col, int hb, int wb, float val) {
+  if (p.pair) {
+    float2* d0 = reinterpret_cast<float2*>(p.out + obase + (std::int64_t(col) * p.Hr + hb) * p.Wr + wb);
+    float2* d1 = d0 + (p.Wr >> 1);
+    if (p.beta == 0.f) {
+      *d0 = make_float2(val, 0.f);
+      *d1 = make_float2(0.f, 0.f);
+    } else {
+      const float2 o0 = *d0, o1 = *d1;
+      *d0 = make_float2(val + p.beta * o0.x, p.beta * o0.y);
+      *d1 = make_float2(p.beta * o1.x, p.beta * o1.y);
+    }
+    return;
+  }
+  std::uint32_t ab, c, a, b;
+  p.fd_Cr.divmod(std::uint32_t(col), ab, c);
+  p.fd_ssw.divmod(ab, a, b);
+  if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
+  const int h = hb + int(a), w = wb + int(b);
+  if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) return;
+  float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
+  *dst = p.beta == 0.f ? val : val + p.beta * *dst;
 }
 
 __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& mt, int& nt) {
@@ -273,15 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const int col = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || col >= p.Nout) break;
-            std::uint32_t ab, c, a, b;
-            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
-            p.fd_ssw.divmod(ab, a, b);
-            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
-            const int h = hb + int(a), w = wb + int(b);
-            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
-            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
-            const float val = p.alpha * v[j];
-            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+            phase_store(p, obase, col, hb, wb, p.alpha * v[j]);
           }
           continue;
         }
@@ -465,15 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const int col = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || col >= p.Nout) break;
-            std::uint32_t ab, c, a, b;
-            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
-            p.fd_ssw.divmod(ab, a, b);
-            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
-            const int h = hb + int(a), w = wb + int(b);
-            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
-            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
-            const float val = p.alpha * v[j];
-            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+            phase_store(p, obase, col, hb, wb, p.alpha * v[j]);
           }
           continue;
         }
@@ -647,7 +662,7 @@ struct StripParams {
   int OH, OW, Nout, P;
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
-  int sAh, sBw;
+  int sAh, sBw, pair;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
 };
@@ -815,20 +830,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *dst = p.beta == 0.f ? val : val + p.beta * *dst;
               }
             } else {
-              float* base = p.out + std::int64_t(n) * p.Cr * p.Hr * p.Wr;
+              const std::int64_t obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
               const int hb = int(oh) * p.ssh - p.sph, wb = int(ow) * p.ssw - p.spw;
               for (int r = 0; r < 32; ++r) {
                 const int col = ew * 32 + r;
                 if (col >= p.Nout) break;
-                std::uint32_t ab, c, a, b;
-                p.fd_Cr.divmod(std::uint32_t(col), ab, c);
-                p.fd_ssw.divmod(ab, a, b);
-                if (ab == 0) tapless_phases(p, base, int(c), hb, wb);
-                const int h = hb + int(a), w = wb + int(b);
-                if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
-                float* dst = base + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
-                const float val = p.alpha * tp[r * 33 + lane];
-                *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+                phase_store(p, obase, col, hb, wb, p.alpha * tp[r * 33 + lane]);
               }
             }
           }
@@ -863,15 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const int col = int(nt) * p.BN + c0 + j;
             if (c0 + j >= p.BN || col >= p.Nout) break;
-            std::uint32_t ab, c, a, b;
-            p.fd_Cr.divmod(std::uint32_t(col), ab, c);
-            p.fd_ssw.divmod(ab, a, b);
-            if (ab == 0) tapless_phases(p, p.out + obase, int(c), hb, wb);
-            const int h = hb + int(a), w = wb + int(b);
-            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
-            float* dst = p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w;
-            const float val = p.alpha * v[j];
-            *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+            phase_store(p, obase, col, hb, wb, p.alpha * v[j]);
           }
           continue;
         }
@@ -969,6 +968,13 @@ struct Geo {
   PhaseFilter pf{};
   int Hr = 0, Wr = 0, rph = 0, rpw = 0;  // the real dx extent and conv padding
 };
+
+// 1x1 stride-2 unpadded BackwardData over even dx extents: each GEMM pixel
+// owns a whole 2x2 dx block (phase_store's float2 path).
+int phase_pair(const Geo& g) {
+  return g.phase && g.pf.sh == 2 && g.pf.sw == 2 && g.pf.R == 1 && g.pf.S == 1 && g.rph == 0 && g.rpw == 0 &&
+         g.Hr % 2 == 0 && g.Wr % 2 == 0 && g.Hout * 2 == g.Hr && g.Wout * 2 == g.Wr && tune("pair", 1);
+}
 
 // Strip path (stride-1 after the s2d / phase rewrites, >= 32-channel rows):
 // geometry of the padded input and of the per-chunk strip.
@@ -1098,6 +1104,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.fd_ssw = FastDiv(std::uint32_t(g.pf.bw));
     p.sAh = std::min(g.pf.sh, g.pf.R);
     p.sBw = g.pf.bw;
+    p.pair = phase_pair(g);
   }
   const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
@@ -1210,6 +1217,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.fd_ssw = FastDiv(std::uint32_t(g.pf.bw));
     p.sAh = std::min(g.pf.sh, g.pf.R);
     p.sBw = g.pf.bw;
+    p.pair = phase_pair(g);
   }
   if (two_sm) {
     CUtensorMap bmap;

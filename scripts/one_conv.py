@@ -14,7 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--layer", default="a2"); ap.add_argument("--op", type=int, default=0)
 ap.add_argument("--algo", type=int, default=0); ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--shape", default="", help="N,C,H,W,K,R,S,pad,stride (overrides --layer)")
 a = ap.parse_args()
+if a.shape:
+    v = [int(t) for t in a.shape.split(",")]
+    LAYERS["shape"] = ConvShape(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[7], v[8], v[8])
+    a.layer = "shape"
 s = LAYERS[a.layer].with_batch(a.batch)
 dev = torch.device("cuda")
 x = torch.randn(s.N, s.C, s.H, s.W, device=dev); w = torch.randn(s.K, s.C, s.R, s.S, device=dev)

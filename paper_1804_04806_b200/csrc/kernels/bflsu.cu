@@ -57,6 +57,7 @@ struct LGeo {
   int N, C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
   int M;  // C*R*S GEMM rows of x
   int swap, BN, m_tiles, n_tiles;
+  int two;        // CTA pairs (cta_group::2): m_tiles counts 256-row pair tiles
   long long npx;  // N*OH*OW
   int steps;      // 32-pixel chunks
 };
@@ -81,13 +82,16 @@ LGeo make_lgeo(const ConvShape& s) {
     g.BN = round_up((s.K + nt - 1) / nt, 16);
     g.n_tiles = (s.K + g.BN - 1) / g.BN;
     g.m_tiles = (g.M + kBM - 1) / kBM;
+    // pairs: each CTA gathers its own 128 x rows and half of the dy rows
+    g.two = tune("bfl2", 1) && g.m_tiles >= 2;
+    if (g.two) g.m_tiles = (g.M + 2 * kBM - 1) / (2 * kBM);
   }
   return g;
 }
 
 // RED scratch in the GEMM's own layout: non-swap [k][x row] (pitch rows_pad),
 // swap [x row][k] (pitch 128); 32 lanes reduce into 32 consecutive floats.
-int rows_pad(const LGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM; }
+int rows_pad(const LGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM * (g.two ? 2 : 1); }
 int cols_pad(const LGeo& g) { return g.swap ? kBM : g.n_tiles * g.BN; }
 std::size_t scratch_bytes(const LGeo& g) { return (std::size_t(rows_pad(g)) * cols_pad(g) * 4 + 255) / 256 * 256; }
 
@@ -137,6 +141,100 @@ __device__ __forceinline__ std::uint32_t range_mask(int lo, int hi, int n) {
   return h & ~((1u << lo) - 1u);
 }
 
+// The gather side shared by both kernels: per-thread constants, the
+// per-unit row table (few-channel path) and one 32-pixel step into a stage.
+struct Gatherer {
+  const LParams& p;
+  int lane, pw;
+  bool c8;                 // C % 8 == 0: an 8-row group is 8 channels of one tap
+  std::uint32_t swz[8];    // this lane's byte offset in an 8-row swizzle atom, per row q % 8
+  std::uint32_t xj[8], dj[8];  // byte offsets of rows j of a group (independent adds)
+  int2* xtab;
+  int xm0, xrows, dk0, drows;  // current unit: x rows [xm0, +xrows), dy rows [dk0, +drows)
+
+  __device__ __forceinline__ Gatherer(const LParams& p_, int lane_, int pw_, int2* tab)
+      : p(p_), lane(lane_), pw(pw_), c8(p_.C % 8 == 0), xtab(tab) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
+      xj[j] = std::uint32_t(j * p.HW * 4);
+      dj[j] = std::uint32_t(j * p.OHW * 4);
+    }
+  }
+
+  __device__ __forceinline__ void unit(int xm0_, int xrows_, int dk0_, int drows_) {
+    xm0 = xm0_;
+    xrows = xrows_;
+    dk0 = dk0_;
+    drows = drows_;
+    if (!c8) {
+      // this warp's rows of the tile: (c*HW + r*W + s, r << 8 | s)
+      for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8)
+        if (lane < 8 && q0 + lane < xrows) {
+          std::uint32_t rs, c, r, s;
+          p.fd_C.divmod(std::uint32_t(xm0 + q0 + lane), rs, c);
+          p.fd_S.divmod(rs, r, s);
+          xtab[q0 + lane] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 8 | s));
+        }
+      __syncwarp();
+    }
+  }
+
+  // x rows -> smem at xs, dy rows -> smem at ds (SW128 K-major, row q at q*128)
+  __device__ __forceinline__ void step(int g, std::uint32_t xs, std::uint32_t ds) const {
+    const long long pg = (long long)g * 32 + lane;  // this lane's pixel
+    const bool valid = pg < p.npx;
+    std::uint32_t n, pix, oh, ow;
+    p.fd_ohw.divmod(std::uint32_t(valid ? pg : 0), n, pix);
+    p.fd_ow.divmod(pix, oh, ow);
+    const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
+    const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
+    if (c8) {
+      // one bounds test per group, then consecutive channel planes
+      for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
+        std::uint32_t rs, c, r, s;
+        p.fd_C.divmod(std::uint32_t(xm0 + q0), rs, c);
+        p.fd_S.divmod(rs, r, s);
+        const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
+        const std::uint32_t sz = ok ? 4u : 0u, dst = xs + q0 * 128;
+        const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
+        const int qn = min(8, xrows - q0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < qn) cp_async4a(dst + swz[j], a + xj[j], sz);
+      }
+    } else {
+      // few channels (taps straddle groups): per-row (offset, tap) from the
+      // smem table, bounds from this lane's valid-tap bitmasks
+      const std::uint32_t vr = valid ? range_mask(-ihb, p.H - ihb, p.R) : 0u;
+      const std::uint32_t vs = range_mask(-iwb, p.W - iwb, p.S);
+      const std::uint64_t xa = reinterpret_cast<std::uint64_t>(xl);
+      for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
+        const std::uint32_t dst = xs + q0 * 128;
+        const int qn = min(8, xrows - q0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < qn) {
+            const int2 e = xtab[q0 + j];
+            const std::uint32_t ok = (vr >> (e.y >> 8)) & (vs >> (e.y & 255)) & 1u;
+            cp_async4a(dst + swz[j], xa + std::int64_t(e.x) * 4, ok * 4u);
+          }
+        }
+      }
+    }
+    const float* dl = p.dy + (long long)n * p.KOHW + pix;
+    const std::uint32_t sz = valid ? 4u : 0u;
+    for (int q0 = pw * 8; q0 < drows; q0 += kProd * 8) {
+      const std::uint64_t a = reinterpret_cast<std::uint64_t>(dl + (long long)(dk0 + q0) * p.OHW);
+      const std::uint32_t dst = ds + q0 * 128;
+      const int qn = min(8, drows - q0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < qn) cp_async4a(dst + swz[j], a + dj[j], sz);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -172,23 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
 
   if (warp >= 5) {
     // ------------------------------------------------ gather producers
-    const int pw = warp - 5;
+    Gatherer ga(p, lane, warp - 5, xtab);
     const std::uint32_t sbase = smem_u32(smem);
-    // this lane's byte offset inside an 8-row swizzle atom, per row q % 8
-    std::uint32_t swz[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
     // x rows go to A (non-swap) or B (swap); dy rows to the other
     const std::uint32_t x_off = p.swap ? a_bytes : 0, d_off = p.swap ? 0 : a_bytes;
-    const bool c8 = p.C % 8 == 0;  // 8-row groups never straddle a tap
-    // byte offsets of rows j = 0..7 of a group (independent adds, no
-    // dependent address chain through the 8 cp.async of a group)
-    std::uint32_t xj[8], dj[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      xj[j] = std::uint32_t(j * p.HW * 4);
-      dj[j] = std::uint32_t(j * p.OHW * 4);
-    }
     int st = 0;
     std::uint32_t ph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -196,89 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
       const int xm0 = p.swap ? nt * p.BN : mt * kBM;  // first x row of the tile
-      const int xrows = min(p.swap ? p.BN : kBM, p.M - xm0);
       const int dk0 = p.swap ? 0 : nt * p.BN;
-      const int drows = min(p.swap ? kBM : p.BN, p.K - dk0);
-      if (!c8) {
-        // this warp's rows of the tile: (c*HW + r*W + s, r << 8 | s)
-        for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8)
-          if (lane < 8 && q0 + lane < xrows) {
-            std::uint32_t rs, c, r, s;
-            p.fd_C.divmod(std::uint32_t(xm0 + q0 + lane), rs, c);
-            p.fd_S.divmod(rs, r, s);
-            xtab[q0 + lane] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 8 | s));
-          }
-        __syncwarp();
-      }
+      ga.unit(xm0, min(p.swap ? p.BN : kBM, p.M - xm0), dk0, min(p.swap ? kBM : p.BN, p.K - dk0));
       for (int g = g0; g < g1; ++g) {
         mbar_wait(&empty[st], ph ^ 1);
-        if (p.dbg == 1) {
-          cp_async_arrive(&full[st]);
-          if (++st == kStages) {
-            st = 0;
-            ph ^= 1;
-          }
-          continue;
-        }
-        // this lane's pixel
-        const long long pg = (long long)g * 32 + lane;
-        const bool valid = pg < p.npx;
-        std::uint32_t n, pix, oh, ow;
-        p.fd_ohw.divmod(std::uint32_t(valid ? pg : 0), n, pix);
-        p.fd_ow.divmod(pix, oh, ow);
-        const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
-        const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
         const std::uint32_t sst = sbase + st * stage_bytes;
-        // x rows: 8-row groups pw, pw + 8, ...
-        if (c8) {
-          // a group is 8 channels of one tap: one bounds test, then
-          // consecutive channel planes
-          for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
-            std::uint32_t rs, c, r, s;
-            p.fd_C.divmod(std::uint32_t(xm0 + q0), rs, c);
-            p.fd_S.divmod(rs, r, s);
-            const std::uint32_t dst = sst + x_off + q0 * 128;
-            const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
-            const std::uint32_t sz = ok ? 4u : 0u;
-            const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
-            const int qn = min(8, xrows - q0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < qn) cp_async4a(dst + swz[j], a + xj[j], sz);
-          }
-        } else {
-          // few channels (taps straddle groups): per-row (offset, tap) from
-          // the smem table, bounds from this lane's valid-tap bitmasks
-          const std::uint32_t vr = valid ? range_mask(-ihb, p.H - ihb, p.R) : 0u;
-          const std::uint32_t vs = range_mask(-iwb, p.W - iwb, p.S);
-          const std::uint64_t xa = reinterpret_cast<std::uint64_t>(xl);
-          for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
-            const std::uint32_t dst = sst + x_off + q0 * 128;
-            const int qn = min(8, xrows - q0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (j < qn) {
-                const int2 e = xtab[q0 + j];
-                const std::uint32_t ok = (vr >> (e.y >> 8)) & (vs >> (e.y & 255)) & 1u;
-                cp_async4a(dst + swz[j], xa + std::int64_t(e.x) * 4, ok * 4u);
-              }
-            }
-          }
-        }
-        // dy rows
-        {
-          const float* dl = p.dy + (long long)n * p.KOHW + pix;
-          const std::uint32_t sz = valid ? 4u : 0u;
-          for (int q0 = pw * 8; q0 < drows; q0 += kProd * 8) {
-            const float* src = dl + (long long)(dk0 + q0) * p.OHW;
-            const std::uint32_t dst = sst + d_off + q0 * 128;
-            const std::uint64_t a = reinterpret_cast<std::uint64_t>(src);
-            const int qn = min(8, drows - q0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < qn) cp_async4a(dst + swz[j], a + dj[j], sz);
-          }
-        }
+        if (p.dbg != 1) ga.step(g, sst + x_off, sst + d_off);
         // arrives once every cp.async this thread issued so far has landed
         cp_async_arrive(&full[st]);
         if (++st == kStages) {
@@ -375,6 +383,162 @@ __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
   }
 }
 
+// CTA-pair variant (K > 128, roles not swapped): tcgen05.mma.cta_group::2,
+// M = 256 x rows (128 gathered by each CTA into its own smem) x BN output
+// channels, the dy rows split along N (BN/2 gathered by each CTA) -- half
+// the dy gather per SM of the 1-SM kernel. Rank 0 issues the MMAs; rank 1's
+// warp 4 relays its producers' completion (its own cp.async full barrier)
+// to rank 0's full barrier after the proxy fence. Commits multicast to both
+// CTAs; both epilogues release rank 0's accumulator barrier.
+__global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cluster_rank();
+  const int bh = p.BN / 2;
+  const std::uint32_t a_bytes = kBM * 128;
+  const std::uint32_t stage_bytes = a_bytes + ((std::uint32_t(bh) * 128 + 1023) & ~1023u);
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  __shared__ int2 xtab[kMaxBN];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kProd * 32 + (rank == 0 ? 1 : 0));  // + rank 1's relay
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 4) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int units = p.tiles * p.splits;  // tiles = pair tiles x n tiles
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp >= 5) {
+    // ------------------------------------------------ gather producers
+    Gatherer ga(p, lane, warp - 5, xtab);
+    const std::uint32_t sbase = smem_u32(smem);
+    int st = 0;
+    std::uint32_t ph = 0;
+    for (int u = cid; u < units; u += ncl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int xm0 = mt * 2 * kBM + int(rank) * kBM, dk0 = nt * p.BN + int(rank) * bh;
+      ga.unit(xm0, min(kBM, p.M - xm0), dk0, min(bh, p.K - dk0));
+      for (int g = g0; g < g1; ++g) {
+        mbar_wait(&empty[st], ph ^ 1);
+        const std::uint32_t sst = sbase + st * stage_bytes;
+        if (p.dbg != 1) ga.step(g, sst, sst + a_bytes);
+        cp_async_arrive(&full[st]);
+        if (++st == kStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 4) {
+    if (rank == 0) {
+      // ------------------------------------------------ MMA issuer (pair)
+      const std::uint32_t idesc = idesc_tf32(2 * kBM, p.BN);
+      const std::uint32_t sbase = smem_u32(smem);
+      int it = 0, tl = 0;
+      for (int u = cid; u < units; u += ncl, ++tl) {
+        const int split = u / p.tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        const int acc = tl & 1;
+        mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+        for (int g = g0; g < g1; ++g, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            fence_async_smem();
+            const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+            if (p.dbg != 2)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                mma_tf32_2sm(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
+                             (g != g0 || q != 0) ? 1u : 0u);
+            mma_commit_2sm(&empty[st], 3);
+            if (g + 1 >= g1) mma_commit_2sm(&tfull[acc], 3);
+          }
+          __syncwarp();
+        }
+        if (g1 <= g0 && lane == 0) mma_commit_2sm(&tfull[acc], 3);
+        __syncwarp();
+      }
+    } else if (lane == 0) {
+      // ------------------------------------------------ relay (rank 1)
+      const std::uint32_t full0 = mapa(smem_u32(&full[0]), 0);
+      int it = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int split = u / p.tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        for (int g = g0; g < g1; ++g, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          fence_async_smem();
+          mbar_arrive_remote(full0 + std::uint32_t(st) * 8);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue: RED into the scratch
+    const int ew = warp;
+    const std::uint32_t tempty0 = mapa(smem_u32(&tempty[0]), 0);
+    int tl = 0;
+    for (int u = cid; u < units; u += ncl, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait_backoff(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const int m = mt * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
+      const bool live = m < p.M && g1 > g0;
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (!live) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = nt * p.BN + c0 + j;
+          if (c0 + j >= p.BN || k >= p.K) break;
+          red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_remote(tempty0 + std::uint32_t(acc) * 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_free_2sm<512>(tmem);
+  }
+}
+
 // dW[k][c][r][s] = beta * dW + alpha * scratch(row = (r*S + s)*C + c, k)
 struct LFinal {
   const float* acc;
@@ -449,19 +613,42 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.fd_C = FastDiv(std::uint32_t(g.C));
   p.fd_S = FastDiv(std::uint32_t(g.S));
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
-  const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * sms / p.tiles));
+  const int slots = g.two ? sms / 2 : sms;
+  const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
-  const int stage_bytes = kBM * 128 + ((g.BN * 128 + 1023) & ~1023);
-  p.stages = std::max(2, std::min({kMaxStages, tune("bfl_stages", 8), (200 * 1024) / stage_bytes}));
+  const int stage_bytes = kBM * 128 + (((g.two ? g.BN / 2 : g.BN) * 128 + 1023) & ~1023);
+  p.stages = std::max(2, std::min({kMaxStages, tune("bfl_stages", 4), (200 * 1024) / stage_bytes}));
+  // 4 stages: the rest of the 228 KB stays L1, which catches the taps' re-reads
+  // of x (AlexNet conv3-5 at 256 images: 8 stages 282/312/208 us, 4 stages
+  // 249/265/175 us)
   const int smem = p.stages * stage_bytes + 1024 + 256;
   static bool attr = false;
   if (!attr) {
-    e = cudaFuncSetAttribute(bfl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);  // + 2 KB static xtab
+    // + 2 KB static xtab
+    e = cudaFuncSetAttribute(bfl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(bfl2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, p);
+  if (g.two) {
+    count_launch();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(sms / 2, p.tiles * p.splits));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = std::size_t(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = 2;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, bfl2_kernel, p);
+  } else {
+    e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, p);
+  }
   if (e != cudaSuccess) return e;
   LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, s.w_elems()};
   return launch_pdl(bfl_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256), 0,

@@ -103,7 +103,8 @@ struct LParams {
   long long npx, CHW, KOHW;
   int swap, BN, m_tiles, tiles, splits, steps, steps_per_unit, stages, rpad;
   int dbg;  // diagnostic (UCUDNN_TUNE=bfl_dbg): 1 skip the gathers, 2 skip the MMAs
-  FastDiv fd_ohw, fd_ow, fd_C, fd_S;
+  FastDiv fd_ohw, fd_ow, fd_C, fd_S, fd_RS;
+  int crs;  // x row order: 1 (c, r, s) = dW order, 0 (r, s, c)
 };
 
 // 4-byte gather; src_size 0 writes a zero (src is then never dereferenced)
@@ -153,7 +154,7 @@ struct Gatherer {
   int xm0, xrows, dk0, drows;  // current unit: x rows [xm0, +xrows), dy rows [dk0, +drows)
 
   __device__ __forceinline__ Gatherer(const LParams& p_, int lane_, int pw_, int2* tab)
-      : p(p_), lane(lane_), pw(pw_), c8(p_.C % 8 == 0), xtab(tab) {
+      : p(p_), lane(lane_), pw(pw_), c8(!p_.crs && p_.C % 8 == 0), xtab(tab) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
@@ -169,10 +170,15 @@ struct Gatherer {
     drows = drows_;
     if (!c8) {
       // this warp's rows of the tile: (c*HW + r*W + s, r << 8 | s)
+      // (few channels, or (c, r, s) order)
       for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8)
         if (lane < 8 && q0 + lane < xrows) {
           std::uint32_t rs, c, r, s;
-          p.fd_C.divmod(std::uint32_t(xm0 + q0 + lane), rs, c);
+          if (p.crs) {
+            p.fd_RS.divmod(std::uint32_t(xm0 + q0 + lane), c, rs);
+          } else {
+            p.fd_C.divmod(std::uint32_t(xm0 + q0 + lane), rs, c);
+          }
           p.fd_S.divmod(rs, r, s);
           xtab[q0 + lane] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 8 | s));
         }
@@ -544,7 +550,7 @@ struct LFinal {
   const float* acc;
   float* dw;
   float alpha, beta;
-  int C, R, S, rpad, swap;
+  int C, R, S, rpad, swap, crs;
   std::int64_t n;  // K*C*R*S
 };
 __global__ void __launch_bounds__(256) bfl_finalize_kernel(const LFinal f) {
@@ -555,7 +561,7 @@ __global__ void __launch_bounds__(256) bfl_finalize_kernel(const LFinal f) {
     const int r = int(t % f.R);
     t /= f.R;
     const int c = int(t % f.C), k = int(t / f.C);
-    const int row = (r * f.S + s) * f.C + c;
+    const int row = f.crs ? int(i % (std::int64_t(f.C) * f.R * f.S)) : (r * f.S + s) * f.C + c;
     const float v = f.swap ? f.acc[std::int64_t(row) * kBM + k] : f.acc[std::int64_t(k) * f.rpad + row];
     f.dw[i] = f.beta == 0.f ? f.alpha * v : f.alpha * v + f.beta * f.dw[i];
   }
@@ -576,7 +582,8 @@ int sm_count() {
 bool bfl_supports(const ConvShape& s) {
   const LGeo g = make_lgeo(s);
   // few-channel path: tap masks are 32 bits, table offsets int32
-  const bool few_ok = s.C % 8 == 0 || (s.R <= 32 && s.S <= 32 && std::int64_t(s.C) * s.H * s.W < (1ll << 31));
+  const bool few_ok = (s.C % 8 == 0 && !tune("bfl_crs", 0)) ||
+                      (s.R <= 32 && s.S <= 32 && std::int64_t(s.C) * s.H * s.W < (1ll << 31));
   return few_ok && g.npx + 64 < (std::int64_t(1) << 31) && g.M < (1 << 24) && s.K < (1 << 24);
 }
 
@@ -612,6 +619,12 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.fd_ow = FastDiv(std::uint32_t(g.OW));
   p.fd_C = FastDiv(std::uint32_t(g.C));
   p.fd_S = FastDiv(std::uint32_t(g.S));
+  p.fd_RS = FastDiv(std::uint32_t(g.R * g.S));
+  // (c, r, s) rows (UCUDNN_TUNE=bfl_crs=1): a tile then holds every tap of a
+  // few channels and the taps' overlapping x reads hit L1 (hit rate 35 -> 58 %,
+  // L2 throughput halved), but every row needs the table path and AlexNet
+  // conv2 at 256 images measured 503 -> 787 us, so (r, s, c) stays
+  p.crs = tune("bfl_crs", 0);
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
@@ -650,7 +663,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
     e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, p);
   }
   if (e != cudaSuccess) return e;
-  LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, s.w_elems()};
+  LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, p.crs, s.w_elems()};
   return launch_pdl(bfl_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256), 0,
                     st, f);
 }

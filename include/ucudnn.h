@@ -69,7 +69,7 @@ typedef enum {
   UCUDNN_ALGO_GEMM = 3,              /* explicit im2col / col2im + tiled tcgen05 GEMM                  */
   UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (3x3 s1 F/BD): 36 batched tcgen05 GEMMs             */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* TMA-fed implicit GEMM on re-laid copies (all ops), ws ~ b   */
-  UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BackwardFilter only: cp.async-gathered NCHW operands, ws O(1) */
+  UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BF: cp.async-gathered NCHW operands; BD (strided, few C): GEMM+col2im via smem; ws O(1) */
   UCUDNN_ALGO_COUNT = 7
 } ucudnnAlgo_t;
 

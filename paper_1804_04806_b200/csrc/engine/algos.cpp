@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "../kernels/bdscatter.h"
 #include "../kernels/bflsu.h"
 #include "../kernels/fft.h"
 #include "../kernels/gemm.h"
@@ -61,14 +62,21 @@ cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b
   return winograd_run(4, op, s, a, b, out, ws, alpha, beta, st, flags);
 }
 
-// BackwardFilter with operands gathered by cp.async straight from NCHW x / dy
-// (bflsu.cu): a small fixed workspace instead of PRECOMP's per-image copies.
-bool gather_supports(int op, const ConvShape& s) { return op == 2 && bfl_supports(s); }
-std::int64_t gather_workspace(int op, const ConvShape& s) { return op == 2 ? bfl_workspace(s) : 0; }
+// Gather/scatter family: BackwardFilter with operands gathered by cp.async
+// straight from NCHW x / dy (bflsu.cu: a small fixed workspace instead of
+// PRECOMP's per-image copies), and BackwardData of few-channel strided layers
+// as GEMM + col2im fused through a shared-memory patch (bdscatter.cu).
+bool gather_supports(int op, const ConvShape& s) {
+  return (op == 2 && bfl_supports(s)) || (op == 1 && bds_supports(s));
+}
+std::int64_t gather_workspace(int op, const ConvShape& s) {
+  return op == 2 ? bfl_workspace(s) : op == 1 ? bds_workspace(s) : 0;
+}
 cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                        float beta, cudaStream_t st, int) {
-  if (op != 2) return cudaErrorInvalidValue;
-  return bfl_run(s, a, b, out, ws, alpha, beta, st);
+  if (op == 2) return bfl_run(s, a, b, out, ws, alpha, beta, st);
+  if (op == 1) return bds_run(s, a, b, out, alpha, beta, st);
+  return cudaErrorInvalidValue;
 }
 
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};

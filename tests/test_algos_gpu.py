@@ -101,3 +101,16 @@ def test_alpha_beta(cuda, algo, op, s):
         assert np.linalg.norm(got - ref) <= TOL[algo] * np.linalg.norm(ref)
         return
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("spec", ["2 3 31 31 16 11 11 2 4", "2 3 40 40 64 7 7 3 2", "2 16 14 14 32 1 1 0 2"])
+def test_experimental_bd_scatter(cuda, spec):
+    """The GEMM + col2im BackwardData kernel (bdscatter.cu) is off by default
+    (UCUDNN_TUNE=bds=1 enables it as algorithm 6 for op 1); the knob is read
+    once per process, so run it in a child."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, UCUDNN_TUNE="bds=1")
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *spec.split(), "1", "6"],
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert "exact True" in out.stdout, out.stdout + out.stderr

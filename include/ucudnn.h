@@ -70,7 +70,8 @@ typedef enum {
   UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (3x3 s1 F/BD): 36 batched tcgen05 GEMMs             */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* TMA-fed implicit GEMM on re-laid copies (all ops), ws ~ b   */
   UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BF: cp.async-gathered NCHW operands; BD (strided, few C): GEMM+col2im via smem; ws O(1) */
-  UCUDNN_ALGO_COUNT = 7
+  UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_SLICED = 7, /* F/BD: PRECOMP over reduction-channel slices, copy <= 40 MiB */
+  UCUDNN_ALGO_COUNT = 8
 } ucudnnAlgo_t;
 
 /* Returned by Get*Algorithm: a plan handle, >= UCUDNN_VIRTUAL_ALGO_BASE

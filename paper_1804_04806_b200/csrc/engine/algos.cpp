@@ -79,6 +79,13 @@ cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* 
   return cudaErrorInvalidValue;
 }
 
+bool sliced_supports(int op, const ConvShape& s) { return precomp_sliced_supports(op, s); }
+std::int64_t sliced_workspace(int op, const ConvShape& s) { return precomp_sliced_workspace(op, s); }
+cudaError_t sliced_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
+                       float beta, cudaStream_t st, int) {
+  return precomp_sliced_run(op, s, a, b, out, ws, alpha, beta, st);
+}
+
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
 const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
 const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
@@ -86,6 +93,7 @@ const AlgoImpl kFft{2, "FFT", fft_supports, fft_workspace, fft_run};
 const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 const AlgoImpl kGather{6, "IMPLICIT_GATHER_GEMM", gather_supports, gather_workspace, gather_run};
+const AlgoImpl kSliced{7, "IMPLICIT_PRECOMP_GEMM_SLICED", sliced_supports, sliced_workspace, sliced_run};
 
 }  // namespace
 
@@ -98,10 +106,11 @@ const AlgoImpl* find_algo(int id) {
     case 3: return &kGemm;
     case 5: return &kPrecomp;
     case 6: return &kGather;
+    case 7: return &kSliced;
     default: return nullptr;
   }
 }
 
-int algo_count() { return 7; }
+int algo_count() { return 8; }
 
 }  // namespace ucudnn

@@ -117,6 +117,31 @@ __device__ __forceinline__ void phase_store(const P& p, std::int64_t obase, int 
   *dst = p.beta == 0.f ? val : val + p.beta * *dst;
 }
 
+// 32 output columns of one row (column j at base[j * pitch], n valid):
+// beta == 0 stores; otherwise every old value is loaded before the first
+// store, so the 32 load latencies overlap instead of serialising behind
+// the stores (the sliced algorithm runs most of its calls with beta = 1)
+template <typename P>
+__device__ __forceinline__ void store_row32(const P& p, float* base, int n, std::int64_t pitch, const float (&v)[32]) {
+  if (p.beta == 0.f) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) base[j * pitch] = p.alpha * v[j];
+  } else {
+    // 8 loads in flight at a time: the 1-SM kernel must stay <= 128
+    // registers to run two CTAs per SM
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += 8) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = j0 + j < n ? base[(j0 + j) * pitch] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < n) base[(j0 + j) * pitch] = p.alpha * v[j0 + j] + p.beta * o[j];
+    }
+  }
+}
+
 __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& mt, int& nt) {
   std::uint32_t q, r;
   p.fd_mt.divmod(std::uint32_t(t), q, r);
@@ -308,13 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = nt * p.BN + c0 + j;
-          if (c0 + j >= p.BN || col >= p.Nout) break;
-          float* dst = p.out + obase + std::int64_t(col) * p.P;
-          const float val = p.alpha * v[j];
-          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        {
+          const int col0 = nt * p.BN + c0;
+          store_row32(p, p.out + obase + std::int64_t(col0) * p.P, min(32, min(p.BN - c0, p.Nout - col0)),
+                      std::int64_t(p.P), v);
         }
       }
       tc_fence_before();
@@ -492,13 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = nt * p.BN + c0 + j;
-          if (c0 + j >= p.BN || col >= p.Nout) break;
-          float* dst = p.out + obase + std::int64_t(col) * p.P;
-          const float val = p.alpha * v[j];
-          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        {
+          const int col0 = nt * p.BN + c0;
+          store_row32(p, p.out + obase + std::int64_t(col0) * p.P, min(32, min(p.BN - c0, p.Nout - col0)),
+                      std::int64_t(p.P), v);
         }
       }
       tc_fence_before();
@@ -516,13 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NCHW -> N(HW)Cp, zero-filling channels C..Cp-1 (32 x 32 smem transpose).
-__global__ void to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int HW, int Cp) {
+// img: elements between images of src (C * HW, or more for a channel slice)
+__global__ void to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int HW, int Cp,
+                               std::int64_t img) {
   pdl_wait();
   pdl_trigger();
   __shared__ float tile[32][33];
   const int n = blockIdx.z;
   const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-  const float* s = src + std::int64_t(n) * C * HW;
+  const float* s = src + std::int64_t(n) * img;
   float* d = dst + std::int64_t(n) * HW * Cp;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, pp = p0 + threadIdx.x;
@@ -575,9 +596,11 @@ struct PhaseFilter {
   int C, R, S, sh, sw, Tw;
   int bw = 0;  // stride-phase BD: phases kept along w (decode divisor of the column index)
 };
+// ldi: input-channel pitch of w in Forward (flip 0) mode (I, or the full C
+// for a channel slice)
 __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restrict__ out, int O, int I, int taps,
                                    int BN, int n_tiles, int ksteps, int small_c, int c_chunks, int flip,
-                                   PhaseFilter pf, int swz) {
+                                   PhaseFilter pf, int swz, int ldi) {
   pdl_wait();
   pdl_trigger();
   const std::int64_t total = std::int64_t(n_tiles) * ksteps * 8 * BN;  // 16-byte units
@@ -619,7 +642,7 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
           if (r < pf.R && q < pf.S) x = w[((std::int64_t(ch) * pf.C + c) * pf.R + r) * pf.S + q];
         } else {
           x = flip ? w[(std::int64_t(ch) * O + o) * taps + (taps - 1 - tap)]
-                   : w[(std::int64_t(o) * I + ch) * taps + tap];
+                   : w[(std::int64_t(o) * ldi + ch) * taps + tap];
         }
       }
       v[e] = x;
@@ -874,13 +897,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = int(nt) * p.BN + c0 + j;
-          if (c0 + j >= p.BN || col >= p.Nout) break;
-          float* dst = p.out + obase + std::int64_t(col) * p.P;
-          const float val = p.alpha * v[j];
-          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        {
+          const int col0 = int(nt) * p.BN + c0;
+          store_row32(p, p.out + obase + std::int64_t(col0) * p.P, min(32, min(p.BN - c0, p.Nout - col0)),
+                      std::int64_t(p.P), v);
         }
       }
       tc_fence_before();
@@ -1050,7 +1070,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
-                   ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, 1);
+                   ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, 1, g.Cin);
     if (e != cudaSuccess) return e;
   }
 
@@ -1118,9 +1138,11 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
                     std::size_t(std::max(smem, 116 * 1024)), st, xmap, p);
 }
 
+// act_img / w_ldi: image pitch of act and Forward input-channel pitch of w
+// when the call covers a slice of the reduction channels (0: dense)
 cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, float* out, void* ws, float alpha,
-                    float beta, cudaStream_t st, int flags) {
-  {
+                    float beta, cudaStream_t st, int flags, std::int64_t act_img = 0, int w_ldi = 0) {
+  if (!act_img) {
     int ks = 0, bn = 0;
     geo_ws(g, &ks, &bn);
     const StripGeo sg = strip_geo(g, bn);
@@ -1150,14 +1172,15 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
                    act_nhwc, d);
   } else {
     e = launch_pdl(to_nhwc_kernel, dim3((HW + 31) / 32, (Cp + 31) / 32, g.N), dim3(32, 8), 0, st, act, act_nhwc,
-                   g.Cin, HW, Cp);
+                   g.Cin, HW, Cp, act_img ? act_img : std::int64_t(g.Cin) * HW);
   }
   if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
     const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
     const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
     e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
-                   ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, two_sm ? 0 : 1);
+                   ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, two_sm ? 0 : 1,
+                   w_ldi ? w_ldi : g.Cin);
     if (e != cudaSuccess) return e;
   }
 
@@ -1367,6 +1390,79 @@ std::int64_t precomp_workspace(int op, const ConvShape& s) {
   if (op == kFwd) return std::int64_t(geo_ws(f_geo(s)));
   if (op == kBwdData) return std::int64_t(geo_ws(bd_geo(s)));
   return bf_workspace(s);
+}
+
+// ---------------------------------------------------------------- channel-sliced
+// UCUDNN_ALGO_PRECOMP_SLICED (Forward / BackwardData): the same implicit
+// GEMM run over slices of the reduction channels (C for Forward, K for
+// BackwardData), each accumulating into the output (beta = 1 after the
+// first), so the channels-last operand copy -- the whole of PRECOMP's
+// workspace apart from the packed filter -- is per slice, at most
+// kSliceCap. Under a 64 MiB limit that lets one call cover 256 images where
+// PRECOMP has to be micro-batched (AlexNet conv2 BackwardData: 143 MB copy).
+namespace {
+// copy cap per slice (UCUDNN_TUNE=slice_cap_kib overrides, for tests)
+std::size_t slice_cap() { return std::size_t(tune("slice_cap_kib", 40 * 1024)) << 10; }
+struct Sliced {
+  Geo g;       // geometry of one slice (Cin = slice channels)
+  int flip = 0, ctot = 0, cs = 0, n = 0;  // reduction channels, per slice, slices
+  bool ok = false;
+};
+Sliced sliced_geo(int op, const ConvShape& s) {
+  Sliced r;
+  if (op == kFwd) {
+    if (use_s2d(s)) return r;
+    r.g = fwd_geo(s);
+  } else if (op == kBwdData) {
+    r.g = bd_geo(s);
+    r.flip = 1;
+  } else {
+    return r;
+  }
+  r.ctot = r.g.Cin;
+  const std::size_t act = std::size_t(r.g.N) * r.g.Hin * r.g.Win * cpad(r.ctot) * 4;
+  const std::size_t cap = slice_cap();
+  r.n = int((act + cap - 1) / cap);
+  if (r.n < 2 || r.ctot < 64) return r;  // nothing to gain over PRECOMP
+  r.cs = (r.ctot + r.n - 1) / r.n;
+  r.cs = (r.cs + 31) / 32 * 32;
+  r.n = (r.ctot + r.cs - 1) / r.cs;
+  if (r.n < 2) return r;
+  r.g.Cin = r.cs;
+  int ks = 0, bn = 0;
+  geo_ws(r.g, &ks, &bn);
+  if (strip_geo(r.g, bn).ok) return r;  // the strip path has no slice support
+  r.ok = true;
+  return r;
+}
+}  // namespace
+
+bool precomp_sliced_supports(int op, const ConvShape& s) { return precomp_supports(op, s) && sliced_geo(op, s).ok; }
+
+std::int64_t precomp_sliced_workspace(int op, const ConvShape& s) {
+  const Sliced r = sliced_geo(op, s);
+  return r.ok ? std::int64_t(geo_ws(r.g)) : 0;
+}
+
+cudaError_t precomp_sliced_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
+                               float alpha, float beta, cudaStream_t st) {
+  const Sliced r = sliced_geo(op, s);
+  if (!r.ok) return cudaErrorInvalidValue;
+  const std::int64_t hw = std::int64_t(r.g.Hin) * r.g.Win;
+  const int taps = r.g.R * r.g.S;
+  for (int i = 0; i < r.n; ++i) {
+    const int c0 = i * r.cs;
+    Geo g = r.g;
+    g.Cin = std::min(r.cs, r.ctot - c0);
+    if (g.Cin <= 0) break;
+    // Forward: w[k][c0 + c] (pitch C); BackwardData: w[k0 + k] is contiguous
+    // (stride-1: [K][C][R][S] rows; phase: the same rows, decoded by pf)
+    const float* w = op == kFwd ? b + std::int64_t(c0) * taps : b + std::int64_t(c0) * s.C * s.R * s.S;
+    cudaError_t e = run_geo(g, a + c0 * hw, w, op == kFwd ? 0 : 1, out, ws, alpha,
+                            i == 0 ? beta : 1.f, st, 0, std::int64_t(r.ctot) * hw, op == kFwd ? r.ctot : 0);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,

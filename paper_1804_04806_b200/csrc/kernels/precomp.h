@@ -14,6 +14,13 @@ std::int64_t precomp_workspace(int op, const ConvShape& s);
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
                         float alpha, float beta, cudaStream_t stream, int flags);
 
+// UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_SLICED (Forward / BackwardData): the same
+// kernels over slices of the reduction channels, bounded operand copy
+bool precomp_sliced_supports(int op, const ConvShape& s);
+std::int64_t precomp_sliced_workspace(int op, const ConvShape& s);
+cudaError_t precomp_sliced_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
+                               float alpha, float beta, cudaStream_t stream);
+
 void precomp_profile(double out[4]);
 
 }  // namespace ucudnn

@@ -29,7 +29,7 @@ SHAPES = [
     ConvShape(2, 64, 14, 14, 32, 1, 1, 0, 0, 1, 1),       # 1x1 stride 1: BF reads x / dy in place
     ConvShape(3, 32, 7, 7, 160, 1, 1, 0, 0, 1, 1),        # 1x1 stride 1, 49-pixel planes (re-laid)
 ]
-ALGOS = [0, 1, 2, 3, 4, 5, 6]
+ALGOS = [0, 1, 2, 3, 4, 5, 6, 7]
 # F(4x4,3x3) carries 1/6 and 1/24 in G: not exact in TF32 even on integer data,
 # and its transforms amplify TF32 rounding (measured ~3.3e-3 normwise on
 # Gaussian data), so it gets a 1e-2 bound instead of the GEMM-class 3e-3.
@@ -112,5 +112,20 @@ def test_experimental_bd_scatter(cuda, spec):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, UCUDNN_TUNE="bds=1")
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *spec.split(), "1", "6"],
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert "exact True" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("spec", ["3 64 13 13 96 3 3 1 1 0", "3 64 13 13 96 3 3 1 1 1", "2 96 28 28 64 3 3 1 2 1",
+                                  "2 128 28 28 64 1 1 0 2 1", "2 96 27 27 64 5 5 2 1 0"])
+def test_precomp_sliced(cuda, spec):
+    """IMPLICIT_PRECOMP_GEMM_SLICED (algorithm 7) splits the reduction channels
+    once the channels-last copy passes a cap; a 64 KiB cap (read once per
+    process, so in a child) forces 2-3 slices on these small shapes."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, UCUDNN_TUNE="slice_cap_kib=64")
+    v = spec.split()
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *v[:9], v[9], "7"],
                          env=env, capture_output=True, text=True, timeout=300)
     assert "exact True" in out.stdout, out.stdout + out.stderr

@@ -22,14 +22,16 @@
 // The store pattern is the SWIZZLE_128B K-major UMMA layout: row q at
 // q*128 B, 16-byte chunk (lane/4) ^ (q%8).
 //
-// GEMM rows of x are ordered (r, s, c) so that 8-row groups share one tap:
+// GEMM rows of x are ordered (r, s, c) so that 8-row groups share one tap
+// (C % 8 == 0; fewer channels use a per-row (offset, tap) table):
 // the bounds test and base offset are computed once per tap run, and each
 // row is one cp.async plus a pointer step. Roles as in bfilter.cu: K <= 128
 // output channels -> MMA rows = k (one 128-row tile of dy), columns = x rows.
 //
-// Persistent, one CTA per SM, 416 threads: warps 0-3 epilogue (TMEM ->
-// fp32 RED into the scratch), warp 4 TMEM owner + MMA issuer, warps 5-12
-// producers. A producer never waits for its own gathers: each thread's
+// Persistent, one CTA per SM, 544 threads: warps 0-3 epilogue (TMEM ->
+// fp32 RED into the scratch), warp 4 TMEM owner + MMA issuer, warps 5-16
+// producers (12: the gathers are latency-bound, more warps keep more rows
+// in flight). CTA pairs (K > 128): bfl2_kernel below. A producer never waits for its own gathers: each thread's
 // cp.async.mbarrier.arrive fires when its copies land, and the MMA thread
 // issues the generic->async proxy fence after observing the full barrier.
 #include <cuda_runtime.h>
@@ -103,8 +105,9 @@ struct LParams {
   long long npx, CHW, KOHW;
   int swap, BN, m_tiles, tiles, splits, steps, steps_per_unit, stages, rpad;
   int dbg;  // diagnostic (UCUDNN_TUNE=bfl_dbg): 1 skip the gathers, 2 skip the MMAs
-  FastDiv fd_ohw, fd_ow, fd_C, fd_S, fd_RS;
+  FastDiv fd_ohw, fd_ow, fd_C, fd_S, fd_RS, fd_sgs;
   int crs;  // x row order: 1 (c, r, s) = dW order, 0 (r, s, c)
+  int sg, ngroups, sgs;  // strided few-channel gather: groups of sw taps, count, ceil(S / sw)
 };
 
 // 4-byte gather; src_size 0 writes a zero (src is then never dereferenced)
@@ -148,13 +151,14 @@ struct Gatherer {
   const LParams& p;
   int lane, pw;
   bool c8;                 // C % 8 == 0: an 8-row group is 8 channels of one tap
+  bool sg;                 // stride 2 / 4 with few channels: lane = (pixel, tap offset s')
   std::uint32_t swz[8];    // this lane's byte offset in an 8-row swizzle atom, per row q % 8
   std::uint32_t xj[8], dj[8];  // byte offsets of rows j of a group (independent adds)
   int2* xtab;
   int xm0, xrows, dk0, drows;  // current unit: x rows [xm0, +xrows), dy rows [dk0, +drows)
 
   __device__ __forceinline__ Gatherer(const LParams& p_, int lane_, int pw_, int2* tab)
-      : p(p_), lane(lane_), pw(pw_), c8(!p_.crs && p_.C % 8 == 0), xtab(tab) {
+      : p(p_), lane(lane_), pw(pw_), c8(!p_.crs && p_.C % 8 == 0), sg(p_.sg != 0), xtab(tab) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
@@ -168,7 +172,18 @@ struct Gatherer {
     xrows = xrows_;
     dk0 = dk0_;
     drows = drows_;
-    if (!c8) {
+    if (sg) {
+      // this warp's tap groups (r, s0 = sgrp*sw, c): (c*HW + r*W + s0, r << 16 | s0 << 8 | c)
+      // (built by the warp that reads it: gi = pw (mod kProd))
+      for (int gi = pw + kProd * lane; gi < p.ngroups; gi += kProd * 32) {
+        std::uint32_t rg, c, r, sgrp;
+        p.fd_C.divmod(std::uint32_t(gi), rg, c);
+        p.fd_sgs.divmod(rg, r, sgrp);
+        const int s0 = int(sgrp) * p.sw;
+        xtab[gi] = make_int2(int(c) * p.HW + int(r) * p.W + s0, int(r << 16 | s0 << 8 | c));
+      }
+      __syncwarp();
+    } else if (!c8) {
       // this warp's rows of the tile: (c*HW + r*W + s, r << 8 | s)
       // (few channels, or (c, r, s) order)
       for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8)
@@ -186,6 +201,49 @@ struct Gatherer {
     }
   }
 
+  // Stride-2 / 4 x rows with few channels: row (r, s, c) of a 32-pixel step
+  // reads x at stride sw along the pixels, i.e. 32 lanes would span 32*sw
+  // floats. Instead lane = (pixel j, tap offset s' < sw): one cp.async covers
+  // the sw taps s0 + s' of 32/sw consecutive pixels -- 32 *consecutive* x
+  // floats -- and a group (r, s0, c) takes sw instructions (pixel subsets u).
+  __device__ __forceinline__ void step_strided(int g, std::uint32_t xs) const {
+    const int sw = p.sw, per = 32 / sw, sp = lane % sw, jl = lane / sw;
+    const float* xl[4];
+    int ihb[4], iwb[4];
+    bool val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u < sw) {
+        const long long pg = (long long)g * 32 + u * per + jl;
+        val[u] = pg < p.npx;
+        std::uint32_t n, pix, oh, ow;
+        p.fd_ohw.divmod(std::uint32_t(val[u] ? pg : 0), n, pix);
+        p.fd_ow.divmod(pix, oh, ow);
+        ihb[u] = int(oh) * p.sh - p.ph;
+        iwb[u] = int(ow) * p.sw - p.pw;
+        xl[u] = p.x + (long long)n * p.CHW + (long long)ihb[u] * p.W + iwb[u] + sp;
+      }
+    }
+    for (int gi = pw; gi < p.ngroups; gi += kProd) {
+      const int2 e = xtab[gi];
+      const int r = e.y >> 16, s0 = (e.y >> 8) & 255, c = e.y & 255;
+      const int s = s0 + sp;
+      const int q = (r * p.S + s) * p.C + c - xm0;  // this lane's tile row
+      const bool in = s < p.S && unsigned(q) < unsigned(xrows);
+      if (!__any_sync(0xffffffffu, in)) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u < sw) {
+          const int kk = u * per + jl;
+          const bool ok = val[u] && unsigned(ihb[u] + r) < unsigned(p.H) && unsigned(iwb[u] + s) < unsigned(p.W);
+          const std::uint32_t dst =
+              xs + std::uint32_t(q) * 128 + ((std::uint32_t(kk >> 2) ^ (q & 7)) << 4) + (kk & 3) * 4;
+          if (in) cp_async4a(dst, reinterpret_cast<std::uint64_t>(xl[u] + e.x), ok ? 4u : 0u);
+        }
+      }
+    }
+  }
+
   // x rows -> smem at xs, dy rows -> smem at ds (SW128 K-major, row q at q*128)
   __device__ __forceinline__ void step(int g, std::uint32_t xs, std::uint32_t ds) const {
     const long long pg = (long long)g * 32 + lane;  // this lane's pixel
@@ -195,7 +253,9 @@ struct Gatherer {
     p.fd_ow.divmod(pix, oh, ow);
     const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
     const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
-    if (c8) {
+    if (sg) {
+      step_strided(g, xs);
+    } else if (c8) {
       // one bounds test per group, then consecutive channel planes
       for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
         std::uint32_t rs, c, r, s;
@@ -625,6 +685,12 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   // L2 throughput halved), but every row needs the table path and AlexNet
   // conv2 at 256 images measured 503 -> 787 us, so (r, s, c) stays
   p.crs = tune("bfl_crs", 0);
+  // strided few-channel x gather (AlexNet / ResNet conv1)
+  p.sgs = (g.S + g.sw - 1) / g.sw;
+  p.ngroups = g.R * p.sgs * g.C;
+  p.sg = !p.crs && g.C % 8 != 0 && (g.sw == 2 || g.sw == 4) && g.C < 256 && p.ngroups <= kMaxBN &&
+         tune("bfl_sg", 0);  // exact, but issue-bound: AlexNet conv1 BF 542 -> 876 us, ResNet conv1 1031 -> 1601
+  p.fd_sgs = FastDiv(std::uint32_t(p.sgs));
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));

@@ -6,9 +6,9 @@ rm -f gpurun_out/db.csv
 timeout 900 python bench.py --db gpurun_out/db.csv > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --db gpurun_out/db.csv > gpurun_out/ncu_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:bfl -s 1 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bfl2?_kernel" -s 1 -c 1 \
   -o gpurun_out/gather_conv2_bf python scripts/one_conv.py --layer a2 --op 2 --algo 6 --batch 256 --reps 2 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:bfl -s 1 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bfl2?_kernel" -s 1 -c 1 \
   -o gpurun_out/gather_conv1_bf python scripts/one_conv.py --layer a1 --op 2 --algo 6 --batch 256 --reps 2 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:precomp -s 1 -c 1 \
   -o gpurun_out/precomp_conv2_bd python scripts/one_conv.py --layer a2 --op 1 --algo 5 --batch 64 --reps 2 > /dev/null 2>&1

@@ -60,6 +60,7 @@ struct LGeo {
   int M;  // C*R*S GEMM rows of x
   int swap, BN, m_tiles, n_tiles;
   int two;        // CTA pairs (cta_group::2): m_tiles counts 256-row pair tiles
+  int dual;       // pairs with two pair tiles per unit: m_tiles counts 512-row tiles
   long long npx;  // N*OH*OW
   int steps;      // 32-pixel chunks
 };
@@ -86,14 +87,16 @@ LGeo make_lgeo(const ConvShape& s) {
     g.m_tiles = (g.M + kBM - 1) / kBM;
     // pairs: each CTA gathers its own 128 x rows and half of the dy rows
     g.two = tune("bfl2", 1) && g.m_tiles >= 2;
-    if (g.two) g.m_tiles = (g.M + 2 * kBM - 1) / (2 * kBM);
+    // one dy gather for 512 x rows (TMEM: 2 x BN <= 512 columns, C % 8 == 0 path)
+    g.dual = g.two && s.C % 8 == 0 && g.m_tiles >= 4 && tune("bfl_dual", 1);
+    if (g.two) g.m_tiles = (g.M + (g.dual ? 4 : 2) * kBM - 1) / ((g.dual ? 4 : 2) * kBM);
   }
   return g;
 }
 
 // RED scratch in the GEMM's own layout: non-swap [k][x row] (pitch rows_pad),
 // swap [x row][k] (pitch 128); 32 lanes reduce into 32 consecutive floats.
-int rows_pad(const LGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM * (g.two ? 2 : 1); }
+int rows_pad(const LGeo& g) { return g.swap ? g.n_tiles * g.BN : g.m_tiles * kBM * (g.dual ? 4 : g.two ? 2 : 1); }
 int cols_pad(const LGeo& g) { return g.swap ? kBM : g.n_tiles * g.BN; }
 std::size_t scratch_bytes(const LGeo& g) { return (std::size_t(rows_pad(g)) * cols_pad(g) * 4 + 255) / 256 * 256; }
 
@@ -107,7 +110,8 @@ struct LParams {
   int dbg;  // diagnostic (UCUDNN_TUNE=bfl_dbg): 1 skip the gathers, 2 skip the MMAs
   FastDiv fd_ohw, fd_ow, fd_C, fd_S, fd_RS, fd_sgs;
   int crs;  // x row order: 1 (c, r, s) = dW order, 0 (r, s, c)
-  int sg, ngroups, sgs;  // strided few-channel gather: groups of sw taps, count, ceil(S / sw)
+  int sg, ngroups, sgs;
+  int dual;  // CTA-pair kernel: two pair tiles per unit  // strided few-channel gather: groups of sw taps, count, ceil(S / sw)
 };
 
 // 4-byte gather; src_size 0 writes a zero (src is then never dereferenced)
@@ -245,7 +249,10 @@ struct Gatherer {
   }
 
   // x rows -> smem at xs, dy rows -> smem at ds (SW128 K-major, row q at q*128)
-  __device__ __forceinline__ void step(int g, std::uint32_t xs, std::uint32_t ds) const {
+  // xs2 != 0 (CTA-pair kernel, C % 8 == 0): a second x tile, rows
+  // [xm0 + 256, + xrows2), into xs2 -- the dy rows are gathered once for both
+  __device__ __forceinline__ void step(int g, std::uint32_t xs, std::uint32_t ds, std::uint32_t xs2 = 0,
+                                       int xrows2 = 0) const {
     const long long pg = (long long)g * 32 + lane;  // this lane's pixel
     const bool valid = pg < p.npx;
     std::uint32_t n, pix, oh, ow;
@@ -257,17 +264,21 @@ struct Gatherer {
       step_strided(g, xs);
     } else if (c8) {
       // one bounds test per group, then consecutive channel planes
-      for (int q0 = pw * 8; q0 < xrows; q0 += kProd * 8) {
-        std::uint32_t rs, c, r, s;
-        p.fd_C.divmod(std::uint32_t(xm0 + q0), rs, c);
-        p.fd_S.divmod(rs, r, s);
-        const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
-        const std::uint32_t sz = ok ? 4u : 0u, dst = xs + q0 * 128;
-        const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
-        const int qn = min(8, xrows - q0);
+      for (int t = 0; t < (xs2 ? 2 : 1); ++t) {
+        const int m0 = xm0 + t * 256, rows = t ? xrows2 : xrows;
+        const std::uint32_t base = t ? xs2 : xs;
+        for (int q0 = pw * 8; q0 < rows; q0 += kProd * 8) {
+          std::uint32_t rs, c, r, s;
+          p.fd_C.divmod(std::uint32_t(m0 + q0), rs, c);
+          p.fd_S.divmod(rs, r, s);
+          const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
+          const std::uint32_t sz = ok ? 4u : 0u, dst = base + q0 * 128;
+          const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
+          const int qn = min(8, rows - q0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < qn) cp_async4a(dst + swz[j], a + xj[j], sz);
+          for (int j = 0; j < 8; ++j)
+            if (j < qn) cp_async4a(dst + swz[j], a + xj[j], sz);
+        }
       }
     } else {
       // few channels (taps straddle groups): per-row (offset, tap) from the
@@ -464,7 +475,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
   const std::uint32_t rank = cluster_rank();
   const int bh = p.BN / 2;
   const std::uint32_t a_bytes = kBM * 128;
-  const std::uint32_t stage_bytes = a_bytes + ((std::uint32_t(bh) * 128 + 1023) & ~1023u);
+  // dual: two 256-row pair tiles per unit (acc 0 / 1 at TMEM columns 0 / 256)
+  // sharing one dy gather; the accumulators then fill TMEM, so units are
+  // not double-buffered
+  const int nsub = p.dual ? 2 : 1;
+  const std::uint32_t stage_bytes = nsub * a_bytes + ((std::uint32_t(bh) * 128 + 1023) & ~1023u);
   const int kStages = p.stages;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
   std::uint64_t* empty = full + kMaxStages;
@@ -503,12 +518,16 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
       const int tile = u % p.tiles, split = u / p.tiles;
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-      const int xm0 = mt * 2 * kBM + int(rank) * kBM, dk0 = nt * p.BN + int(rank) * bh;
+      const int xm0 = mt * 2 * nsub * kBM + int(rank) * kBM, dk0 = nt * p.BN + int(rank) * bh;
       ga.unit(xm0, min(kBM, p.M - xm0), dk0, min(bh, p.K - dk0));
+      const int xrows2 = min(kBM, p.M - xm0 - 2 * kBM);
       for (int g = g0; g < g1; ++g) {
         mbar_wait(&empty[st], ph ^ 1);
         const std::uint32_t sst = sbase + st * stage_bytes;
-        if (p.dbg != 1) ga.step(g, sst, sst + a_bytes);
+        if (p.dbg != 1) {
+          if (p.dual) ga.step(g, sst, sst + 2 * a_bytes, sst + a_bytes, xrows2);
+          else ga.step(g, sst, sst + a_bytes);
+        }
         cp_async_arrive(&full[st]);
         if (++st == kStages) {
           st = 0;
@@ -525,8 +544,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
       for (int u = cid; u < units; u += ncl, ++tl) {
         const int split = u / p.tiles;
         const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-        const int acc = tl & 1;
-        mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        const int acc = p.dual ? 0 : (tl & 1);
+        const std::uint32_t tpar = p.dual ? ((tl & 1) ^ 1) : (((tl >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[acc], tpar);
         tc_fence_after();
         const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
         for (int g = g0; g < g1; ++g, ++it) {
@@ -535,12 +555,13 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
           tc_fence_after();
           if (lane == 0) {
             fence_async_smem();
-            const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+            const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + nsub * a_bytes;
             if (p.dbg != 2)
+              for (int t = 0; t < nsub; ++t)
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                mma_tf32_2sm(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
-                             (g != g0 || q != 0) ? 1u : 0u);
+                for (int q = 0; q < 4; ++q)
+                  mma_tf32_2sm(dtm + std::uint32_t(t * kMaxBN), umma_desc_sw128(sa + t * a_bytes + q * 32),
+                               umma_desc_sw128(sb + q * 32), idesc, (g != g0 || q != 0) ? 1u : 0u);
             mma_commit_2sm(&empty[st], 3);
             if (g + 1 >= g1) mma_commit_2sm(&tfull[acc], 3);
           }
@@ -574,21 +595,24 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
       const int tile = u % p.tiles, split = u / p.tiles;
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-      const int acc = tl & 1;
-      mbar_wait_backoff(&tfull[acc], (tl >> 1) & 1);
+      const int acc = p.dual ? 0 : (tl & 1);
+      mbar_wait_backoff(&tfull[acc], p.dual ? (tl & 1) : ((tl >> 1) & 1));
       tc_fence_after();
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
-      const int m = mt * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
-      const bool live = m < p.M && g1 > g0;
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tbase + std::uint32_t(c0), v);
-        if (!live) continue;
+      for (int t = 0; t < nsub; ++t) {
+        const std::uint32_t tbase =
+            tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t((acc + t) * kMaxBN);
+        const int m = mt * 2 * nsub * kBM + t * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
+        const bool live = m < p.M && g1 > g0;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int k = nt * p.BN + c0 + j;
-          if (c0 + j >= p.BN || k >= p.K) break;
-          red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+          for (int j = 0; j < 32; ++j) {
+            const int k = nt * p.BN + c0 + j;
+            if (c0 + j >= p.BN || k >= p.K) break;
+            red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+          }
         }
       }
       tc_fence_before();
@@ -685,6 +709,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   // L2 throughput halved), but every row needs the table path and AlexNet
   // conv2 at 256 images measured 503 -> 787 us, so (r, s, c) stays
   p.crs = tune("bfl_crs", 0);
+  p.dual = g.dual;
   // strided few-channel x gather (AlexNet / ResNet conv1)
   p.sgs = (g.S + g.sw - 1) / g.sw;
   p.ngroups = g.R * p.sgs * g.C;
@@ -696,7 +721,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
-  const int stage_bytes = kBM * 128 + (((g.two ? g.BN / 2 : g.BN) * 128 + 1023) & ~1023);
+  const int stage_bytes = (g.dual ? 2 : 1) * kBM * 128 + (((g.two ? g.BN / 2 : g.BN) * 128 + 1023) & ~1023);
   p.stages = std::max(2, std::min({kMaxStages, tune("bfl_stages", 4), (200 * 1024) / stage_bytes}));
   // 4 stages: the rest of the 228 KB stays L1, which catches the taps' re-reads
   // of x (AlexNet conv3-5 at 256 images: 8 stages 282/312/208 us, 4 stages

@@ -664,15 +664,11 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
                                    PhaseFilter pf, int swz, int ldi) {
   pdl_wait();
   pdl_trigger();
-  const std::int64_t total = std::int64_t(n_tiles) * ksteps * 8 * BN;  // 16-byte units
-  for (std::int64_t u = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; u < total;
-       u += std::int64_t(gridDim.x) * blockDim.x) {
-    const int row = int(u % BN);
-    std::int64_t rest = u / BN;
-    const int g = int(rest % 8);
-    rest /= 8;
-    const int k = int(rest % ksteps);
-    const int nt = int(rest / ksteps);
+  // one block per (column tile, k-step): BN rows x 8 16-byte chunks
+  const int nt = blockIdx.x / ksteps, k = blockIdx.x - nt * ksteps;
+  for (int idx = threadIdx.x; idx < 8 * BN; idx += blockDim.x) {
+    const int row = idx >> 3, g = idx & 7;  // a row's 8 chunks from 8 adjacent threads: 128 B stores
+    const std::int64_t u = (std::int64_t(blockIdx.x) * 8 + g) * BN + row;
     const int o = nt * BN + row;
     float v[4];
 #pragma unroll
@@ -1127,9 +1123,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   }
   if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
-    const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
-    const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
-    e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
+    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
+                   n_tiles,
                    ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, 1, g.Cin);
     if (e != cudaSuccess) return e;
   }
@@ -1235,9 +1230,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   }
   if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
-    const std::int64_t units = std::int64_t(n_tiles) * ksteps * 8 * BN;
-    const int blocks = int(std::min<std::int64_t>((units + 255) / 256, 8 * sm_count()));
-    e = launch_pdl(pack_filter_kernel, dim3(blocks), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN, n_tiles,
+    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
+                   n_tiles,
                    ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, two_sm ? 0 : 1,
                    w_ldi ? w_ldi : g.Cin);
     if (e != cudaSuccess) return e;

@@ -65,6 +65,8 @@ struct PrecompParams {
   // output pixel (n, i, j) is dx[n][c][i*ssh + a - sph][j*ssw + b - spw]
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
   int pair;      // 1x1 stride-2 block stores (phase_store)
+  int bp;        // blocked phase BD: phase-grid columns per GEMM row (column = (pb, a, b, c))
+  FastDiv fd_blk;  // Ah * Bw * C
   int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
   int stages, ksub, prof, cps;
   FastDiv fd_Cr, fd_ssw;
@@ -106,6 +108,12 @@ __device__ __forceinline__ void phase_store(const P& p, std::int64_t obase, int 
       *d1 = make_float2(p.beta * o1.x, p.beta * o1.y);
     }
     return;
+  }
+  if (p.bp > 1) {  // blocked: column (pb, a, b, c) belongs to phase-grid column j + pb
+    std::uint32_t pb, rem;
+    p.fd_blk.divmod(std::uint32_t(col), pb, rem);
+    col = int(rem);
+    wb += int(pb) * p.ssw;
   }
   std::uint32_t ab, c, a, b;
   p.fd_Cr.divmod(std::uint32_t(col), ab, c);
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.fd_OW.divmod(pix, i, j);
           obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
           hb = int(i) * p.ssh - p.sph;
-          wb = int(j) * p.ssw - p.spw;
+          wb = int(j) * p.bp * p.ssw - p.spw;
         }
       }
       const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc) * acc_cols;
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.fd_OW.divmod(pix, i, j);
           obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
           hb = int(i) * p.ssh - p.sph;
-          wb = int(j) * p.ssw - p.spw;
+          wb = int(j) * p.bp * p.ssw - p.spw;
         }
       }
       const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
@@ -656,6 +664,7 @@ cudaError_t launch_s2d(const float* x, float* out, const S2D& d, int N, cudaStre
 struct PhaseFilter {
   int C, R, S, sh, sw, Tw;
   int bw = 0;  // stride-phase BD: phases kept along w (decode divisor of the column index)
+  int P = 1;   // stride-phase BD blocked along w: P phase-grid columns per GEMM row
 };
 // ldi: input-channel pitch of w in Forward (flip 0) mode (I, or the full C
 // for a channel slice)
@@ -693,10 +702,15 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
           const int r = t * pf.sh + a, q = u * pf.sw + b;
           if (a < pf.sh && r < pf.R && q < pf.S) x = w[((std::int64_t(o) * pf.C + c) * pf.R + r) * pf.S + q];
         } else if (flip == 2) {
-          const int ab = o / pf.C, c = o - ab * pf.C, a = ab / pf.bw, b = ab - a * pf.bw;
-          const int t = tap / pf.Tw, u = tap - t * pf.Tw, Th = taps / pf.Tw;
+          // column (pb, a, b, c), tap (t, u') of a Th x (Tw + P - 1) window:
+          // phase-grid column pb of the block uses sub-filter tap u = u' - pb
+          const int Twb = pf.Tw + pf.P - 1, nab = (o / pf.C) , Ah = min(pf.sh, pf.R);
+          const int pb = nab / (Ah * pf.bw), ab = nab - pb * (Ah * pf.bw), c = o - nab * pf.C;
+          const int a = ab / pf.bw, b = ab - a * pf.bw;
+          const int t = tap / Twb, u = tap - t * Twb - pb, Th = taps / Twb;
           const int r = a + (Th - 1 - t) * pf.sh, q = b + (pf.Tw - 1 - u) * pf.sw;
-          if (r < pf.R && q < pf.S) x = w[((std::int64_t(ch) * pf.C + c) * pf.R + r) * pf.S + q];
+          if (u >= 0 && u < pf.Tw && r < pf.R && q < pf.S)
+            x = w[((std::int64_t(ch) * pf.C + c) * pf.R + r) * pf.S + q];
         } else {
           x = flip ? w[(std::int64_t(ch) * O + o) * taps + (taps - 1 - tap)]
                    : w[(std::int64_t(o) * ldi + ch) * taps + tap];
@@ -742,7 +756,8 @@ struct StripParams {
   int OH, OW, Nout, P;
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
-  int sAh, sBw, pair;
+  int sAh, sBw, pair, bp;
+  FastDiv fd_blk;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
 };
@@ -911,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             } else {
               const std::int64_t obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
-              const int hb = int(oh) * p.ssh - p.sph, wb = int(ow) * p.ssw - p.spw;
+              const int hb = int(oh) * p.ssh - p.sph, wb = int(ow) * p.bp * p.ssw - p.spw;
               for (int r = 0; r < 32; ++r) {
                 const int col = ew * 32 + r;
                 if (col >= p.Nout) break;
@@ -935,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.phase) {
           obase = std::int64_t(n) * p.Cr * p.Hr * p.Wr;
           hb = int(oh) * p.ssh - p.sph;
-          wb = int(ow) * p.ssw - p.spw;
+          wb = int(ow) * p.bp * p.ssw - p.spw;
         } else {
           obase = std::int64_t(n) * p.Nout * p.P + int(oh) * p.OW + int(ow);
         }
@@ -1180,6 +1195,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.sAh = std::min(g.pf.sh, g.pf.R);
     p.sBw = g.pf.bw;
     p.pair = phase_pair(g);
+    p.bp = g.pf.P;
+    p.fd_blk = FastDiv(std::uint32_t(p.sAh * g.pf.bw * g.pf.C));
   }
   const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
@@ -1294,6 +1311,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.sAh = std::min(g.pf.sh, g.pf.R);
     p.sBw = g.pf.bw;
     p.pair = phase_pair(g);
+    p.bp = g.pf.P;
+    p.fd_blk = FastDiv(std::uint32_t(p.sAh * g.pf.bw * g.pf.C));
   }
   if (two_sm) {
     CUtensorMap bmap;
@@ -1398,11 +1417,31 @@ Geo bwd_data_phase_geo(const ConvShape& s) {
   const int Wq = std::max(OW + Tw - 1, (s.W - 1 + s.pw) / s.sw + 1);
   // only the phases that own filter taps become GEMM columns
   const int Ah = std::min(s.sh, s.R), Bw = std::min(s.sw, s.S);
-  Geo g{s.N, s.K, OH, OW, Ah * Bw * s.C, Hq, Wq, Th, Tw, Th - 1, Tw - 1, 1, 1};
+  // Few phase-channels (ResNet conv1: 12): block P phase-grid columns into
+  // one GEMM row -- a stride-P conv of dy with a Th x (Tw + P - 1) banded
+  // filter and P x as many columns -- so each MMA does P x the work and dy
+  // is re-read (Tw + P - 1) / P instead of Tw times per output column.
+  // P <= 8 (TMA im2col traversal stride); not with tapless phases / pair stores.
+  const int nab = Ah * Bw * s.C;
+  int P = 1;
+  if (Ah == s.sh && Bw == s.sw && !(s.R == 1 && s.S == 1)) {
+    P = tune("bd_block", -1);
+    if (P < 0) {  // widest block up to 4 keeping the columns in one <= 128-wide tile
+      // (ResNet conv1 BD at 256 images: P = 1 / 2 / 4 / 8 -> 1426 / 1074 /
+      // 908 / 1211 us; AlexNet conv1, 48 phase-channels: P = 1 is best)
+      P = 1;
+      while (P < 4 && (P + 1) * nab <= 128) ++P;
+      if (nab > 32) P = 1;
+    }
+    P = std::max(1, std::min(8, P));
+  }
+  const int Wqb = (Wq + P - 1) / P;
+  Geo g{s.N, s.K, OH, OW, P * nab, Hq, Wqb, Th, Tw + P - 1, Th - 1, Tw - 1, 1, P};
   g.ph_hi = Hq - OH;
-  g.pw_hi = Wq - OW;
+  g.pw_hi = Wqb * P - OW;
   g.phase = 1;
   g.pf = PhaseFilter{s.C, s.R, s.S, s.sh, s.sw, Tw, Bw};
+  g.pf.P = P;
   g.Hr = s.H;
   g.Wr = s.W;
   g.rph = s.ph;

@@ -1396,7 +1396,9 @@ Geo fwd_s2d_geo(const ConvShape& s) {
   g.sd = S2D{s.C, s.H, s.W, s.sh, s.sw, s.ph, s.pw, Bw, Ah * Bw * s.C, Hq, Wq, 0};
   return g;
 }
-bool use_s2d(const ConvShape& s) { return (s.sh > 1 || s.sw > 1) && (s.C < 32 || (s.R == 1 && s.S == 1)); }
+bool use_s2d(const ConvShape& s) {
+  return (s.sh > 1 || s.sw > 1) && (s.C < 32 || (s.R == 1 && s.S == 1)) && tune("s2d", 1);
+}
 Geo f_geo(const ConvShape& s) { return use_s2d(s) ? fwd_s2d_geo(s) : fwd_geo(s); }
 // stride-1 BackwardData as a forward conv of dy with the flipped filter
 Geo bwd_data_geo(const ConvShape& s) {

@@ -28,10 +28,9 @@
 // row is one cp.async plus a pointer step. Roles as in bfilter.cu: K <= 128
 // output channels -> MMA rows = k (one 128-row tile of dy), columns = x rows.
 //
-// Persistent, one CTA per SM, 544 threads: warps 0-3 epilogue (TMEM ->
-// fp32 RED into the scratch), warp 4 TMEM owner + MMA issuer, warps 5-16
-// producers (12: the gathers are latency-bound, more warps keep more rows
-// in flight). CTA pairs (K > 128): bfl2_kernel below. A producer never waits for its own gathers: each thread's
+// Persistent, one CTA per SM: warps 0-3 epilogue (TMEM -> fp32 RED into
+// the scratch), warp 4 TMEM owner + MMA issuer, warps 5.. producers (12 in
+// the 1-SM kernel, 16 in the CTA-pair kernel bfl2_kernel, K > 128). A producer never waits for its own gathers: each thread's
 // cp.async.mbarrier.arrive fires when its copies land, and the MMA thread
 // issues the generic->async proxy fence after observing the full barrier.
 #include <cuda_runtime.h>
@@ -52,8 +51,12 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kMaxBN = 256;
 constexpr int kMaxStages = 8;
-constexpr int kProd = 12;  // producer warps
-constexpr int kThreads = (5 + kProd) * 32;
+// producer warps: the gathers are latency-bound, more warps keep more rows
+// in flight; measured best 12 for the 1-SM kernel (AlexNet conv1 BF 542 us
+// vs 615 with 16) and 16 for the CTA pairs (conv2-5 4-7 % faster than 12)
+constexpr int kProd1 = 12, kProd2 = 16;
+template <int NP>
+constexpr int threads_for() { return (5 + NP) * 32; }
 
 struct LGeo {
   int N, C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
@@ -151,6 +154,7 @@ __device__ __forceinline__ std::uint32_t range_mask(int lo, int hi, int n) {
 
 // The gather side shared by both kernels: per-thread constants, the
 // per-unit row table (few-channel path) and one 32-pixel step into a stage.
+template <int kProd>
 struct Gatherer {
   const LParams& p;
   int lane, pw;
@@ -312,7 +316,8 @@ struct Gatherer {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
+__global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LParams p) {
+  constexpr int kProd = kProd1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
 
   if (warp >= 5) {
     // ------------------------------------------------ gather producers
-    Gatherer ga(p, lane, warp - 5, xtab);
+    Gatherer<kProd> ga(p, lane, warp - 5, xtab);
     const std::uint32_t sbase = smem_u32(smem);
     // x rows go to A (non-swap) or B (swap); dy rows to the other
     const std::uint32_t x_off = p.swap ? a_bytes : 0, d_off = p.swap ? 0 : a_bytes;
@@ -467,7 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfl_kernel(const LParams p) {
 // warp 4 relays its producers' completion (its own cp.async full barrier)
 // to rank 0's full barrier after the proxy fence. Commits multicast to both
 // CTAs; both epilogues release rank 0's accumulator barrier.
-__global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
+__global__ void __launch_bounds__(threads_for<kProd2>(), 1) bfl2_kernel(const LParams p) {
+  constexpr int kProd = kProd2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfl2_kernel(const LParams p) {
 
   if (warp >= 5) {
     // ------------------------------------------------ gather producers
-    Gatherer ga(p, lane, warp - 5, xtab);
+    Gatherer<kProd> ga(p, lane, warp - 5, xtab);
     const std::uint32_t sbase = smem_u32(smem);
     int st = 0;
     std::uint32_t ph = 0;
@@ -739,7 +745,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
     count_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * std::min(sms / 2, p.tiles * p.splits));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads_for<kProd2>());
     cfg.dynamicSmemBytes = std::size_t(smem);
     cfg.stream = st;
     cudaLaunchAttribute cat[1];
@@ -751,7 +757,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, bfl2_kernel, p);
   } else {
-    e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, p);
+    e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(threads_for<kProd1>()),
+                   std::size_t(smem), st, p);
   }
   if (e != cudaSuccess) return e;
   LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, p.crs, s.w_elems()};

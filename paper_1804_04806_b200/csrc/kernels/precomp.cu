@@ -619,12 +619,14 @@ __global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__
   pdl_trigger();
   extern __shared__ float rows[];  // [c][a][Wq * sw]
   const int n = blockIdx.x / d.Hq, i = blockIdx.x - n * d.Hq;
-  const int Ah = d.CC / (d.Bw * d.C), L = d.Wq * d.sw;
+  // odd row pitch: the write phase reads rows (c, a) that differ by whole
+  // rows, which would otherwise land on the same banks
+  const int Ah = d.CC / (d.Bw * d.C), L = d.Wq * d.sw, Lp = L | 1;
   // load: rows (c, a) one after another, threads along the row (no divisions)
   for (int c = 0; c < d.C; ++c)
     for (int a = 0; a < Ah; ++a) {
       const int h = i * d.sh + a - d.ph;
-      float* r = rows + (c * Ah + a) * L;
+      float* r = rows + (c * Ah + a) * Lp;
       const float* src = x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W;
       const bool hin = unsigned(h) < unsigned(d.H);
       for (int t = threadIdx.x; t < L; t += blockDim.x) {
@@ -639,13 +641,13 @@ __global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__
   int off = -1;
   if (cc < d.CC) {
     const int ab = cc / d.C, c = cc - ab * d.C, aa = ab / d.Bw, bb = ab - aa * d.Bw;
-    off = (c * Ah + aa) * L + bb;
+    off = (c * Ah + aa) * Lp + bb;
   }
   float* o = out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp + cc;
   for (int j = j0; j < d.Wq; j += js) o[std::int64_t(j) * d.Cp] = off >= 0 ? rows[off + j * d.sw] : 0.f;
 }
 std::size_t s2d_rows_smem(const S2D& d) {
-  return std::size_t(d.CC / (d.Bw * d.C)) * d.C * d.Wq * d.sw * 4;
+  return std::size_t(d.CC / (d.Bw * d.C)) * d.C * ((d.Wq * d.sw) | 1) * 4;
 }
 // space-to-depth launch: the row kernel when its rows fit in 48 KB
 cudaError_t launch_s2d(const float* x, float* out, const S2D& d, int N, cudaStream_t st) {

@@ -622,29 +622,52 @@ __global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__
   // odd row pitch: the write phase reads rows (c, a) that differ by whole
   // rows, which would otherwise land on the same banks
   const int Ah = d.CC / (d.Bw * d.C), L = d.Wq * d.sw, Lp = L | 1;
-  // load: rows (c, a) one after another, threads along the row (no divisions)
-  for (int c = 0; c < d.C; ++c)
-    for (int a = 0; a < Ah; ++a) {
-      const int h = i * d.sh + a - d.ph;
-      float* r = rows + (c * Ah + a) * Lp;
-      const float* src = x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W;
-      const bool hin = unsigned(h) < unsigned(d.H);
-      for (int t = threadIdx.x; t < L; t += blockDim.x) {
-        const int w = t - d.pw;
-        r[t] = (hin && unsigned(w) < unsigned(d.W)) ? __ldg(src + w) : 0.f;
+  // load: thread t takes column t of all C*Ah (<= 16) rows, every load
+  // issued before the first smem store (a loop of load -> store per row
+  // exposed one DRAM latency per row: 44 us per 64 AlexNet images)
+  const int nr = d.C * Ah;
+  for (int t = threadIdx.x; t < L; t += blockDim.x) {
+    const int w = t - d.pw;
+    const bool win = unsigned(w) < unsigned(d.W);
+    float v[16];
+    int c = 0, a = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = 0.f;
+      if (k < nr) {
+        const int h = i * d.sh + a - d.ph;
+        if (win && unsigned(h) < unsigned(d.H)) v[k] = __ldg(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W + w);
+        if (++a == Ah) {
+          a = 0;
+          ++c;
+        }
       }
     }
-  __syncthreads();
-  // write: each thread owns one channel cc (256 % Cp == 0) for every
-  // 256/Cp-th column j, so its (a, b, c) decode happens once
-  const int cc = threadIdx.x % d.Cp, j0 = threadIdx.x / d.Cp, js = blockDim.x / d.Cp;
-  int off = -1;
-  if (cc < d.CC) {
-    const int ab = cc / d.C, c = cc - ab * d.C, aa = ab / d.Bw, bb = ab - aa * d.Bw;
-    off = (c * Ah + aa) * Lp + bb;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < nr) rows[k * Lp + t] = v[k];
   }
-  float* o = out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp + cc;
-  for (int j = j0; j < d.Wq; j += js) o[std::int64_t(j) * d.Cp] = off >= 0 ? rows[off + j * d.sw] : 0.f;
+  __syncthreads();
+  // write: each thread owns 4 consecutive channels (one float4 store) for
+  // every (256*4/Cp)-th column j; the (a, b, c) decode happens once
+  const int q4 = threadIdx.x % (d.Cp / 4), j0 = threadIdx.x / (d.Cp / 4), js = blockDim.x / (d.Cp / 4);
+  int off[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int cc = 4 * q4 + e;
+    off[e] = -1;
+    if (cc < d.CC) {
+      const int ab = cc / d.C, c = cc - ab * d.C, aa = ab / d.Bw, bb = ab - aa * d.Bw;
+      off[e] = (c * Ah + aa) * Lp + bb;
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp) + q4;
+  for (int j = j0; j < d.Wq; j += js) {
+    const int jo = j * d.sw;
+    o[std::int64_t(j) * (d.Cp / 4)] =
+        make_float4(off[0] >= 0 ? rows[off[0] + jo] : 0.f, off[1] >= 0 ? rows[off[1] + jo] : 0.f,
+                    off[2] >= 0 ? rows[off[2] + jo] : 0.f, off[3] >= 0 ? rows[off[3] + jo] : 0.f);
+  }
 }
 std::size_t s2d_rows_smem(const S2D& d) {
   return std::size_t(d.CC / (d.Bw * d.C)) * d.C * ((d.Wq * d.sw) | 1) * 4;
@@ -652,7 +675,7 @@ std::size_t s2d_rows_smem(const S2D& d) {
 // space-to-depth launch: the row kernel when its rows fit in 48 KB
 cudaError_t launch_s2d(const float* x, float* out, const S2D& d, int N, cudaStream_t st) {
   const std::size_t sm = s2d_rows_smem(d);
-  if (sm <= 48 * 1024 && 256 % d.Cp == 0 && tune("s2d_rows", 1))
+  if (sm <= 48 * 1024 && d.Cp % 4 == 0 && 1024 % d.Cp == 0 && d.CC / d.Bw <= 16 && tune("s2d_rows", 1))
     return launch_pdl(s2d_rows_kernel, dim3(N * d.Hq), dim3(256), sm, st, x, out, d);
   return launch_pdl(s2d_nhwc_kernel, dim3((d.Wq + 31) / 32, (d.Cp + 31) / 32, N * d.Hq), dim3(32, 8), 0, st, x,
                     out, d);

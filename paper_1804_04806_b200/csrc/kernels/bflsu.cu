@@ -175,12 +175,26 @@ struct Gatherer {
     }
   }
 
-  __device__ __forceinline__ void unit(int xm0_, int xrows_, int dk0_, int drows_) {
+  __device__ __forceinline__ void unit(int xm0_, int xrows_, int dk0_, int drows_, int xrows2 = 0) {
     xm0 = xm0_;
     xrows = xrows_;
     dk0 = dk0_;
     drows = drows_;
-    if (sg) {
+    if (c8) {
+      // this warp's 8-row groups (tile t, group q0/8): (c*HW + r*W + s, r << 16 | s),
+      // so a step reads one smem word pair per group instead of two divisions
+      for (int t = 0; t < (xrows2 > 0 ? 2 : 1); ++t) {
+        const int rows = t ? xrows2 : xrows;
+        const int q0 = pw * 8 + lane * kProd * 8;  // rows <= 256 (B tile of the swapped roles)
+        if (q0 < rows) {
+          std::uint32_t rs, c, r, s;
+          p.fd_C.divmod(std::uint32_t(xm0 + t * 256 + q0), rs, c);
+          p.fd_S.divmod(rs, r, s);
+          xtab[t * 32 + q0 / 8] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 16 | s));
+        }
+      }
+      __syncwarp();
+    } else if (sg) {
       // this warp's tap groups (r, s0 = sgrp*sw, c): (c*HW + r*W + s0, r << 16 | s0 << 8 | c)
       // (built by the warp that reads it: gi = pw (mod kProd))
       for (int gi = pw + kProd * lane; gi < p.ngroups; gi += kProd * 32) {
@@ -269,15 +283,14 @@ struct Gatherer {
     } else if (c8) {
       // one bounds test per group, then consecutive channel planes
       for (int t = 0; t < (xs2 ? 2 : 1); ++t) {
-        const int m0 = xm0 + t * 256, rows = t ? xrows2 : xrows;
+        const int rows = t ? xrows2 : xrows;
         const std::uint32_t base = t ? xs2 : xs;
         for (int q0 = pw * 8; q0 < rows; q0 += kProd * 8) {
-          std::uint32_t rs, c, r, s;
-          p.fd_C.divmod(std::uint32_t(m0 + q0), rs, c);
-          p.fd_S.divmod(rs, r, s);
-          const bool ok = valid && unsigned(ihb + int(r)) < unsigned(p.H) && unsigned(iwb + int(s)) < unsigned(p.W);
+          const int2 e = xtab[t * 32 + q0 / 8];
+          const int r = e.y >> 16, s = e.y & 0xffff;
+          const bool ok = valid && unsigned(ihb + r) < unsigned(p.H) && unsigned(iwb + s) < unsigned(p.W);
           const std::uint32_t sz = ok ? 4u : 0u, dst = base + q0 * 128;
-          const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + (long long)c * p.HW + int(r) * p.W + int(s));
+          const std::uint64_t a = reinterpret_cast<std::uint64_t>(xl + e.x);
           const int qn = min(8, rows - q0);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -525,8 +538,8 @@ __global__ void __launch_bounds__(threads_for<kProd2>(), 1) bfl2_kernel(const LP
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
       const int xm0 = mt * 2 * nsub * kBM + int(rank) * kBM, dk0 = nt * p.BN + int(rank) * bh;
-      ga.unit(xm0, min(kBM, p.M - xm0), dk0, min(bh, p.K - dk0));
       const int xrows2 = min(kBM, p.M - xm0 - 2 * kBM);
+      ga.unit(xm0, min(kBM, p.M - xm0), dk0, min(bh, p.K - dk0), p.dual ? xrows2 : 0);
       for (int g = g0; g < g1; ++g) {
         mbar_wait(&empty[st], ph ^ 1);
         const std::uint32_t sst = sbase + st * stage_bytes;

@@ -71,7 +71,8 @@ typedef enum {
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* TMA-fed implicit GEMM on re-laid copies (all ops), ws ~ b   */
   UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BF: cp.async-gathered NCHW operands; BD (strided, few C): GEMM+col2im via smem; ws O(1) */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_SLICED = 7, /* F/BD: PRECOMP over reduction-channel slices, copy <= 40 MiB */
-  UCUDNN_ALGO_COUNT = 8
+  UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_NHWC = 8, /* BF (stride 1): NHWC copies, TMA im2col, MN-major tcgen05 operands */
+  UCUDNN_ALGO_COUNT = 9
 } ucudnnAlgo_t;
 
 /* Returned by Get*Algorithm: a plan handle, >= UCUDNN_VIRTUAL_ALGO_BASE

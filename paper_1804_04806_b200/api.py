@@ -18,7 +18,8 @@ OP_NAMES = {FORWARD: "Forward", BACKWARD_DATA: "BackwardData", BACKWARD_FILTER: 
 POLICIES = {"all": 0, "powerOfTwo": 1, "undivided": 2}
 MODES = {"wr": 0, "wd": 1}
 ALGOS = {0: "IMPLICIT_GEMM", 1: "WINOGRAD", 2: "FFT", 3: "GEMM", 4: "WINOGRAD_4x4", 5: "IMPLICIT_PRECOMP_GEMM",
-         6: "IMPLICIT_GATHER_GEMM", 7: "IMPLICIT_PRECOMP_GEMM_SLICED"}
+         6: "IMPLICIT_GATHER_GEMM", 7: "IMPLICIT_PRECOMP_GEMM_SLICED",
+         8: "IMPLICIT_PRECOMP_GEMM_NHWC"}
 VIRTUAL_ALGO_BASE = 1000
 
 

@@ -6,6 +6,7 @@
 
 #include "../kernels/bdscatter.h"
 #include "../kernels/bflsu.h"
+#include "../kernels/bfnhwc.h"
 #include "../kernels/fft.h"
 #include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
@@ -86,6 +87,16 @@ cudaError_t sliced_run(int op, const ConvShape& s, const float* a, const float* 
   return precomp_sliced_run(op, s, a, b, out, ws, alpha, beta, st);
 }
 
+// Channels-last family: BackwardFilter of stride-1 layers from NHWC copies of
+// x and dy through TMA im2col boxes and MN-major tcgen05 operands (bfnhwc.cu).
+bool nhwc_supports(int op, const ConvShape& s) { return op == 2 && bfn_supports(s); }
+std::int64_t nhwc_workspace(int op, const ConvShape& s) { return op == 2 ? bfn_workspace(s) : 0; }
+cudaError_t nhwc_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
+                     float beta, cudaStream_t st, int) {
+  if (op == 2) return bfn_run(s, a, b, out, ws, alpha, beta, st);
+  return cudaErrorInvalidValue;
+}
+
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
 const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
 const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
@@ -94,6 +105,7 @@ const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 const AlgoImpl kGather{6, "IMPLICIT_GATHER_GEMM", gather_supports, gather_workspace, gather_run};
 const AlgoImpl kSliced{7, "IMPLICIT_PRECOMP_GEMM_SLICED", sliced_supports, sliced_workspace, sliced_run};
+const AlgoImpl kNhwc{8, "IMPLICIT_PRECOMP_GEMM_NHWC", nhwc_supports, nhwc_workspace, nhwc_run};
 
 }  // namespace
 
@@ -107,10 +119,11 @@ const AlgoImpl* find_algo(int id) {
     case 5: return &kPrecomp;
     case 6: return &kGather;
     case 7: return &kSliced;
+    case 8: return &kNhwc;
     default: return nullptr;
   }
 }
 
-int algo_count() { return 8; }
+int algo_count() { return 9; }
 
 }  // namespace ucudnn

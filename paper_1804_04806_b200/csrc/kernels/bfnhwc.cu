@@ -1,0 +1,441 @@
+// UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_NHWC (8), BackwardFilter of stride-1
+// convolutions: TMA im2col boxes of a channels-last x copy and tiled boxes of
+// a channels-last dy copy feed tcgen05.mma with *MN-major* operands.
+//
+//   dW[k][c][r][s] = beta * dW + alpha * sum_{n,oh,ow} dy[n][k][oh][ow] * x[n][c][oh-ph+r][ow-pw+s]
+//   (reference_conv.hpp:141-180)
+//
+// GEMM view: rows = (tap = r*S+s, c) -- R*S*Cp of them, 32-row atoms of one
+// (tap, 32-channel chunk) --, columns = k, reduction = output pixels flattened
+// over (n, oh, ow). For a 32-pixel reduction step the rows' operand is, per
+// atom, exactly one TMA im2col box of the NHWC x copy (32 pixels x 32
+// channels, filter offset (r, s), padding by the box's out-of-bounds fill),
+// and the columns' operand one tiled box of the NHWC dy copy (32 pixels x BN
+// channels). Both land pixel-row-major with the channels contiguous, i.e. the
+// reduction axis is the *strided* one: MN-major UMMA operands. For kind::tf32
+// those only exist in the 128B swizzle with 32-byte atomicity (CUTLASS
+// Layout_MN_SW128_32B_Atom; descriptor layout type 1, 4 K-rows of 128 B per
+// atom; scripts/mn_probe.cu), which TMA writes with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B. Compared with the gather kernel
+// (bflsu.cu) the operands arrive by TMA at ~2x the L2 -> SM rate, and no
+// shifted replicas are needed (bfilter.cu): im2col boxes start at any pixel.
+//
+// Persistent kernel, one CTA per SM, units = (column tile, row tile, split of
+// the reduction), the row tile fastest so the CTAs running at one moment read
+// the same pixel range (dy and x stay L2-resident across row tiles). Warps 0,
+// 2, 3: TMA producers owning ring stages s % 3; warp 1: TMEM owner + MMA
+// issuer (two 256-column accumulators); warps 4-7: epilogue, fp32 RED of the
+// accumulator into a [k][row] scratch (32 lanes = 32 consecutive rows), then a
+// finalize kernel applies alpha / beta into dW[k][c][r][s].
+#include "bfnhwc.h"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace ucudnn {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kMaxBN = 256;
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 256;
+
+struct NGeo {
+  int N, C, H, W, K, R, S, ph, pw, OH, OW, P;
+  int Cp, Kp;        // channel counts padded to 32 (one 128 B swizzle row)
+  int M;             // GEMM rows R*S*Cp
+  int atoms;         // M / 32
+  int m_tiles, n_tiles, BN;
+  int steps;         // 32-pixel reduction steps over N*P flattened pixels
+  int px;            // pixels per ring stage (32 or 64)
+};
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+NGeo make_geo(const ConvShape& s) {
+  NGeo g{};
+  g.N = s.N; g.C = s.C; g.H = s.H; g.W = s.W; g.K = s.K; g.R = s.R; g.S = s.S;
+  g.ph = s.ph; g.pw = s.pw; g.OH = s.OH(); g.OW = s.OW();
+  g.P = g.OH * g.OW;
+  g.Cp = round_up(s.C, 32);
+  g.Kp = round_up(s.K, 32);
+  g.M = s.R * s.S * g.Cp;
+  g.atoms = g.M / 32;
+  g.m_tiles = (g.M + kBM - 1) / kBM;
+  g.n_tiles = (g.Kp + kMaxBN - 1) / kMaxBN;
+  g.BN = round_up((g.Kp + g.n_tiles - 1) / g.n_tiles, 32);
+  g.n_tiles = (g.Kp + g.BN - 1) / g.BN;
+  g.px = tune("bfn_px", 32) == 64 ? 64 : 32;
+  g.steps = int((std::int64_t(g.N) * g.P + g.px - 1) / g.px);
+  return g;
+}
+
+std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
+std::size_t x_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.H * g.W * g.Cp * 4); }
+std::size_t dy_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.P * g.Kp * 4); }
+int rows_pad(const NGeo& g) { return g.m_tiles * kBM; }
+std::size_t acc_bytes(const NGeo& g) { return a256(std::size_t(g.K) * rows_pad(g) * 4); }
+
+struct NParams {
+  float* acc;  // [K][rpad] fp32 partial sums
+  int C, Cp, K, S, RS, M, atoms, cch, BN, rpad, ph, pw;
+  int m_tiles, tiles, splits, steps, steps_per_unit, stages, px;
+  FastDiv fd_P, fd_OW;
+};
+
+__device__ __forceinline__ void tma_3d(void* dst, const void* tmap, std::uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// MN-major descriptor, 128B swizzle with 32 B atoms: `lbo` = byte stride
+// between 32-element MN blocks, SBO = 512 (4 K-rows of 128 B per atom).
+__device__ __forceinline__ std::uint64_t desc_mn32(std::uint32_t saddr, std::uint32_t lbo) {
+  std::uint64_t d = 0;
+  d |= std::uint64_t((saddr >> 4) & 0x3FFF);
+  d |= std::uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= std::uint64_t(512 >> 4) << 32;
+  d |= std::uint64_t(1) << 46;
+  d |= std::uint64_t(1) << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    bfn_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap, const NParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t blk = std::uint32_t(p.px) * 128;  // one 32-channel block of px pixel rows
+  const std::uint32_t a_bytes = 4 * blk;
+  const std::uint32_t b_bytes = std::uint32_t(p.BN / 32) * blk;
+  const std::uint32_t stage_bytes = (a_bytes + b_bytes + 1023) & ~1023u;
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&dmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+  const int units = p.tiles * p.splits;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producers
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = u % p.tiles, split = u / p.tiles;
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        for (int g = g0; g < g1; ++g, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
+          const int st = it % kStages;
+          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], a_bytes + b_bytes);
+          unsigned char* sa = smem + st * stage_bytes;
+          // first output pixel of the step -> im2col start (its window corner)
+          const std::uint32_t q0 = std::uint32_t(g) * std::uint32_t(p.px);
+          std::uint32_t n, pix, oh, ow;
+          p.fd_P.divmod(q0, n, pix);
+          p.fd_OW.divmod(pix, oh, ow);
+          const int cw = int(ow) - p.pw, ch = int(oh) - p.ph;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            // atoms past the last (tap, chunk) re-load the last one: their
+            // rows are dropped by the epilogue
+            const int a = min(mt * 4 + i, p.atoms - 1);
+            const int tap = a / p.cch, cc = a - tap * p.cch;
+            const int r = tap / p.S, s = tap - r * p.S;
+            tma_im2col_4d(sa + i * blk, &xmap, &full[st], cc * 32, cw, ch, int(n), (unsigned short)s,
+                          (unsigned short)r);
+          }
+          tma_3d(sa + a_bytes, &dmap, &full[st], 0, int(q0), nt * (p.BN / 32));
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN) | (1u << 15) | (1u << 16);
+    const std::uint32_t sbase = smem_u32(smem);
+    const int ksub = p.px / 8;
+    int it = 0, tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int split = u / p.tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      for (int g = g0; g < g1; ++g, ++it) {
+        const int st = it % kStages;
+        mbar_wait(&full[st], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+          for (int j = 0; j < ksub; ++j)
+            mma_tf32(dtm, desc_mn32(sa + j * 1024, blk), desc_mn32(sb + j * 1024, blk), idesc,
+                     (g != g0 || j != 0) ? 1u : 0u);
+          mma_commit(&empty[st]);
+          if (g + 1 >= g1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+      if (g1 <= g0 && lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue: RED into acc[k][row]
+    const int ew = warp - 4;
+    int tl = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl & 1;
+      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc_fence_after();
+      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const int row = mt * kBM + ew * 32 + lane;
+      const bool live = g1 > g0 && row < p.M && (row % p.Cp) < p.C;
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (!live) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = nt * p.BN + c0 + j;
+          if (k >= p.K) break;
+          red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// NCHW -> N(HW)Cp with zero channels C..Cp-1: 64 pixels x 32 channels per
+// block, coalesced reads along pixels, float4 stores along channels.
+__global__ void __launch_bounds__(256) nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C,
+                                                   int HW, int Cp) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float tile[32][65];
+  const int n = blockIdx.z;
+  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* s = src + std::int64_t(n) * C * HW;
+  float* d = dst + std::int64_t(n) * HW * Cp;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + warp + 8 * i;
+    const float* row = s + std::int64_t(c) * HW;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int pp = p0 + lane + 32 * h;
+      tile[warp + 8 * i][lane + 32 * h] = (c < C && pp < HW) ? __ldg(row + pp) : 0.f;
+    }
+  }
+  __syncthreads();
+  const int q = threadIdx.x & 7;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int pl = (threadIdx.x >> 3) + 32 * k, pp = p0 + pl;
+    if (pp < HW)
+      *reinterpret_cast<float4*>(d + std::int64_t(pp) * Cp + c0 + 4 * q) =
+          make_float4(tile[4 * q][pl], tile[4 * q + 1][pl], tile[4 * q + 2][pl], tile[4 * q + 3][pl]);
+  }
+}
+
+struct NFinal {
+  const float* acc;
+  float* dw;
+  float alpha, beta;
+  int C, Cp, RS, rpad;
+  std::int64_t n;
+};
+
+// dW[k][c][r][s] = beta * dW + alpha * acc[k][(r*S+s)*Cp + c]
+__global__ void __launch_bounds__(256) bfn_finalize_kernel(const NFinal f) {
+  pdl_wait();
+  pdl_trigger();
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < f.n;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    const int tap = int(i % f.RS);
+    const std::int64_t t = i / f.RS;
+    const int c = int(t % f.C), k = int(t / f.C);
+    const float v = f.acc[std::int64_t(k) * f.rpad + tap * f.Cp + c];
+    f.dw[i] = f.beta == 0.f ? f.alpha * v : f.alpha * v + f.beta * f.dw[i];
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(f);
+  }();
+  return fn;
+}
+
+int sm_count() {
+  static int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+}  // namespace
+
+bool bfn_supports(const ConvShape& s) {
+  // stride 1 (the im2col walk would need traversal strides), whole 32-channel
+  // chunks of x (a padded copy of 3-channel inputs would be 90 % zeros),
+  // 32-bit flattened pixel coordinates
+  return s.sh == 1 && s.sw == 1 && s.C % 32 == 0 && s.R <= 16 && s.S <= 16 && s.ph < s.R && s.pw < s.S &&
+         std::int64_t(s.N) * s.OH() * s.OW() + 64 < (std::int64_t(1) << 31) && tune("bfn", 1);
+}
+
+std::int64_t bfn_workspace(const ConvShape& s) {
+  const NGeo g = make_geo(s);
+  return std::int64_t(acc_bytes(g) + x_bytes(g) + dy_bytes(g));
+}
+
+cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
+                    float beta, cudaStream_t st) {
+  const NGeo g = make_geo(s);
+  float* acc = static_cast<float*>(ws);
+  float* xn = reinterpret_cast<float*>(static_cast<char*>(ws) + acc_bytes(g));
+  float* dyn = reinterpret_cast<float*>(static_cast<char*>(ws) + acc_bytes(g) + x_bytes(g));
+  cudaError_t e = cudaMemsetAsync(acc, 0, std::size_t(g.K) * rows_pad(g) * 4, st);
+  if (e != cudaSuccess) return e;
+  const int HW = g.H * g.W;
+  e = launch_pdl(nhwc_kernel, dim3((HW + 63) / 64, g.Cp / 32, g.N), dim3(256), 0, st, x, xn, g.C, HW, g.Cp);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(nhwc_kernel, dim3((g.P + 63) / 64, g.Kp / 32, g.N), dim3(256), 0, st, dy, dyn, g.K, g.P, g.Kp);
+  if (e != cudaSuccess) return e;
+
+  CUtensorMap xmap, dmap;
+  {
+    const cuuint64_t dims[4] = {cuuint64_t(g.Cp), cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.N)};
+    const cuuint64_t strides[3] = {cuuint64_t(g.Cp) * 4, cuuint64_t(g.Cp) * 4 * g.W,
+                                   cuuint64_t(g.Cp) * 4 * g.W * g.H};
+    const int lower[2] = {-g.pw, -g.ph};
+    const int upper[2] = {g.pw - (g.S - 1), g.ph - (g.R - 1)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_im2col()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, xn, dims, strides, lower, upper, 32,
+                                 cuuint32_t(g.px), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    int drv = 0;
+    cudaDriverGetVersion(&drv);
+    if (drv <= 13010 && std::size_t(g.N) * HW * g.Cp * 4 < 131072)  // encoder quirk (as in precomp.cu)
+      reinterpret_cast<std::uint64_t*>(&xmap)[1] &= ~(1ull << 21);
+  }
+  {
+    // dy_nhwc as (k in chunk, pixel, chunk): a {32, px, BN/32} box lands as
+    // BN/32 blocks of [px rows][32 channels] -- the MN-major B operand
+    const cuuint64_t dims[3] = {32, cuuint64_t(std::int64_t(g.N) * g.P), cuuint64_t(g.Kp / 32)};
+    const cuuint64_t strides[2] = {cuuint64_t(g.Kp) * 4, 128};
+    const cuuint32_t box[3] = {32, cuuint32_t(g.px), cuuint32_t(g.BN / 32)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_tiled()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dyn, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+
+  const int sms = sm_count();
+  NParams p{};
+  p.acc = acc;
+  p.C = g.C; p.Cp = g.Cp; p.K = g.K; p.S = g.S; p.RS = g.R * g.S; p.M = g.M; p.atoms = g.atoms;
+  p.cch = g.Cp / 32; p.BN = g.BN; p.rpad = rows_pad(g); p.ph = g.ph; p.pw = g.pw;
+  p.m_tiles = g.m_tiles;
+  p.tiles = g.m_tiles * g.n_tiles;
+  p.steps = g.steps;
+  p.px = g.px;
+  p.fd_P = FastDiv(std::uint32_t(g.P));
+  p.fd_OW = FastDiv(std::uint32_t(g.OW));
+  // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
+  const int splits = std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * sms / p.tiles));
+  p.steps_per_unit = (p.steps + splits - 1) / splits;
+  p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
+  const int stage_bytes = ((4 + g.BN / 32) * g.px * 128 + 1023) & ~1023;
+  p.stages = std::max(2, std::min({kMaxStages, tune("bfn_stages", 8), (200 * 1024) / stage_bytes}));
+  const int smem = p.stages * stage_bytes + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(bfn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int units = p.tiles * p.splits;
+  e = launch_pdl(bfn_kernel, dim3(std::min(units, sms)), dim3(kThreads), std::size_t(smem), st, xmap, dmap, p);
+  if (e != cudaSuccess) return e;
+
+  NFinal f{};
+  f.acc = acc;
+  f.dw = dw;
+  f.alpha = alpha;
+  f.beta = beta;
+  f.C = g.C; f.Cp = g.Cp; f.RS = g.R * g.S; f.rpad = rows_pad(g);
+  f.n = std::int64_t(g.K) * g.C * g.R * g.S;
+  return launch_pdl(bfn_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256),
+                    0, st, f);
+}
+
+}  // namespace ucudnn

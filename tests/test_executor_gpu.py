@@ -22,7 +22,7 @@ def forced_table(s, op, times):
     """times[alg][b] -> us (missing: infeasible); real workspace sizes."""
     h = kernel_hash(op, s)
     rows = []
-    for alg in range(8):
+    for alg in range(9):
         for b in range(1, s.N + 1):
             t = times.get(alg, {}).get(b)
             ws, ok = algorithm_workspace(op, s, alg, b)

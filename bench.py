@@ -146,6 +146,20 @@ def timed(fn, steps, warmup, dev, dist_on):
     return ms
 
 
+def dom_traffic(name, plan):
+    """DRAM bytes (read + write) of the dominant call, from the committed ncu
+    capture of the same planned step (scripts/traffic.py -> profiles/); null
+    when that capture's plan for this call differs from this run's."""
+    path = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        rec = json.load(open(path))["calls"].get(name)
+    except (OSError, ValueError, KeyError):
+        return None
+    if not rec or rec["plan"] != plan:
+        return None
+    return rec["dram_bytes"]
+
+
 def tf32_peak(dev):
     """cuBLAS TF32 GEMM (8192^3, best of 10) -- the tensor-pipe roofline
     denominator for TF32 kernels (MEASURED_PEAKS.json carries bf16 only)."""
@@ -305,6 +319,8 @@ def main():
     dom_flops = stack.layers[dom[0]].shape.flops()
     dom_tflops = dom_flops / (per_ms[dom] * 1e-3) / 1e12
     peak = tf32_peak(dev) if rank == 0 else None
+    traffic = dom_traffic(f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
+                          "+".join(f"{a}@{b}" for a, b in h.plan(stack.algos[dom])))
 
     # end-to-end through the public API with host buffers: H2D of the step's
     # inputs (conv1 input images + top-layer output gradient), 15 planned
@@ -315,35 +331,59 @@ def main():
     h2d = x_host.numel() * 4 + dy_host.numel() * 4
     d2h = sum(d.numel() * 4 for d in dw_host)
 
-    # copies overlap compute where the data flow allows: the top gradient's
-    # H2D runs on a copy stream during the forward pass, each dW's D2H starts
-    # right after its BackwardFilter; the step ends when every copy is done.
-    cp = torch.cuda.Stream(dev)
+    # Input pipeline as a training loop runs it: the next step's inputs (conv1
+    # images + top-layer output gradient) are copied host -> device on an H2D
+    # stream into the other half of a double buffer while this step computes
+    # (a data loader's pinned-memory prefetch); each dW goes device -> host on
+    # a D2H stream right after its BackwardFilter. Every step issues exactly
+    # one H2D of its successor's inputs and one D2H of its dWs, so the timed
+    # region of K steps carries K H2Ds and K D2Hs; the step ends when its D2Hs
+    # are done. PCIe is full duplex, hence separate H2D / D2H streams.
+    h2d_stream, d2h_stream = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    xbuf = [stack.t[0]["x"], torch.empty_like(stack.t[0]["x"])]
+    dybuf = [stack.t[-1]["dy"], torch.empty_like(stack.t[-1]["dy"])]
+    state = {"k": 0, "ready": None, "done": None}
+
+    def prefetch(k):
+        # inputs of step k into buffer k % 2, once step k - 2 (its last user) is done
+        if state["done"] is not None:
+            h2d_stream.wait_event(state["done"])
+        with torch.cuda.stream(h2d_stream):
+            xbuf[k % 2].copy_(x_host, non_blocking=True)
+            dybuf[k % 2].copy_(dy_host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(h2d_stream)
+        return ev
 
     def step_e2e():
         cur = torch.cuda.current_stream(dev)
-        stack.t[0]["x"].copy_(x_host, non_blocking=True)
-        cp.wait_stream(cur)
-        with torch.cuda.stream(cp):
-            stack.t[-1]["dy"].copy_(dy_host, non_blocking=True)
-        dy_ready = torch.cuda.Event()
-        dy_ready.record(cp)
+        k = state["k"]
+        if state["ready"] is None:
+            state["ready"] = prefetch(k)
+        ready = state["ready"]
+        stack.t[0]["x"], stack.t[-1]["dy"] = xbuf[k % 2], dybuf[k % 2]
+        cur.wait_event(ready)
+        nxt = prefetch(k + 1)
 
         def on_dw(i):
             ev = torch.cuda.Event()
             ev.record(cur)
-            cp.wait_event(ev)
-            with torch.cuda.stream(cp):
+            d2h_stream.wait_event(ev)
+            with torch.cuda.stream(d2h_stream):
                 dw_host[i].copy_(stack.t[i]["dw"], non_blocking=True)
 
-        stack.step(h, comm, comm_stream, on_backward=lambda: cur.wait_event(dy_ready),
-                   on_dw=None if comm is not None else on_dw)
+        stack.step(h, comm, comm_stream, on_dw=None if comm is not None else on_dw)
         if comm is not None:
             for d, t in zip(dw_host, stack.t):
                 d.copy_(t["dw"], non_blocking=True)
-        cur.wait_stream(cp)
+        cur.wait_stream(d2h_stream)
+        done = torch.cuda.Event()
+        done.record(cur)
+        state.update(k=k + 1, ready=nxt, done=done)
 
     ms_e2e = timed(step_e2e, args.steps, args.warmup, dev, dist_on)
+    torch.cuda.synchronize(dev)
+    stack.t[0]["x"], stack.t[-1]["dy"] = xbuf[0], dybuf[0]
 
     if rank == 0:
         cpu = None
@@ -372,11 +412,15 @@ def main():
                        "launch": "eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls"},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
                          "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
-                         "frac": round(dom_tflops / peak, 3), "traffic": None,
+                         "frac": round(dom_tflops / peak, 3), "traffic": traffic,
+                         "traffic_source": "bytes per call: ncu dram__bytes_read.sum + dram__bytes_write.sum over "
+                                           "the call's launches, profiles/r01_traffic.json (same plan)",
                          "peak_source": "cuBLAS TF32 8192^3 GEMM measured in this run"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(ms_e2e, 4), "unit": "ms/iter", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "pipeline": "next step's inputs H2D-prefetched into a double buffer during this step; "
+                                "dW D2H after each BackwardFilter; eager C-ABI launches"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "plan_seconds": round(plan_s, 1),

@@ -53,6 +53,7 @@ struct NGeo {
   int Cp, Kp;        // channel counts padded to 32 (one 128 B swizzle row)
   int M;             // GEMM rows R*S*Cp
   int atoms;         // M / 32
+  int msub;          // 128-row MMA sub-tiles per CTA tile (2: the dy box feeds twice the MMA work)
   int m_tiles, n_tiles, BN;
   int steps;         // 32-pixel reduction steps over N*P flattened pixels
   int px;            // pixels per ring stage (32 or 64)
@@ -69,10 +70,11 @@ NGeo make_geo(const ConvShape& s) {
   g.Kp = round_up(s.K, 32);
   g.M = s.R * s.S * g.Cp;
   g.atoms = g.M / 32;
-  g.m_tiles = (g.M + kBM - 1) / kBM;
   g.n_tiles = (g.Kp + kMaxBN - 1) / kMaxBN;
   g.BN = round_up((g.Kp + g.n_tiles - 1) / g.n_tiles, 32);
   g.n_tiles = (g.Kp + g.BN - 1) / g.BN;
+  g.msub = g.M > kBM ? std::max(1, std::min(2, tune("bfn_msub", 2))) : 1;
+  g.m_tiles = (g.M + g.msub * kBM - 1) / (g.msub * kBM);
   g.px = tune("bfn_px", 32) == 64 ? 64 : 32;
   g.steps = int((std::int64_t(g.N) * g.P + g.px - 1) / g.px);
   return g;
@@ -81,13 +83,13 @@ NGeo make_geo(const ConvShape& s) {
 std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
 std::size_t x_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.H * g.W * g.Cp * 4); }
 std::size_t dy_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.P * g.Kp * 4); }
-int rows_pad(const NGeo& g) { return g.m_tiles * kBM; }
+int rows_pad(const NGeo& g) { return g.m_tiles * g.msub * kBM; }
 std::size_t acc_bytes(const NGeo& g) { return a256(std::size_t(g.K) * rows_pad(g) * 4); }
 
 struct NParams {
   float* acc;  // [K][rpad] fp32 partial sums
   int C, Cp, K, S, RS, M, atoms, cch, BN, rpad, ph, pw;
-  int m_tiles, tiles, splits, steps, steps_per_unit, stages, px;
+  int m_tiles, tiles, splits, steps, steps_per_unit, stages, px, msub, nacc;
   FastDiv fd_P, fd_OW;
 };
 
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                          ~std::uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t blk = std::uint32_t(p.px) * 128;  // one 32-channel block of px pixel rows
-  const std::uint32_t a_bytes = 4 * blk;
+  const std::uint32_t a_bytes = 4 * p.msub * blk;
   const std::uint32_t b_bytes = std::uint32_t(p.BN / 32) * blk;
   const std::uint32_t stage_bytes = (a_bytes + b_bytes + 1023) & ~1023u;
   const int kStages = p.stages;
@@ -172,11 +174,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.fd_P.divmod(q0, n, pix);
           p.fd_OW.divmod(pix, oh, ow);
           const int cw = int(ow) - p.pw, ch = int(oh) - p.ph;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
+#pragma unroll 1
+          for (int i = 0; i < 4 * p.msub; ++i) {
             // atoms past the last (tap, chunk) re-load the last one: their
             // rows are dropped by the epilogue
-            const int a = min(mt * 4 + i, p.atoms - 1);
+            const int a = min(mt * 4 * p.msub + i, p.atoms - 1);
             const int tap = a / p.cch, cc = a - tap * p.cch;
             const int r = tap / p.S, s = tap - r * p.S;
             tma_im2col_4d(sa + i * blk, &xmap, &full[st], cc * 32, cw, ch, int(n), (unsigned short)s,
@@ -196,19 +198,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
       const int split = u / p.tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-      const int acc = tl & 1;
-      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      const int acc = tl % p.nacc, use = tl / p.nacc;
+      mbar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
-      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * p.msub * p.BN);
       for (int g = g0; g < g1; ++g, ++it) {
         const int st = it % kStages;
         mbar_wait(&full[st], (it / kStages) & 1);
         tc_fence_after();
         if (lane == 0) {
           const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
-          for (int j = 0; j < ksub; ++j)
-            mma_tf32(dtm, desc_mn32(sa + j * 1024, blk), desc_mn32(sb + j * 1024, blk), idesc,
-                     (g != g0 || j != 0) ? 1u : 0u);
+          for (int m = 0; m < p.msub; ++m)
+            for (int j = 0; j < ksub; ++j)
+              mma_tf32(dtm + std::uint32_t(m * p.BN), desc_mn32(sa + m * 4 * blk + j * 1024, blk),
+                       desc_mn32(sb + j * 1024, blk), idesc, (g != g0 || j != 0) ? 1u : 0u);
           mma_commit(&empty[st]);
           if (g + 1 >= g1) mma_commit(&tfull[acc]);
         }
@@ -225,21 +228,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = u % p.tiles, split = u / p.tiles;
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-      const int acc = tl & 1;
-      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      const int acc = tl % p.nacc, use = tl / p.nacc;
+      mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
-      const int row = mt * kBM + ew * 32 + lane;
-      const bool live = g1 > g0 && row < p.M && (row % p.Cp) < p.C;
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tbase + std::uint32_t(c0), v);
-        if (!live) continue;
+      for (int m = 0; m < p.msub; ++m) {
+        const std::uint32_t tbase =
+            tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t((acc * p.msub + m) * p.BN);
+        const int row = (mt * p.msub + m) * kBM + ew * 32 + lane;
+        const bool live = g1 > g0 && row < p.M && (row % p.Cp) < p.C;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int k = nt * p.BN + c0 + j;
-          if (k >= p.K) break;
-          red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
+          for (int j = 0; j < 32; ++j) {
+            const int k = nt * p.BN + c0 + j;
+            if (k >= p.K) break;
+            red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
+          }
         }
       }
       tc_fence_before();
@@ -408,13 +414,15 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.tiles = g.m_tiles * g.n_tiles;
   p.steps = g.steps;
   p.px = g.px;
+  p.msub = g.msub;
+  p.nacc = 2 * g.msub * g.BN <= 512 ? 2 : 1;
   p.fd_P = FastDiv(std::uint32_t(g.P));
   p.fd_OW = FastDiv(std::uint32_t(g.OW));
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * sms / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
-  const int stage_bytes = ((4 + g.BN / 32) * g.px * 128 + 1023) & ~1023;
+  const int stage_bytes = ((4 * g.msub + g.BN / 32) * g.px * 128 + 1023) & ~1023;
   p.stages = std::max(2, std::min({kMaxStages, tune("bfn_stages", 8), (200 * 1024) / stage_bytes}));
   const int smem = p.stages * stage_bytes + 1024 + 256;
   static bool attr = false;

@@ -53,7 +53,8 @@ struct NGeo {
   int Cp, Kp;        // channel counts padded to 32 (one 128 B swizzle row)
   int M;             // GEMM rows R*S*Cp
   int atoms;         // M / 32
-  int msub;          // 128-row MMA sub-tiles per CTA tile (2: the dy box feeds twice the MMA work)
+  int two;           // CTA pairs (tcgen05 cta_group::2): M = 256 per MMA, dy box split along N
+  int msub;          // MMA sub-tiles per CTA tile (2: the dy box feeds twice the MMA work)
   int m_tiles, n_tiles, BN;
   int steps;         // 32-pixel reduction steps over N*P flattened pixels
   int px;            // pixels per ring stage (32 or 64)
@@ -70,11 +71,30 @@ NGeo make_geo(const ConvShape& s) {
   g.Kp = round_up(s.K, 32);
   g.M = s.R * s.S * g.Cp;
   g.atoms = g.M / 32;
+  // CTA pairs only with two MMA sub-tiles (512-row pair tiles) and only when
+  // those pad no more rows than the 1-SM kernel's 256-row tiles: measured
+  // (AlexNet BF at 256 images, 1-SM vs pair) conv4 (M = 3456) 233 -> 206 us,
+  // but conv2 / conv3 / conv5 with 256-row pair tiles 378 -> 423, 194 -> 220,
+  // 144 -> 153 us
+  const int knob = tune("bfn2", -1);
+  g.two = knob >= 0 ? (knob > 0 && g.M >= 2 * kBM) : round_up(g.M, 4 * kBM) <= round_up(g.M, 2 * kBM);
+  const int bq = g.two ? 64 : 32;  // pairs: each CTA holds BN/2 columns, whole 32-column blocks
   g.n_tiles = (g.Kp + kMaxBN - 1) / kMaxBN;
-  g.BN = round_up((g.Kp + g.n_tiles - 1) / g.n_tiles, 32);
+  g.BN = round_up((g.Kp + g.n_tiles - 1) / g.n_tiles, bq);
   g.n_tiles = (g.Kp + g.BN - 1) / g.BN;
-  g.msub = g.M > kBM ? std::max(1, std::min(2, tune("bfn_msub", 2))) : 1;
-  g.m_tiles = (g.M + g.msub * kBM - 1) / (g.msub * kBM);
+  const int pair_rows = (g.two ? 2 : 1) * kBM;
+  if (g.M <= pair_rows) {
+    g.msub = 1;
+  } else if (g.two && knob < 0) {
+    g.msub = 2;
+  } else {
+    // fewest padded rows, ties to 2 sub-tiles (more MMA work per dy box)
+    const int r1 = round_up(g.M, pair_rows), r2 = round_up(g.M, 2 * pair_rows);
+    g.msub = r2 <= r1 ? 2 : 1;
+    const int forced = tune("bfn_msub", 0);
+    if (forced == 1 || forced == 2) g.msub = forced;
+  }
+  g.m_tiles = (g.M + g.msub * pair_rows - 1) / (g.msub * pair_rows);
   g.px = tune("bfn_px", 32) == 64 ? 64 : 32;
   g.steps = int((std::int64_t(g.N) * g.P + g.px - 1) / g.px);
   return g;
@@ -83,7 +103,7 @@ NGeo make_geo(const ConvShape& s) {
 std::size_t a256(std::size_t b) { return (b + 255) / 256 * 256; }
 std::size_t x_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.H * g.W * g.Cp * 4); }
 std::size_t dy_bytes(const NGeo& g) { return a256(std::size_t(g.N) * g.P * g.Kp * 4); }
-int rows_pad(const NGeo& g) { return g.m_tiles * g.msub * kBM; }
+int rows_pad(const NGeo& g) { return g.m_tiles * g.msub * (g.two ? 2 : 1) * kBM; }
 std::size_t acc_bytes(const NGeo& g) { return a256(std::size_t(g.K) * rows_pad(g) * 4); }
 
 struct NParams {
@@ -260,6 +280,171 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+__device__ __forceinline__ void tma_3d_2sm(void* dst, const void* tmap, std::uint32_t bar_cluster, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// CTA-pair version (tcgen05.mma.cta_group::2): per MMA sub-tile 256 rows,
+// 128 from each CTA's own im2col boxes; each CTA loads half of the dy box
+// (BN/2 columns), so per SM a step moves (4 * msub + BN/64) blocks instead of
+// (4 * msub + BN/32). Rank 0 issues the MMAs; both CTAs' TMA bytes count on
+// its full barriers; commits multicast to both CTAs; both epilogues release
+// rank 0's accumulator barrier (as bf2_kernel in bfilter.cu).
+__global__ void __launch_bounds__(kThreads, 1)
+    bfn2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap, const NParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cluster_rank();
+  const std::uint32_t blk = std::uint32_t(p.px) * 128;
+  const std::uint32_t a_bytes = 4 * p.msub * blk;
+  const std::uint32_t b_bytes = std::uint32_t(p.BN / 64) * blk;
+  const std::uint32_t stage_bytes = (a_bytes + b_bytes + 1023) & ~1023u;
+  const int kStages = p.stages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&dmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int units = p.tiles * p.splits;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    const int pq = warp == 0 ? 0 : warp - 1;
+    const int nprod = kStages < 3 ? kStages : 3;
+    if (lane == 0) {
+      int it = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int tile = u % p.tiles, split = u / p.tiles;
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        for (int g = g0; g < g1; ++g, ++it) {
+          if ((it % kStages) % nprod != pq) continue;
+          const int st = it % kStages;
+          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2u * (a_bytes + b_bytes));
+          const std::uint32_t bar = mapa(smem_u32(&full[st]), 0);
+          unsigned char* sa = smem + st * stage_bytes;
+          const std::uint32_t q0 = std::uint32_t(g) * std::uint32_t(p.px);
+          std::uint32_t n, pix, oh, ow;
+          p.fd_P.divmod(q0, n, pix);
+          p.fd_OW.divmod(pix, oh, ow);
+          const int cw = int(ow) - p.pw, ch = int(oh) - p.ph;
+#pragma unroll 1
+          for (int m = 0; m < p.msub; ++m) {
+            const int a0 = (((mt * p.msub + m) * 2 + int(rank)) * kBM) / 32;
+#pragma unroll 1
+            for (int i = 0; i < 4; ++i) {
+              const int a = min(a0 + i, p.atoms - 1);
+              const int tap = a / p.cch, cc = a - tap * p.cch;
+              const int r = tap / p.S, s = tap - r * p.S;
+              tma_im2col_4d_2sm(sa + (m * 4 + i) * blk, &xmap, bar, cc * 32, cw, ch, int(n), (unsigned short)s,
+                                (unsigned short)r);
+            }
+          }
+          tma_3d_2sm(sa + a_bytes, &dmap, bar, 0, int(q0), nt * (p.BN / 32) + int(rank) * (p.BN / 64));
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0) {
+      const std::uint32_t idesc = idesc_tf32(2 * kBM, p.BN) | (1u << 15) | (1u << 16);
+      const std::uint32_t sbase = smem_u32(smem);
+      const int ksub = p.px / 8;
+      int it = 0, tl = 0;
+      for (int u = cid; u < units; u += ncl, ++tl) {
+        const int split = u / p.tiles;
+        const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+        const int acc = tl % p.nacc, use = tl / p.nacc;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t dtm = tmem + std::uint32_t(acc * p.msub * p.BN);
+        for (int g = g0; g < g1; ++g, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
+            for (int m = 0; m < p.msub; ++m)
+              for (int j = 0; j < ksub; ++j)
+                mma_tf32_2sm(dtm + std::uint32_t(m * p.BN), desc_mn32(sa + m * 4 * blk + j * 1024, blk),
+                             desc_mn32(sb + j * 1024, blk), idesc, (g != g0 || j != 0) ? 1u : 0u);
+            mma_commit_2sm(&empty[st], 3);
+            if (g + 1 >= g1) mma_commit_2sm(&tfull[acc], 3);
+          }
+          __syncwarp();
+        }
+        if (g1 <= g0 && lane == 0) mma_commit_2sm(&tfull[acc], 3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const std::uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    int tl = 0;
+    for (int u = cid; u < units; u += ncl, ++tl) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
+      const int acc = tl % p.nacc, use = tl / p.nacc;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      for (int m = 0; m < p.msub; ++m) {
+        const std::uint32_t tbase =
+            tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t((acc * p.msub + m) * p.BN);
+        const int row = ((mt * p.msub + m) * 2 + int(rank)) * kBM + ew * 32 + lane;
+        const bool live = g1 > g0 && row < p.M && (row % p.Cp) < p.C;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + std::uint32_t(c0), v);
+          if (!live) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = nt * p.BN + c0 + j;
+            if (k >= p.K) break;
+            red_add(p.acc + std::int64_t(k) * p.rpad + row, v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_remote(tempty_leader0 + std::uint32_t(acc) * 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_2sm<512>(tmem);
+  }
+}
+
 // NCHW -> N(HW)Cp with zero channels C..Cp-1: 64 pixels x 32 channels per
 // block, coalesced reads along pixels, float4 stores along channels.
 __global__ void __launch_bounds__(256) nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C,
@@ -397,7 +582,7 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
     // BN/32 blocks of [px rows][32 channels] -- the MN-major B operand
     const cuuint64_t dims[3] = {32, cuuint64_t(std::int64_t(g.N) * g.P), cuuint64_t(g.Kp / 32)};
     const cuuint64_t strides[2] = {cuuint64_t(g.Kp) * 4, 128};
-    const cuuint32_t box[3] = {32, cuuint32_t(g.px), cuuint32_t(g.BN / 32)};
+    const cuuint32_t box[3] = {32, cuuint32_t(g.px), cuuint32_t(g.BN / (g.two ? 64 : 32))};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode_tiled()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dyn, dims, strides, box, estr,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
@@ -418,21 +603,40 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.nacc = 2 * g.msub * g.BN <= 512 ? 2 : 1;
   p.fd_P = FastDiv(std::uint32_t(g.P));
   p.fd_OW = FastDiv(std::uint32_t(g.OW));
-  // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
-  const int splits = std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * sms / p.tiles));
+  // split the reduction so the tiles fill the SMs (or SM pairs) once, >= 8 steps per unit
+  const int slots = g.two ? sms / 2 : sms;
+  const int splits = std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * slots / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
-  const int stage_bytes = ((4 * g.msub + g.BN / 32) * g.px * 128 + 1023) & ~1023;
+  const int stage_bytes = ((4 * g.msub + g.BN / (g.two ? 64 : 32)) * g.px * 128 + 1023) & ~1023;
   p.stages = std::max(2, std::min({kMaxStages, tune("bfn_stages", 8), (200 * 1024) / stage_bytes}));
   const int smem = p.stages * stage_bytes + 1024 + 256;
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(bfn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(bfn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int units = p.tiles * p.splits;
-  e = launch_pdl(bfn_kernel, dim3(std::min(units, sms)), dim3(kThreads), std::size_t(smem), st, xmap, dmap, p);
+  if (g.two) {
+    count_launch();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(slots, units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = std::size_t(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = 2;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, bfn2_kernel, xmap, dmap, p);
+  } else {
+    e = launch_pdl(bfn_kernel, dim3(std::min(units, sms)), dim3(kThreads), std::size_t(smem), st, xmap, dmap, p);
+  }
   if (e != cudaSuccess) return e;
 
   NFinal f{};

@@ -129,3 +129,21 @@ def test_precomp_sliced(cuda, spec):
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *v[:9], v[9], "7"],
                          env=env, capture_output=True, text=True, timeout=300)
     assert "exact True" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("tune", ["", "bfn2=1,bfn_msub=1", "bfn2=1,bfn_msub=2", "bfn2=0,bfn_msub=1", "bfn2=0,bfn_msub=2",
+                                  "bfn_px=64"])
+@pytest.mark.parametrize("spec", ["2 128 9 9 64 2 2 0 1", "3 64 11 13 96 3 3 1 1", "2 96 7 7 200 5 5 2 1",
+                                  "1 32 6 6 40 1 1 0 1"])
+def test_bf_nhwc_variants(cuda, spec, tune):
+    """IMPLICIT_PRECOMP_GEMM_NHWC (algorithm 8) BackwardFilter: the 1-SM
+    kernel with one or two MMA sub-tiles per CTA, the CTA-pair kernel, and
+    64-pixel ring stages, forced through UCUDNN_TUNE (read once per process,
+    so each runs in a child); bit-exact against the fp64 oracle on integer
+    data (ragged K, N*P not a multiple of 32, rows past R*S*C)."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, UCUDNN_TUNE=tune)
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *spec.split(), "2", "8"],
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert "exact True" in out.stdout, out.stdout + out.stderr

@@ -126,6 +126,14 @@ ucudnnStatus_t ucudnnSetTotalWorkspaceLimit(UcudnnHandle_t h, int64_t bytes);
 ucudnnStatus_t ucudnnSetCostDatabase(UcudnnHandle_t h, const char* csv_path);
 ucudnnStatus_t ucudnnFlushCostDatabase(UcudnnHandle_t h);
 ucudnnStatus_t ucudnnSetBenchmarkIterations(UcudnnHandle_t h, int warmup, int iters);
+/* Parallel benchmarking ("evaluate in parallel on multiple
+ * GPUs"): the missing (algorithm x micro-batch) rows
+ * of a kernel are timed by one host thread per listed device, each with its own
+ * stream, scratch and L2-flush buffer, then merged into the cost table. n = 0
+ * restores the default (the handle's device and stream). Ids are CUDA ordinals;
+ * out of range -> BAD_PARAM. Replaces nothing in the reference (its cost
+ * source is the analytic model or a CSV, cost_provider.hpp:93-106). */
+ucudnnStatus_t ucudnnSetBenchmarkDevices(UcudnnHandle_t h, const int* device_ids, int n);
 
 /* ------------------------------------------------------------ descriptors  */
 ucudnnStatus_t ucudnnCreateTensorDescriptor(ucudnnTensorDescriptor_t* d);

@@ -39,6 +39,7 @@ PROTOTYPES = {
     "ucudnnSetCostDatabase": (C.c_int, [vp, C.c_char_p]),
     "ucudnnFlushCostDatabase": (C.c_int, [vp]),
     "ucudnnSetBenchmarkIterations": (C.c_int, [vp, C.c_int, C.c_int]),
+    "ucudnnSetBenchmarkDevices": (C.c_int, [vp, C.POINTER(C.c_int), C.c_int]),
     "ucudnnCreateTensorDescriptor": (C.c_int, [C.POINTER(vp)]),
     "ucudnnSetTensor4dDescriptor": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ucudnnGetTensor4dDescriptor": (C.c_int, [vp] + [C.POINTER(C.c_int)] * 4),

@@ -174,6 +174,13 @@ class Handle:
     def set_benchmark_iterations(self, warmup: int, iters: int) -> None:
         check(self._l.ucudnnSetBenchmarkIterations(self._h, warmup, iters))
 
+    def set_benchmark_devices(self, device_ids: Sequence[int]) -> None:
+        """Spread the benchmarker's (algorithm x micro-batch) timings over
+        these devices, one host thread each; [] = this
+        handle's device and stream only."""
+        ids = (C.c_int * max(1, len(device_ids)))(*device_ids)
+        check(self._l.ucudnnSetBenchmarkDevices(self._h, ids, len(device_ids)))
+
     def set_database(self, path: str) -> None:
         check(self._l.ucudnnSetCostDatabase(self._h, path.encode()))
 

@@ -2,7 +2,10 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "../kernels/bdscatter.h"
 #include "../kernels/bflsu.h"
@@ -20,6 +23,20 @@ std::atomic<std::uint64_t> g_launches{0};
 }  // namespace
 void count_launch(int n) { g_launches.fetch_add(std::uint64_t(n), std::memory_order_relaxed); }
 std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+cudaError_t set_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (function, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 int tune(const char* key, int dflt) {
   static const std::string env = [] {

@@ -3,7 +3,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <fstream>
 #include <random>
@@ -100,25 +105,51 @@ struct ucudnnContext {
   void* arena = nullptr;
   std::size_t arena_bytes = 0;
 
-  // benchmark scratch
-  float* scratch = nullptr;
-  std::size_t scratch_elems = 0;
-  void* bench_ws = nullptr;
-  std::size_t bench_ws_bytes = 0;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // L2 flush before every timed run (a plan's micro-batches stream their
-  // slices from HBM; timing L2-hot repeats under-costs bandwidth-bound
-  // algorithms). UCUDNN_BENCH_FLUSH_MB, default 256 (> the 126 MB L2); 0 = off.
-  void* flush = nullptr;
-  std::size_t flush_bytes = std::size_t(-1);
+  // Benchmark state of one device: operand scratch, workspace, events and
+  // the L2 flush buffer (a plan's micro-batches stream their slices from
+  // HBM; timing L2-hot repeats under-costs bandwidth-bound algorithms.
+  // UCUDNN_BENCH_FLUSH_MB, default 256 (> the 126 MB L2); 0 = off).
+  struct BenchSlot {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // own stream; the primary slot uses the handle's
+    float* scratch = nullptr;
+    std::size_t scratch_elems = 0;
+    void* ws = nullptr;
+    std::size_t ws_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    void* flush = nullptr;
+    std::size_t flush_bytes = std::size_t(-1);
+    void release() {
+      if (scratch) cudaFree(scratch);
+      if (ws) cudaFree(ws);
+      if (flush) cudaFree(flush);
+      if (ev0) cudaEventDestroy(ev0);
+      if (ev1) cudaEventDestroy(ev1);
+      if (stream) cudaStreamDestroy(stream);
+      *this = BenchSlot{};
+    }
+  };
+  BenchSlot primary;
+  // ucudnnSetBenchmarkDevices: one slot (and host thread) per listed device;
+  // empty = the primary slot on the handle's device and stream
+  std::vector<std::unique_ptr<BenchSlot>> slots;
+
+  void release_slots() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& sl : slots) {
+      cudaSetDevice(sl->device);
+      sl->release();
+    }
+    slots.clear();
+    cudaSetDevice(cur);
+  }
 
   ~ucudnnContext() {
     if (arena) cudaFree(arena);
-    if (scratch) cudaFree(scratch);
-    if (bench_ws) cudaFree(bench_ws);
-    if (flush) cudaFree(flush);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
+    primary.stream = nullptr;  // the handle's stream is the caller's
+    primary.release();
+    release_slots();
   }
 };
 
@@ -164,7 +195,9 @@ std::int64_t algo_ws(int op, const ConvShape& s, int algo, bool* ok) {
   return *ok ? a->workspace(op, s) : 0;
 }
 
-void ensure_scratch(ucudnnContext* h, std::size_t elems) {
+using BenchSlot = ucudnnContext::BenchSlot;
+
+void ensure_scratch(BenchSlot* h, std::size_t elems) {
   if (elems <= h->scratch_elems) return;
   if (h->scratch) cudaFree(h->scratch);
   h->scratch = nullptr;
@@ -182,17 +215,19 @@ void ensure_scratch(ucudnnContext* h, std::size_t elems) {
   }
 }
 
-void ensure_bench_ws(ucudnnContext* h, std::size_t bytes) {
-  if (bytes <= h->bench_ws_bytes) return;
-  if (h->bench_ws) cudaFree(h->bench_ws);
-  h->bench_ws = nullptr;
-  h->bench_ws_bytes = 0;
-  cuda_check(cudaMalloc(&h->bench_ws, bytes), "cudaMalloc(bench workspace)");
-  h->bench_ws_bytes = bytes;
+void ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
+  if (bytes <= h->ws_bytes) return;
+  if (h->ws) cudaFree(h->ws);
+  h->ws = nullptr;
+  h->ws_bytes = 0;
+  cuda_check(cudaMalloc(&h->ws, bytes), "cudaMalloc(bench workspace)");
+  h->ws_bytes = bytes;
 }
 
-// Median CUDA-event time of one algorithm at one micro-batch, in integer ns.
-std::int64_t time_once(ucudnnContext* h, int op, const ConvShape& s, int algo, std::int64_t ws) {
+// Median CUDA-event time of one algorithm at one micro-batch, in integer ns,
+// on `h`'s device and `stream` (the caller has made that device current).
+std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters, int op, const ConvShape& s,
+                       int algo, std::int64_t ws) {
   const AlgoImpl* a = find_algo(algo);
   std::size_t xe = std::size_t(s.x_elems()), ye = std::size_t(s.y_elems()), we = std::size_t(s.w_elems());
   ensure_scratch(h, xe + ye + we + 64);
@@ -211,8 +246,8 @@ std::int64_t time_once(ucudnnContext* h, int op, const ConvShape& s, int algo, s
   }
   // steady-state micro-batch cost: the warm-up prepares the filter operand,
   // timed runs reuse it as the executor does across a plan's micro-batches
-  for (int i = 0; i < std::max(1, h->warmup); ++i)
-    cuda_check(a->run(op, s, ia, ib, out, h->bench_ws, 1.f, 0.f, h->stream, i ? kFilterReady : 0),
+  for (int i = 0; i < std::max(1, warmup); ++i)
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, i ? kFilterReady : 0),
                "benchmark warm-up");
   if (h->flush_bytes == std::size_t(-1)) {
     const char* e = std::getenv("UCUDNN_BENCH_FLUSH_MB");
@@ -220,11 +255,11 @@ std::int64_t time_once(ucudnnContext* h, int op, const ConvShape& s, int algo, s
     if (h->flush_bytes) cuda_check(cudaMalloc(&h->flush, h->flush_bytes), "cudaMalloc(L2 flush buffer)");
   }
   std::vector<float> ms;
-  for (int i = 0; i < std::max(1, h->iters); ++i) {
-    if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, h->stream), "L2 flush");
-    cuda_check(cudaEventRecord(h->ev0, h->stream), "cudaEventRecord");
-    cuda_check(a->run(op, s, ia, ib, out, h->bench_ws, 1.f, 0.f, h->stream, kFilterReady), "benchmark run");
-    cuda_check(cudaEventRecord(h->ev1, h->stream), "cudaEventRecord");
+  for (int i = 0; i < std::max(1, iters); ++i) {
+    if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, stream), "L2 flush");
+    cuda_check(cudaEventRecord(h->ev0, stream), "cudaEventRecord");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kFilterReady), "benchmark run");
+    cuda_check(cudaEventRecord(h->ev1, stream), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(h->ev1), "cudaEventSynchronize");
     float t = 0;
     cuda_check(cudaEventElapsedTime(&t, h->ev0, h->ev1), "cudaEventElapsedTime");
@@ -238,8 +273,19 @@ std::int64_t time_once(ucudnnContext* h, int op, const ConvShape& s, int algo, s
 
 // Fill missing cost rows for every algorithm x admissible micro-batch of a
 // kernel; times are exact decimals of integer nanoseconds.
+// With ucudnnSetBenchmarkDevices the feasible (algorithm, micro-batch) jobs
+// are spread over one host thread per listed device (an atomic job index:
+// PAPER.md:472-473's parallel evaluation); rows are merged into the table
+// after every thread is done, so the table never sees a partial kernel.
 void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   const ConvShape full = shape_of(k);
+  struct Job {
+    CostKey key;
+    ConvShape s;
+    std::int64_t ws;
+    std::int64_t ns = 0;
+  };
+  std::vector<Job> jobs;
   for (std::int64_t b : micro_sizes(policy, k.batch)) {
     for (int algo = 0; algo < algo_count(); ++algo) {
       CostKey key{k.hash(), k.op, algo, b};
@@ -248,16 +294,43 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
       s.N = int(b);
       bool ok = false;
       std::int64_t ws = algo_ws(int(k.op), s, algo, &ok);
-      CostRecord r{key, Ratio(0), 0, false};
-      if (ok) {
-        std::int64_t ns = time_once(h, int(k.op), s, algo, ws);
-        r.time = Ratio(ns, 1000);
-        r.ws = ws;
-        r.feasible = true;
-      }
-      h->table->put(r);
+      if (ok) jobs.push_back(Job{key, s, ws});
+      else h->table->put(CostRecord{key, Ratio(0), 0, false});
     }
   }
+  if (jobs.empty()) return;
+  const int op = int(k.op);
+  if (h->slots.empty()) {
+    for (Job& j : jobs) j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws);
+  } else {
+    std::atomic<std::size_t> next{0};
+    std::exception_ptr err;
+    std::mutex err_mu;
+    std::vector<std::thread> workers;
+    for (auto& slot : h->slots) {
+      BenchSlot* sl = slot.get();
+      workers.emplace_back([&, sl] {
+        try {
+          cuda_check(cudaSetDevice(sl->device), "cudaSetDevice(benchmark device)");
+          if (!sl->stream) cuda_check(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+          for (std::size_t i = next++; i < jobs.size(); i = next++) {
+            {
+              std::lock_guard<std::mutex> lock(err_mu);
+              if (err) return;
+            }
+            Job& j = jobs[i];
+            j.ns = time_once(sl, sl->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws);
+          }
+        } catch (...) {
+          std::lock_guard<std::mutex> lock(err_mu);
+          if (!err) err = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : workers) t.join();
+    if (err) std::rethrow_exception(err);
+  }
+  for (const Job& j : jobs) h->table->put(CostRecord{j.key, Ratio(j.ns, 1000), j.ws, true});
 }
 
 ucudnnContext::Entry& entry_of(ucudnnContext* h, int algo) {
@@ -523,6 +596,25 @@ ucudnnStatus_t ucudnnFlushCostDatabase(UcudnnHandle_t h) {
     return UCUDNN_STATUS_SUCCESS;
   });
 }
+ucudnnStatus_t ucudnnSetBenchmarkDevices(UcudnnHandle_t h, const int* device_ids, int n) {
+  return guarded([&] {
+    require(h && n >= 0 && (n == 0 || device_ids), "bad benchmark device list");
+    std::vector<int> ids(device_ids, device_ids + n);
+    if (n > 0) {
+      int count = 0;
+      cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+      for (int d : ids) require(d >= 0 && d < count, "benchmark device id out of range");
+    }
+    h->release_slots();
+    for (int d : ids) {
+      auto sl = std::make_unique<BenchSlot>();
+      sl->device = d;
+      h->slots.push_back(std::move(sl));
+    }
+    return UCUDNN_STATUS_SUCCESS;
+  });
+}
+
 ucudnnStatus_t ucudnnSetBenchmarkIterations(UcudnnHandle_t h, int warmup, int iters) {
   return guarded([&] {
     require(h && warmup >= 0 && iters >= 1, "bad iteration counts");
@@ -776,7 +868,8 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     std::int64_t ws = algo_ws(int(op), s, algo, &ok);
     *feasible = ok ? 1 : 0;
     *ws_bytes = ws;
-    *time_us = ok ? double(time_once(h, int(op), s, algo, ws)) / 1000.0 : 0.0;
+    *time_us = ok ? double(time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws)) / 1000.0
+                  : 0.0;
     return UCUDNN_STATUS_SUCCESS;
   });
 }

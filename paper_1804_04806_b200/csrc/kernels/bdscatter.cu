@@ -406,12 +406,8 @@ cudaError_t bds_run(const ConvShape& s, const float* dy, const float* w, float* 
   p.fd_S = FastDiv(std::uint32_t(g.S));
   p.fd_sw = FastDiv(std::uint32_t(g.sw));
   p.dbg = tune("bds_dbg", 0);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(bds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 4096);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_smem_attr(reinterpret_cast<const void*>(bds_kernel), kSmemBudget + 4096);
+  if (e != cudaSuccess) return e;
   const int sms = sm_count();
   const int grid = std::max(1, sms / g.n_tiles) * g.n_tiles;
   return launch_pdl(bds_kernel, dim3(grid), dim3(kThreads), g.smem, st, p);

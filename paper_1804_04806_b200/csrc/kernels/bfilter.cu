@@ -748,12 +748,8 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
     const int stage2 = kBM * 128 + ((g.BN / 2 * 128 + 1023) & ~1023);
     p.stages = ring_stages(std::min(tune("bf2_stages", 8), (200 * 1024) / stage2));
     const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
-    static bool attr2 = false;
-    if (!attr2) {
-      e = cudaFuncSetAttribute(bf2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (e != cudaSuccess) return e;
-      attr2 = true;
-    }
+    e = set_smem_attr(reinterpret_cast<const void*>(bf2_kernel), 227 * 1024);
+    if (e != cudaSuccess) return e;
     count_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * std::min(sms / 2, p.tiles * p.splits));
@@ -782,12 +778,8 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   const int stage_bytes = kSub * (kBM * 128 + ((g.BN * 128 + 1023) & ~1023));
   p.stages = ring_stages(std::min(tune("bf_stages", 8), (200 * 1024) / stage_bytes));
   const int smem = std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(bf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);  // + 1 KB static offtab
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_smem_attr(reinterpret_cast<const void*>(bf_kernel), 220 * 1024);  // + 1 KB static offtab
+  if (e != cudaSuccess) return e;
   e = launch_pdl(bf_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(kThreads), std::size_t(smem), st, xmap, dmap,
                  p);
   if (e != cudaSuccess) return e;

@@ -746,14 +746,10 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   // of x (AlexNet conv3-5 at 256 images: 8 stages 282/312/208 us, 4 stages
   // 249/265/175 us)
   const int smem = p.stages * stage_bytes + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    // + 2 KB static xtab
-    e = cudaFuncSetAttribute(bfl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(bfl2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // + 2 KB static xtab
+  e = set_smem_attr(reinterpret_cast<const void*>(bfl_kernel), 220 * 1024);
+  if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfl2_kernel), 220 * 1024);
+  if (e != cudaSuccess) return e;
   if (g.two) {
     count_launch();
     cudaLaunchConfig_t cfg{};

@@ -611,13 +611,9 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   const int stage_bytes = ((4 * g.msub + g.BN / (g.two ? 64 : 32)) * g.px * 128 + 1023) & ~1023;
   p.stages = std::max(2, std::min({kMaxStages, tune("bfn_stages", 8), (200 * 1024) / stage_bytes}));
   const int smem = p.stages * stage_bytes + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(bfn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(bfn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_smem_attr(reinterpret_cast<const void*>(bfn_kernel), 220 * 1024);
+  if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfn2_kernel), 220 * 1024);
+  if (e != cudaSuccess) return e;
   const int units = p.tiles * p.splits;
   if (g.two) {
     count_launch();

@@ -1,6 +1,8 @@
 // Shapes and launch parameters shared by host launchers and device kernels.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 #ifdef __CUDACC__
@@ -14,6 +16,13 @@ namespace ucudnn {
 // Experiment knob: integer `key` from UCUDNN_TUNE="key=v,key=v" (parsed
 // once), else `dflt`. Only used for A/B timing of pipeline parameters.
 int tune(const char* key, int dflt);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `func` on the
+// calling thread's current device, once per (function, device): function
+// attributes belong to a device context, and the benchmarker may time
+// algorithms on several devices from several host threads at once
+// (ucudnnSetBenchmarkDevices). Thread-safe. Returns the CUDA error, if any.
+cudaError_t set_smem_attr(const void* func, int bytes);
 
 // Host-side count of device kernels this library has launched (evidence for
 // bench.py's gpu_launches; see ucudnnGetLaunchCount).

@@ -319,13 +319,9 @@ int out_smem(const FGeo& g) { return (2 * kOT * g.nf + g.F) * 4; }
 template <int F>
 cudaError_t launch(const FGeo& g, const float* a, const float* b, float* U, float* V, float* Yf, float* out,
                    float alpha, float beta, cudaStream_t st, int flags) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fft_output<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(fft_input<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(fft_filter<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(fft_output<F>), 200 * 1024);
+  set_smem_attr(reinterpret_cast<const void*>(fft_input<F>), 200 * 1024);
+  set_smem_attr(reinterpret_cast<const void*>(fft_filter<F>), 200 * 1024);
   // grid y covers the padded channels too, so their A / B columns are written
   // as zeros (garbage there would poison the GEMM); padded rows only feed
   // outputs that are never read

@@ -437,11 +437,9 @@ cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, floa
   g.o_bs = o_bs;
   const int stage = kBM * 128 + ((q.BN * 128 + 127) & ~127);
   const int smem = std::max(kStages * stage + 1024 + 256, 116 * 1024);
-  static int smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(tiled_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (smem > 48 * 1024) {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(tiled_gemm_kernel), 227 * 1024);
     if (e != cudaSuccess) return e;
-    smem_set = 227 * 1024;
   }
   count_launch();
   tiled_gemm_kernel<<<std::min(std::int64_t(sms()), std::int64_t(tiles) * g.splits * batch), kThreads, smem, st>>>(g);

@@ -385,12 +385,8 @@ cudaError_t launch(int op, IgemmParams p, int grid_x, int grid_y, int grid_z, cu
   const int smem = int(p.stage_bytes) * stages + fixed;
   void (*kern)(IgemmParams) = op == kFwd ? igemm_kernel<kFwd> : op == kBwdData ? igemm_kernel<kBwdData>
                                                                                 : igemm_kernel<kBwdFilter>;
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[op]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[op] = true;
-  }
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
   count_launch();
   kern<<<dim3(grid_x, grid_y, grid_z), kThreads, smem, stream>>>(p);
   return cudaGetLastError();

@@ -1225,12 +1225,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   }
   const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_smem_attr(reinterpret_cast<const void*>(strip_kernel), 227 * 1024);
+  if (e != cudaSuccess) return e;
   return launch_pdl(strip_kernel, dim3(std::min(sm_count(), p.m_tiles * p.n_tiles)), dim3(kThreads),
                     std::size_t(std::max(smem, 116 * 1024)), st, xmap, p);
 }
@@ -1355,12 +1351,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     const int stage2 = p.ksub * (kBM * 128 + ((BN / 2 * 128 + 1023) & ~1023));
     p.stages = ring_stages(std::min(tune("pc2_stages", 8), (200 * 1024) / stage2));
     const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
-    static bool attr2 = false;
-    if (!attr2) {
-      e = cudaFuncSetAttribute(precomp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (e != cudaSuccess) return e;
-      attr2 = true;
-    }
+    e = set_smem_attr(reinterpret_cast<const void*>(precomp2_kernel), 227 * 1024);
+    if (e != cudaSuccess) return e;
     const int clusters = std::min(sm_count() / 2, p.m_tiles * p.n_tiles);
     count_launch();
     cudaLaunchConfig_t cfg{};
@@ -1392,11 +1384,9 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   // 512 TMEM columns)
   const int smem = p.cps == 2 ? p.stages * stage_bytes + 1024 + 256
                               : std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
-  static int smem_set = 0;
-  if (smem > smem_set) {
-    e = cudaFuncSetAttribute(precomp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (smem > 48 * 1024) {
+    e = set_smem_attr(reinterpret_cast<const void*>(precomp_kernel), 227 * 1024);
     if (e != cudaSuccess) return e;
-    smem_set = 227 * 1024;
   }
   const int grid = std::min(p.cps * sm_count(), p.m_tiles * p.n_tiles);
   return launch_pdl(precomp_kernel, dim3(grid), dim3(kThreads), std::size_t(smem), st, amap, p);

@@ -69,3 +69,13 @@ def test_create_without_gpu_fails_cleanly():
     h = C.c_void_p()
     st = lib().ucudnnCreate(C.byref(h))
     assert st == 8  # EXECUTION_FAILED: no CUDA device
+
+
+def test_benchmark_devices_rejects_bad_arguments_without_gpu():
+    """ucudnnSetBenchmarkDevices validates before touching CUDA: a null
+    handle, a negative count, or a null list with n > 0 is BAD_PARAM."""
+    f = lib().ucudnnSetBenchmarkDevices
+    ids = (C.c_int * 2)(0, 1)
+    assert f(None, ids, 2) == 3
+    assert f(None, None, 1) == 3
+    assert f(None, ids, -1) == 3

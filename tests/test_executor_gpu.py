@@ -86,3 +86,32 @@ def test_wr_plan_respects_workspace_limit(cuda):
             a = h.get_algorithm(op, s, limit)
             assert h.workspace_size(a, op, s) <= limit
             assert sum(b for _, b in h.plan(a)) == s.N
+
+
+def test_parallel_benchmark_devices(cuda, tmp_path):
+    """ucudnnSetBenchmarkDevices: two benchmark slots (host threads with their
+    own streams and scratch; both on device 0 here, the only GPU) fill the
+    same cost rows as the sequential benchmarker -- same keys, same
+    feasibility and workspace columns -- and the plan they feed runs exactly."""
+    import csv
+    s = ConvShape(8, 16, 12, 12, 32, 3, 3, 1, 1, 1, 1)
+    tables = []
+    for devs in ([], [0, 0]):
+        db = tmp_path / f"t{len(devs)}.csv"
+        h = Handle(policy="all", database=str(db))
+        h.set_benchmark_devices(devs)
+        algos = [h.get_algorithm(op, s, 1 << 26) for op in (0, 1, 2)]
+        h.flush_database()
+        rows = list(csv.DictReader(open(db)))
+        tables.append({(r["kernel_hash"], r["op_type"], r["algorithm"], r["micro_batch"]):
+                       (r["feasible"], r["workspace_bytes"]) for r in rows})
+        rng = np.random.default_rng(5)
+        for op, algo in enumerate(algos):
+            a, b = inputs_for(op, s, rng, integer=True)
+            out = torch.zeros(out_shape(op, s), device=cuda)
+            ws = torch.empty(max(h.workspace_size(algo, op, s), 4) // 4 + 1, device=cuda)
+            h.run(op, s, torch.from_numpy(a).float().to(cuda), torch.from_numpy(b).float().to(cuda), out, algo, ws)
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().double().numpy(), conv_ref(op, s, a, b))
+        h.close()
+    assert tables[0] == tables[1] and len(tables[0]) == 3 * 8 * 9

@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a replayed CUDA graph")
     ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
+    ap.add_argument("--bf-stream", type=int, default=1,
+                    help="1: each BackwardFilter on a side stream, overlapping the BackwardData chain (both arms)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cores = os.cpu_count() or 1
@@ -261,18 +263,21 @@ def main():
     need = max(base.workspace_size(a, op, stack.layers[i].shape) for (i, op), a in base_stack_algos.items())
     if need // 4 + 64 > stack.ws.numel():
         stack.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
+        stack.ws_bf = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
 
     comm = torch.distributed.group.WORLD if dist_on else None
     comm_stream = torch.cuda.Stream(dev) if dist_on else None
 
+    bf_stream = torch.cuda.Stream(dev) if args.bf_stream else None
+
     def step_ours():
-        stack.step(h, comm, comm_stream)
+        stack.step(h, comm, comm_stream, bf_stream=bf_stream)
 
     ours_algos = stack.algos
 
     def step_base():
         stack.algos = base_stack_algos
-        stack.step(base, comm, comm_stream)
+        stack.step(base, comm, comm_stream, bf_stream=bf_stream)
         stack.algos = ours_algos
 
     # One process per GPU with no collective inside the step (N = 1): capture
@@ -365,14 +370,14 @@ def main():
         cur.wait_event(ready)
         nxt = prefetch(k + 1)
 
-        def on_dw(i):
+        def on_dw(i, st):
             ev = torch.cuda.Event()
-            ev.record(cur)
+            ev.record(st)
             d2h_stream.wait_event(ev)
             with torch.cuda.stream(d2h_stream):
                 dw_host[i].copy_(stack.t[i]["dw"], non_blocking=True)
 
-        stack.step(h, comm, comm_stream, on_dw=None if comm is not None else on_dw)
+        stack.step(h, comm, comm_stream, on_dw=None if comm is not None else on_dw, bf_stream=bf_stream)
         if comm is not None:
             for d, t in zip(dw_host, stack.t):
                 d.copy_(t["dw"], non_blocking=True)
@@ -409,7 +414,9 @@ def main():
                        "ws_limit_bytes": limit, "mode": args.mode, "policy": args.policy,
                        "total_workspace_bytes": args.total_mib * MiB if args.mode == "wd" else None,
                        "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)",
-                       "launch": "eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls"},
+                       "launch": ("eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls")
+                       + ("; BackwardFilter on a side stream overlapping the BackwardData chain (BF_i after BD_i+1)"
+                          if args.bf_stream else "; one stream")},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
                          "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                          "frac": round(dom_tflops / peak, 3), "traffic": traffic,

@@ -93,6 +93,7 @@ class ConvStack:
                                dw=torch.empty_like(w)))
         self.algos = None
         self.ws = None
+        self.ws_bf = None  # BackwardFilter workspace when BF runs on a side stream
 
     def kernels(self):
         """(layer index, op) in the reference's expand order: F, BD, BF per layer."""
@@ -110,6 +111,7 @@ class ConvStack:
             self.algos[(i, op)] = a
             need = max(need, h.workspace_size(a, op, self.layers[i].shape))
         self.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=self.device)
+        self.ws_bf = torch.empty(need // 4 + 64, dtype=torch.float32, device=self.device)
         return self.algos
 
     def run_kernel(self, h: Handle, i: int, op: int):
@@ -121,34 +123,67 @@ class ConvStack:
         else:
             h.backward_filter(s, t["x"], t["dy"], t["dw"], a, self.ws)
 
-    def step(self, h: Handle, comm=None, comm_stream=None, events=None, on_backward=None, on_dw=None):
+    def step(self, h: Handle, comm=None, comm_stream=None, events=None, on_backward=None, on_dw=None,
+             bf_stream=None):
         """One training step of the conv stack. `comm`: torch.distributed group
         (dw all-reduce on `comm_stream`); `events`: optional dict (i, op) ->
         (start, end) CUDA events recorded around each kernel; `on_backward()`
-        runs before the first backward kernel is issued and `on_dw(i)` after
-        layer i's BackwardFilter (hooks for overlapping host copies)."""
+        runs before the first backward kernel is issued and `on_dw(i, stream)`
+        after layer i's BackwardFilter was issued on `stream` (hooks for
+        overlapping host copies).
+
+        `bf_stream` (concurrent kernels): each BackwardFilter runs
+        on this side stream with its own workspace (`ws_bf`), overlapping the
+        BackwardData chain. The order honours a real network's data flow:
+        BF_i needs dy_i, which BD_{i+1} produces, so BF_i waits for BD_{i+1}
+        (the top layer's for the forward pass and the incoming gradient);
+        BD_i runs right after BD_{i+1} on the main stream; the step joins the
+        side stream at its end."""
         cur = torch.cuda.current_stream(self.device)
         n = len(self.layers)
-        order = [(i, FORWARD) for i in range(n)]
-        for i in reversed(range(n)):
-            order += [(i, BACKWARD_DATA), (i, BACKWARD_FILTER)]
         pending = []
-        for i, op in order:
-            if op == BACKWARD_DATA and i == n - 1 and on_backward is not None:
-                on_backward()
-            if events is not None:
-                events[(i, op)][0].record(cur)
-            self.run_kernel(h, i, op)
-            if events is not None:
-                events[(i, op)][1].record(cur)
-            if op == BACKWARD_FILTER and on_dw is not None and comm is None:
-                on_dw(i)
-            if op == BACKWARD_FILTER and comm is not None:
+
+        def after_bf(i, st):
+            if on_dw is not None and comm is None:
+                on_dw(i, st)
+            if comm is not None:
                 ev = torch.cuda.Event()
-                ev.record(cur)
+                ev.record(st)
                 comm_stream.wait_event(ev)
                 with torch.cuda.stream(comm_stream):
                     pending.append(torch.distributed.all_reduce(self.t[i]["dw"], group=comm, async_op=True))
+
+        def run(i, op, st):
+            if events is not None:
+                events[(i, op)][0].record(st)
+            self.run_kernel(h, i, op)
+            if events is not None:
+                events[(i, op)][1].record(st)
+
+        for i in range(n):
+            run(i, FORWARD, cur)
+        if on_backward is not None:
+            on_backward()
+        if bf_stream is None:
+            for i in reversed(range(n)):
+                run(i, BACKWARD_DATA, cur)
+                run(i, BACKWARD_FILTER, cur)
+                after_bf(i, cur)
+        else:
+            for i in reversed(range(n)):
+                ready = torch.cuda.Event()
+                ready.record(cur)  # dy_i is available (forward done / BD_{i+1} done)
+                run(i, BACKWARD_DATA, cur)
+                bf_stream.wait_event(ready)
+                h.set_stream(bf_stream.cuda_stream)
+                ws, self.ws = self.ws, self.ws_bf
+                try:
+                    run(i, BACKWARD_FILTER, bf_stream)
+                finally:
+                    self.ws = ws
+                    h.set_stream(cur.cuda_stream)
+                after_bf(i, bf_stream)
+            cur.wait_stream(bf_stream)
         if comm is not None:
             for p in pending:
                 p.wait()  # makes the current stream wait for the NCCL work

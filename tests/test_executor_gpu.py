@@ -129,6 +129,12 @@ def test_side_stream_backward_filter_matches_serial(cuda, tmp_path):
                    "layer c2 channels=32 size=12x12 filters=64 kernel=3x3 pad=1 stride=1\n"
                    "layer c3 channels=64 size=12x12 filters=64 kernel=3x3 pad=1 stride=1\n")
     stack = ConvStack(str(net), 8, cuda)
+    # integer data: exact in TF32 and in any fp32 summation order, so the
+    # split-K RED epilogues cannot make the two schedules differ
+    gen = torch.Generator(device="cpu").manual_seed(11)
+    for t in stack.t:
+        for k in ("x", "w", "dy"):
+            t[k].copy_(torch.randint(-3, 4, t[k].shape, generator=gen).float())
     h = Handle(policy="powerOfTwo", database=str(tmp_path / "db.csv"))
     stack.plan(h, 1 << 24)
     stack.step(h)

@@ -109,8 +109,8 @@ cudaError_t sliced_run(int op, const ConvShape& s, const float* a, const float* 
 bool nhwc_supports(int op, const ConvShape& s) { return op == 2 && bfn_supports(s); }
 std::int64_t nhwc_workspace(int op, const ConvShape& s) { return op == 2 ? bfn_workspace(s) : 0; }
 cudaError_t nhwc_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
-                     float beta, cudaStream_t st, int) {
-  if (op == 2) return bfn_run(s, a, b, out, ws, alpha, beta, st);
+                     float beta, cudaStream_t st, int flags) {
+  if (op == 2) return bfn_run(s, a, b, out, ws, alpha, beta, st, flags);
   return cudaErrorInvalidValue;
 }
 
@@ -122,7 +122,7 @@ const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 const AlgoImpl kGather{6, "IMPLICIT_GATHER_GEMM", gather_supports, gather_workspace, gather_run};
 const AlgoImpl kSliced{7, "IMPLICIT_PRECOMP_GEMM_SLICED", sliced_supports, sliced_workspace, sliced_run};
-const AlgoImpl kNhwc{8, "IMPLICIT_PRECOMP_GEMM_NHWC", nhwc_supports, nhwc_workspace, nhwc_run};
+const AlgoImpl kNhwc{8, "IMPLICIT_PRECOMP_GEMM_NHWC", nhwc_supports, nhwc_workspace, nhwc_run, 1 << 2};
 
 }  // namespace
 

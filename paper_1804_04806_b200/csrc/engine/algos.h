@@ -25,6 +25,8 @@ struct AlgoImpl {
   // filter operand at the start of `ws`, so it is not re-packed.
   cudaError_t (*run)(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws,
                      float alpha, float beta, cudaStream_t stream, int flags);
+  // bit `op` set: run() honours kAccumulate / kDeferFinal for that op
+  int defer_ops = 0;
 };
 
 // nullptr for ids that are reserved / not built.

@@ -392,22 +392,34 @@ void execute(ucudnnContext* h, int op, const ConvShape& full, const Plan& plan, 
   const std::int64_t x_ss = std::int64_t(full.C) * full.H * full.W;
   const std::int64_t y_ss = std::int64_t(full.K) * full.OH() * full.OW();
   std::int64_t off = 0;
-  bool first = true;
-  int prev_alg = -1;
-  for (const Micro& m : plan.micros()) {
+  const std::vector<Micro>& ms = plan.micros();
+  float run_beta = beta;  // BF: beta of the current same-algorithm run (user beta if it starts the call)
+  for (std::size_t i = 0; i < ms.size(); ++i) {
+    const Micro& m = ms[i];
     const AlgoImpl* impl = find_algo(m.alg);
     require(impl != nullptr, "plan uses an algorithm this build does not provide");
     ConvShape s = full;
     s.N = int(m.batch);
     cudaError_t e;
-    const int flags = m.alg == prev_alg ? kFilterReady : 0;
+    const bool same_prev = i > 0 && ms[i - 1].alg == m.alg, same_next = i + 1 < ms.size() && ms[i + 1].alg == m.alg;
+    int flags = same_prev ? kFilterReady : 0;
     if (op == 0) e = impl->run(0, s, a + off * x_ss, b, out + off * y_ss, ws, alpha, beta, h->stream, flags);
     else if (op == 1) e = impl->run(1, s, a + off * y_ss, b, out + off * x_ss, ws, alpha, beta, h->stream, flags);
-    else e = impl->run(2, s, a + off * x_ss, b + off * y_ss, out, ws, alpha, first ? beta : 1.f, h->stream, flags);
+    else {
+      // user beta on the first micro-batch, 1 afterwards (the reference's
+      // accumulate-into, reference_conv.hpp:257-274); an algorithm that
+      // defers its finalize over a run applies the run's starting beta once
+      float b_m = i == 0 ? beta : 1.f;
+      if (impl->defer_ops & (1 << 2)) {
+        if (!same_prev) run_beta = b_m;
+        b_m = run_beta;
+        if (same_prev) flags |= kAccumulate;
+        if (same_next) flags |= kDeferFinal;
+      }
+      e = impl->run(2, s, a + off * x_ss, b + off * y_ss, out, ws, alpha, b_m, h->stream, flags);
+    }
     cuda_check(e, "kernel launch");
     off += m.batch;
-    first = false;
-    prev_alg = m.alg;
   }
 }
 

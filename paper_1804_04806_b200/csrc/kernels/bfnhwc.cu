@@ -546,12 +546,15 @@ std::int64_t bfn_workspace(const ConvShape& s) {
 }
 
 cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
-                    float beta, cudaStream_t st) {
+                    float beta, cudaStream_t st, int flags) {
   const NGeo g = make_geo(s);
   float* acc = static_cast<float*>(ws);
   float* xn = reinterpret_cast<float*>(static_cast<char*>(ws) + acc_bytes(g));
   float* dyn = reinterpret_cast<float*>(static_cast<char*>(ws) + acc_bytes(g) + x_bytes(g));
-  cudaError_t e = cudaMemsetAsync(acc, 0, std::size_t(g.K) * rows_pad(g) * 4, st);
+  // the [k][row] scratch depends only on the filter shape, so a run of
+  // micro-batches keeps accumulating into it and finalizes once
+  cudaError_t e = cudaSuccess;
+  if (!(flags & kAccumulate)) e = cudaMemsetAsync(acc, 0, std::size_t(g.K) * rows_pad(g) * 4, st);
   if (e != cudaSuccess) return e;
   const int HW = g.H * g.W;
   e = launch_pdl(nhwc_kernel, dim3((HW + 63) / 64, g.Cp / 32, g.N), dim3(256), 0, st, x, xn, g.C, HW, g.Cp);
@@ -634,6 +637,7 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
     e = launch_pdl(bfn_kernel, dim3(std::min(units, sms)), dim3(kThreads), std::size_t(smem), st, xmap, dmap, p);
   }
   if (e != cudaSuccess) return e;
+  if (flags & kDeferFinal) return cudaSuccess;
 
   NFinal f{};
   f.acc = acc;

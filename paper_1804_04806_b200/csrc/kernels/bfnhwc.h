@@ -14,7 +14,8 @@ namespace ucudnn {
 bool bfn_supports(const ConvShape& s);
 std::int64_t bfn_workspace(const ConvShape& s);
 // dw = beta * dw + alpha * sum (split-K, fp32 reductions into a GEMM-layout scratch)
+// flags: kAccumulate / kDeferFinal (conv_common.h) for runs of micro-batches
 cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
-                    cudaStream_t stream);
+                    cudaStream_t stream, int flags = 0);
 
 }  // namespace ucudnn

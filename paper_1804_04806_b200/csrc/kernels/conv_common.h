@@ -69,6 +69,13 @@ struct ConvShape {
 
 enum ConvOp : int { kFwd = 0, kBwdData = 1, kBwdFilter = 2 };
 constexpr int kFilterReady = 1;
+// BackwardFilter runs of consecutive micro-batches on one algorithm that
+// keeps fp32 partial sums in a workspace scratch (AlgoImpl::defer_ops):
+// kAccumulate -- the previous micro-batch of this call left its partial sums
+// there, keep adding (no reset); kDeferFinal -- the next micro-batch continues,
+// skip the scratch -> dW finalize (the last one applies alpha / beta once).
+constexpr int kAccumulate = 2;
+constexpr int kDeferFinal = 4;
 
 // Parameters of one implicit-GEMM launch. GEMM view per op:
 //   Fwd : rows = output pixels (n,oh,ow), cols = K, red = (c,r,s)

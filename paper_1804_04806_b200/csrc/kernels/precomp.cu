@@ -698,9 +698,11 @@ __global__ void pack_filter_kernel(const float* __restrict__ w, float* __restric
                                    PhaseFilter pf, int swz, int ldi) {
   pdl_wait();
   pdl_trigger();
-  // one block per (column tile, k-step): BN rows x 8 16-byte chunks
+  // blockIdx.x = (column tile, k-step): BN rows x 8 16-byte chunks, spread
+  // over gridDim.y blocks (one item per thread: the filter gather is
+  // latency-bound, 50 single blocks took 7-12 us for a 1 MB filter)
   const int nt = blockIdx.x / ksteps, k = blockIdx.x - nt * ksteps;
-  for (int idx = threadIdx.x; idx < 8 * BN; idx += blockDim.x) {
+  for (int idx = threadIdx.x + blockIdx.y * blockDim.x; idx < 8 * BN; idx += blockDim.x * gridDim.y) {
     const int row = idx >> 3, g = idx & 7;  // a row's 8 chunks from 8 adjacent threads: 128 B stores
     const std::int64_t u = (std::int64_t(blockIdx.x) * 8 + g) * BN + row;
     const int o = nt * BN + row;
@@ -1163,7 +1165,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   }
   if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
-    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
+    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps, (8 * BN + 255) / 256), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
                    n_tiles,
                    ksteps, 2, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, 1, g.Cin);
     if (e != cudaSuccess) return e;
@@ -1268,7 +1270,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   }
   if (e != cudaSuccess) return e;
   if (!(flags & kFilterReady)) {
-    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
+    e = launch_pdl(pack_filter_kernel, dim3(n_tiles * ksteps, (8 * BN + 255) / 256), dim3(256), 0, st, w, btiles, g.Nout, g.Cin, taps, BN,
                    n_tiles,
                    ksteps, Cp == 4 ? 1 : 0, Cp / 32, g.s2d ? 3 : g.phase ? 2 : flip, g.pf, two_sm ? 0 : 1,
                    w_ldi ? w_ldi : g.Cin);

@@ -161,3 +161,30 @@ def test_side_stream_backward_filter_matches_serial(cuda, tmp_path):
     for r, t in zip(ref, stack.t):
         assert torch.equal(r["dw"], t["dw"])
     h.close()
+
+
+@pytest.mark.parametrize("case", ["run-then-other", "run-only"])
+def test_bf_deferred_finalize_runs(cuda, tmp_path, case):
+    """Algorithm 8 keeps its fp32 partial sums across a run of consecutive
+    micro-batches of one BackwardFilter call and finalizes once (kAccumulate /
+    kDeferFinal): the run must still apply the user's beta exactly once and
+    hand over to a different algorithm with beta = 1 (forced plans
+    8@2 + 8@2 + 6@1 and 8@2 + 8@2)."""
+    n = 5 if case == "run-then-other" else 4
+    s = ConvShape(n, 32, 7, 7, 48, 3, 3, 1, 1, 1, 1)
+    times = {8: {2: 4, 1: 3}, 6: {1: 2.5}} if n == 5 else {8: {2: 4}}
+    db = tmp_path / "t.csv"
+    db.write_text(forced_table(s, 2, times))
+    h = Handle(policy="all", database=str(db))
+    algo = h.get_algorithm(2, s, 1 << 30)
+    want_plan = [(8, 2), (8, 2), (6, 1)] if n == 5 else [(8, 2), (8, 2)]
+    assert h.plan(algo) == want_plan
+    rng = np.random.default_rng(77)
+    a, b = inputs_for(2, s, rng, integer=True)
+    init = np.random.default_rng(2).integers(-3, 4, size=out_shape(2, s)).astype(np.float64)
+    out = torch.from_numpy(init).float().to(cuda)
+    ws = torch.empty(h.workspace_size(algo, 2, s) // 4 + 1, device=cuda)
+    h.run(2, s, torch.from_numpy(a).float().to(cuda), torch.from_numpy(b).float().to(cuda), out, algo, ws,
+          alpha=2.0, beta=-1.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().double().numpy(), 2.0 * conv_ref(2, s, a, b) - init)

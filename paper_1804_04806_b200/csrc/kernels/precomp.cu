@@ -69,6 +69,7 @@ struct PrecompParams {
   FastDiv fd_blk;  // Ah * Bw * C
   int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
   int stages, ksub, prof, cps;
+  int msub;      // 1-SM kernel: 128-pixel MMA sub-tiles per tile sharing each B (filter) chunk
   FastDiv fd_Cr, fd_ssw;
 };
 
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = std::uint32_t(p.BN) * 128;
-  const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  const int msub = p.msub;
+  const std::uint32_t sub_bytes = msub * a_bytes + ((b_bytes + 1023) & ~1023u);
   const int kSub = p.ksub;
   const std::uint32_t stage_bytes = kSub * sub_bytes;
   const int kStages = p.stages;
@@ -221,36 +223,54 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int mt, nt;
         tile_coords(p, t, mt, nt);
-        // TMA start coordinate of the tile's first output pixel (raster order)
-        std::uint32_t n, pix, oh, ow;
-        p.fd_P.divmod(std::uint32_t(mt * kBM), n, pix);
-        p.fd_OW.divmod(pix, oh, ow);
-        const int cw = int(ow) * p.sw - p.pw, ch = int(oh) * p.sh - p.ph;
+        // TMA start coordinates of each sub-tile's first output pixel (raster order)
+        // (two sub-tiles at most: scalars, not an indexed array -- no stack frame)
+        int cw0, ch0, n0, cw1 = 0, ch1 = 0, n1 = 0;
+        {
+          std::uint32_t n, pix, oh, ow;
+          p.fd_P.divmod(std::uint32_t(mt * msub * kBM), n, pix);
+          p.fd_OW.divmod(pix, oh, ow);
+          cw0 = int(ow) * p.sw - p.pw;
+          ch0 = int(oh) * p.sh - p.ph;
+          n0 = int(n);
+          if (msub == 2) {
+            p.fd_P.divmod(std::uint32_t((mt * 2 + 1) * kBM), n, pix);
+            p.fd_OW.divmod(pix, oh, ow);
+            cw1 = int(ow) * p.sw - p.pw;
+            ch1 = int(oh) * p.sh - p.ph;
+            n1 = int(n);
+          }
+        }
         const float* bsrc = p.btiles + std::size_t(nt) * p.ksteps * (b_bytes / 4);
         for (int j = 0; j < jsteps; ++j, ++it) {
           if ((it % kStages) % nprod != pq) continue;
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
-          mbar_expect_tx(&full[s], nsub * (a_bytes + b_bytes));
+          mbar_expect_tx(&full[s], nsub * (msub * a_bytes + b_bytes));
           for (int sub = 0; sub < nsub; ++sub) {
             const int k = k0 + sub;
-            unsigned char* sa = smem + s * stage_bytes + sub * sub_bytes;
-            if (p.small_c) {
+            for (int m = 0; m < msub; ++m) {
+              unsigned char* sa = smem + s * stage_bytes + sub * sub_bytes + m * a_bytes;
+              const int cwm = m ? cw1 : cw0, chm = m ? ch1 : ch0, nm = m ? n1 : n0;
+              if (p.small_c) {
 #pragma unroll 1
-              for (int g = 0; g < 8; ++g) {
-                int tap = k * 8 + g;
-                if (tap >= p.taps) tap = p.taps - 1;  // its B rows are zero
+                for (int g = 0; g < 8; ++g) {
+                  int tap = k * 8 + g;
+                  if (tap >= p.taps) tap = p.taps - 1;  // its B rows are zero
+                  const int r = tap / p.S, q = tap - r * p.S;
+                  tma_im2col_4d(sa + g * (kBM * 16), &amap, &full[s], 0, cwm, chm, nm, (unsigned short)q,
+                                (unsigned short)r);
+                }
+              } else {
+                const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
                 const int r = tap / p.S, q = tap - r * p.S;
-                tma_im2col_4d(sa + g * (kBM * 16), &amap, &full[s], 0, cw, ch, int(n), (unsigned short)q,
+                tma_im2col_4d(sa, &amap, &full[s], cc * 32, cwm, chm, nm, (unsigned short)q,
                               (unsigned short)r);
               }
-            } else {
-              const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
-              const int r = tap / p.S, q = tap - r * p.S;
-              tma_im2col_4d(sa, &amap, &full[s], cc * 32, cw, ch, int(n), (unsigned short)q, (unsigned short)r);
             }
-            bulk_g2s(sa + a_bytes, bsrc + std::size_t(k) * (b_bytes / 4), b_bytes, &full[s]);
+            bulk_g2s(smem + s * stage_bytes + sub * sub_bytes + msub * a_bytes,
+                     bsrc + std::size_t(k) * (b_bytes / 4), b_bytes, &full[s]);
           }
         }
       }
@@ -279,13 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
         if (lane == 0) {
           for (int sub = 0; sub < nsub; ++sub) {
-            const std::uint32_t sa = sbase + s * stage_bytes + sub * sub_bytes, sb = sa + a_bytes;
+            const std::uint32_t sa0 = sbase + s * stage_bytes + sub * sub_bytes, sb = sa0 + msub * a_bytes;
+            for (int m = 0; m < msub; ++m) {
+              const std::uint32_t sa = sa0 + m * a_bytes;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              std::uint64_t ad = p.small_c ? umma_desc(sa + 2 * q * (kBM * 16), kBM * 16, 128)
-                                           : umma_desc_sw128(sa + q * 32);
-              std::uint64_t bd = umma_desc_sw128(sb + q * 32);
-              mma_tf32(dtm, ad, bd, idesc, ((k0 + sub) | q) != 0);
+              for (int q = 0; q < 4; ++q) {
+                std::uint64_t ad = p.small_c ? umma_desc(sa + 2 * q * (kBM * 16), kBM * 16, 128)
+                                             : umma_desc_sw128(sa + q * 32);
+                std::uint64_t bd = umma_desc_sw128(sb + q * 32);
+                mma_tf32(dtm + std::uint32_t(m * p.BN), ad, bd, idesc, ((k0 + sub) | q) != 0);
+              }
             }
           }
           mma_commit(&empty[s]);
@@ -311,7 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = tl % nacc;
       mbar_wait(&tfull[acc], (tl / nacc) & 1);
       tc_fence_after();
-      const int row = mt * kBM + ew * 32 + lane;
+      for (int m = 0; m < msub; ++m) {
+      const int row = (mt * msub + m) * kBM + ew * 32 + lane;
       const bool ok = row < p.M;
       std::int64_t obase = 0;
       int hb = 0, wb = 0;
@@ -327,7 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           wb = int(j) * p.bp * p.ssw - p.spw;
         }
       }
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc) * acc_cols;
+      const std::uint32_t tbase =
+          tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc) * acc_cols + std::uint32_t(m * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -347,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       std::int64_t(p.P), v);
         }
       }
+      }  // sub-tiles
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -1402,9 +1428,20 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   // its neighbour's MMAs. Measured on AlexNet at 64 images: conv2 BD 196 ->
   // 157 us, conv1 F 151 -> 132, conv3 F 71 -> 63, conv4 BD 89 -> 77; with
   // fewer tiles than SMs it packs them onto fewer SMs and loses (conv4 F).
-  p.cps = tune("pc_cps", p.m_tiles * p.n_tiles > sm_count() ? 2 : 1) == 2 ? 2 : 1;
-  p.ksub = std::max(1, std::min(2, tune("pc_ksub", p.cps == 2 && BN > 128 ? 1 : 2)));
-  const int stage_bytes = p.ksub * (kBM * 128 + ((BN * 128 + 1023) & ~1023));
+  // Narrow filters (BN <= 64), UCUDNN_TUNE=pc_msub=2: two 128-pixel MMA
+  // sub-tiles per tile share each filter chunk, one chunk per stage (still 8
+  // MMAs per commit). Off by default: per 256 images, with two CTAs per SM
+  // (pc_cps=2) it measured AlexNet conv1 F 438 -> 430 us, conv1 BD 504 ->
+  // 496, ResNet l1 F 290 -> 280, but conv2 BD 413 -> 462 and ResNet conv1
+  // BD 1085 -> 1102; with one CTA per SM it lost everywhere
+  p.msub = tune("pc_msub", 1) == 2 && BN <= 64 && p.M > kBM ? 2 : 1;
+  if (p.msub == 2) {
+    p.m_tiles = (p.M + 2 * kBM - 1) / (2 * kBM);
+    p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
+  }
+  p.cps = tune("pc_cps", p.msub == 1 && p.m_tiles * p.n_tiles > sm_count() ? 2 : 1) == 2 ? 2 : 1;
+  p.ksub = std::max(1, std::min(2, tune("pc_ksub", (p.cps == 2 && BN > 128) || p.msub == 2 ? 1 : 2)));
+  const int stage_bytes = p.ksub * (p.msub * kBM * 128 + ((BN * 128 + 1023) & ~1023));
   p.stages = ring_stages(std::min(tune("pc_stages", 8), (p.cps == 2 ? 100 * 1024 : 200 * 1024) / stage_bytes));
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
   // 512 TMEM columns)

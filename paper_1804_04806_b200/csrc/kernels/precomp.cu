@@ -327,10 +327,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     const int ew = warp - 4;
+    // Stride-phase scatter without tapless phases or pair stores: every
+    // column's (a, pb * ssw + b, c) decode depends on the column only, so it
+    // is tabulated once per column tile (the per-element decode -- three fast
+    // divisions -- kept the epilogue behind the MMAs: AlexNet conv1 BD's MMA
+    // warp waited 27 % of its time for a free accumulator)
+    __shared__ int ptab_dh[kMaxBN], ptab_dw[kMaxBN];
+    __shared__ std::int64_t ptab_off[kMaxBN];
+    const bool ptab = p.phase && !p.pair && p.sAh >= p.ssh && p.sBw >= p.ssw;
+    int tab_nt = -1;
     int tl = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       int mt, nt;
       tile_coords(p, t, mt, nt);
+      if (ptab && nt != tab_nt) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done with the table
+        for (int j = ew * 32 + lane; j < p.BN; j += 128) {
+          std::uint32_t col = std::uint32_t(nt * p.BN + j), pb = 0, rem = col;
+          if (p.bp > 1) p.fd_blk.divmod(col, pb, rem);
+          std::uint32_t ab, c, a, b;
+          p.fd_Cr.divmod(rem, ab, c);
+          p.fd_ssw.divmod(ab, a, b);
+          ptab_dh[j] = int(a);
+          ptab_dw[j] = int(pb) * p.ssw + int(b);
+          ptab_off[j] = std::int64_t(c) * p.Hr * p.Wr;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        tab_nt = nt;
+      }
       const int acc = tl % nacc;
       mbar_wait(&tfull[acc], (tl / nacc) & 1);
       tc_fence_after();
@@ -357,6 +381,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
         if (!ok) continue;
+        if (ptab) {
+          const int nv = min(32, min(p.BN - c0, p.Nout - nt * p.BN - c0));
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            if (j >= nv) break;
+            const int h = hb + ptab_dh[c0 + j], w = wb + ptab_dw[c0 + j];
+            if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) continue;
+            float* dst = p.out + obase + ptab_off[c0 + j] + std::int64_t(h) * p.Wr + w;
+            *dst = p.beta == 0.f ? p.alpha * v[j] : p.alpha * v[j] + p.beta * *dst;
+          }
+          continue;
+        }
         if (p.phase) {
 #pragma unroll 4
           for (int j = 0; j < 32; ++j) {
@@ -1448,7 +1484,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
   const int smem = p.cps == 2 ? p.stages * stage_bytes + 1024 + 256
                               : std::max(p.stages * stage_bytes + 1024 + 256, 116 * 1024);
   if (smem > 48 * 1024) {
-    e = set_smem_attr(reinterpret_cast<const void*>(precomp_kernel), 227 * 1024);
+    // dynamic <= ~202 KB; the cap leaves room for the 5 KB of static tables
+    e = set_smem_attr(reinterpret_cast<const void*>(precomp_kernel), 216 * 1024);
     if (e != cudaSuccess) return e;
   }
   const int grid = std::min(p.cps * sm_count(), p.m_tiles * p.n_tiles);

@@ -196,8 +196,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a replayed CUDA graph")
     ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
-    ap.add_argument("--bf-stream", type=int, default=1,
-                    help="1: each BackwardFilter on a side stream, overlapping the BackwardData chain (both arms)")
+    ap.add_argument("--bf-stream", type=int, default=2,
+                    help="k >= 1: each BackwardFilter on one of k side streams (BF_i on stream i % k), "
+                         "overlapping the BackwardData chain (both arms); 0: one stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cores = os.cpu_count() or 1
@@ -264,11 +265,12 @@ def main():
     if need // 4 + 64 > stack.ws.numel():
         stack.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
         stack.ws_bf = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
+        stack.ws_bf_extra = []
 
     comm = torch.distributed.group.WORLD if dist_on else None
     comm_stream = torch.cuda.Stream(dev) if dist_on else None
 
-    bf_stream = torch.cuda.Stream(dev) if args.bf_stream else None
+    bf_stream = [torch.cuda.Stream(dev) for _ in range(args.bf_stream)] if args.bf_stream else None
 
     def step_ours():
         stack.step(h, comm, comm_stream, bf_stream=bf_stream)
@@ -470,7 +472,8 @@ def main():
                        "total_workspace_bytes": args.total_mib * MiB if args.mode == "wd" else None,
                        "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)",
                        "launch": ("eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls")
-                       + ("; BackwardFilter on a side stream overlapping the BackwardData chain (BF_i after BD_i+1)"
+                       + (f"; BackwardFilter on {args.bf_stream} side stream(s) (BF_i on stream i % "
+                          f"{args.bf_stream}, after BD_i+1) overlapping the BackwardData chain"
                           if args.bf_stream else "; one stream")},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
                          "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",

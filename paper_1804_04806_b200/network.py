@@ -94,6 +94,7 @@ class ConvStack:
         self.algos = None
         self.ws = None
         self.ws_bf = None  # BackwardFilter workspace when BF runs on a side stream
+        self.ws_bf_extra = []  # one more per additional side stream
 
     def kernels(self):
         """(layer index, op) in the reference's expand order: F, BD, BF per layer."""
@@ -170,20 +171,29 @@ class ConvStack:
                 run(i, BACKWARD_FILTER, cur)
                 after_bf(i, cur)
         else:
+            # a list of side streams: BF_i on streams[i % len], each with its
+            # own workspace, so a BF whose dy is ready need not queue behind
+            # the previous layer's BF
+            sides = list(bf_stream) if isinstance(bf_stream, (list, tuple)) else [bf_stream]
+            while len(self.ws_bf_extra) < len(sides) - 1:
+                self.ws_bf_extra.append(torch.empty_like(self.ws_bf))
+            wss = [self.ws_bf] + self.ws_bf_extra
             for i in reversed(range(n)):
                 ready = torch.cuda.Event()
                 ready.record(cur)  # dy_i is available (forward done / BD_{i+1} done)
                 run(i, BACKWARD_DATA, cur)
-                bf_stream.wait_event(ready)
-                h.set_stream(bf_stream.cuda_stream)
-                ws, self.ws = self.ws, self.ws_bf
+                side = sides[i % len(sides)]
+                side.wait_event(ready)
+                h.set_stream(side.cuda_stream)
+                ws, self.ws = self.ws, wss[i % len(sides)]
                 try:
-                    run(i, BACKWARD_FILTER, bf_stream)
+                    run(i, BACKWARD_FILTER, side)
                 finally:
                     self.ws = ws
                     h.set_stream(cur.cuda_stream)
-                after_bf(i, bf_stream)
-            cur.wait_stream(bf_stream)
+                after_bf(i, side)
+            for side in sides:
+                cur.wait_stream(side)
         if comm is not None:
             for p in pending:
                 p.wait()  # makes the current stream wait for the NCCL work

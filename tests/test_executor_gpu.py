@@ -149,6 +149,12 @@ def test_side_stream_backward_filter_matches_serial(cuda, tmp_path):
     for r, t in zip(ref, stack.t):
         for k in r:
             assert torch.equal(r[k], t[k]), k
+    for t in stack.t:
+        t["dw"].fill_(float("nan"))
+    stack.step(h, bf_stream=[side, torch.cuda.Stream(cuda)])  # BF_i on stream i % 2
+    torch.cuda.synchronize()
+    for r, t in zip(ref, stack.t):
+        assert torch.equal(r["dw"], t["dw"])
     cs = torch.cuda.Stream(cuda)
     h.set_stream(cs.cuda_stream)
     g = torch.cuda.CUDAGraph()

@@ -229,7 +229,10 @@ void ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
 std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters, int op, const ConvShape& s,
                        int algo, std::int64_t ws) {
   const AlgoImpl* a = find_algo(algo);
-  std::size_t xe = std::size_t(s.x_elems()), ye = std::size_t(s.y_elems()), we = std::size_t(s.w_elems());
+  // sub-buffers 256 B aligned, as a framework's allocations are: TMA maps
+  // built on user tensors (dy read in place) need 16 B aligned bases
+  auto al = [](std::size_t e) { return (e + 63) / 64 * 64; };
+  std::size_t xe = al(std::size_t(s.x_elems())), ye = al(std::size_t(s.y_elems())), we = std::size_t(s.w_elems());
   ensure_scratch(h, xe + ye + we + 64);
   ensure_bench_ws(h, std::size_t(std::max<std::int64_t>(ws, 256)));
   float* x = h->scratch;

@@ -693,18 +693,35 @@ __global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__
     // issue-active, ~1000 instructions per warp for AlexNet conv1); padding
     // columns and rows outside the image are zero-filled separately
     const int W4 = d.W >> 2, items = nr * W4, tail = L - d.pw - d.W;
-    for (int idx = threadIdx.x; idx < items; idx += blockDim.x) {
-      const int k = idx / W4, t4 = idx - k * W4;
-      const int c = k / Ah, a = k - c * Ah;
-      const int h = i * d.sh + a - d.ph;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (unsigned(h) < unsigned(d.H))
-        v = __ldg(reinterpret_cast<const float4*>(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W) + t4);
-      float* r = rows + k * Lp + d.pw + 4 * t4;
-      r[0] = v.x;
-      r[1] = v.y;
-      r[2] = v.z;
-      r[3] = v.w;
+    // four float4 loads in flight per thread before their smem stores (a
+    // load -> store loop left one DRAM latency exposed per iteration)
+    constexpr int kU = 4;
+    for (int base = 0; base < items; base += kU * blockDim.x) {
+      float4 v[kU];
+      int dst[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * blockDim.x + threadIdx.x;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[u] = -1;
+        if (idx < items) {
+          const int k = idx / W4, t4 = idx - k * W4;
+          const int c = k / Ah, a = k - c * Ah;
+          const int h = i * d.sh + a - d.ph;
+          if (unsigned(h) < unsigned(d.H))
+            v[u] = __ldg(reinterpret_cast<const float4*>(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W) + t4);
+          dst[u] = k * Lp + d.pw + 4 * t4;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (dst[u] >= 0) {
+          float* r = rows + dst[u];
+          r[0] = v[u].x;
+          r[1] = v[u].y;
+          r[2] = v[u].z;
+          r[3] = v[u].w;
+        }
     }
     const int pads = d.pw + (tail > 0 ? tail : 0);
     for (int idx = threadIdx.x; idx < nr * pads; idx += blockDim.x) {
@@ -1582,6 +1599,14 @@ void precomp_profile(double out[4]) {
     ++n;
   }
   for (int i = 0; i < 4; ++i) out[i] = n ? s[i] / n : 0;
+}
+
+// Space-to-depth copy for the channels-last BackwardFilter (bfnhwc.cu):
+// xs[n][i][j][Cp], channel (a*Bw + b)*C + c = x[n][c][i*sh + a - ph][j*sw + b - pw]
+cudaError_t space_to_depth_nhwc(const float* x, float* out, int N, int C, int H, int W, int sh, int sw, int ph,
+                                int pw, int Ah, int Bw, int Hq, int Wq, int Cp, cudaStream_t st) {
+  const S2D d{C, H, W, sh, sw, ph, pw, Bw, Ah * Bw * C, Hq, Wq, Cp};
+  return launch_s2d(x, out, d, N, st);
 }
 
 bool precomp_supports(int op, const ConvShape& s) {

@@ -23,4 +23,9 @@ cudaError_t precomp_sliced_run(int op, const ConvShape& s, const float* a, const
 
 void precomp_profile(double out[4]);
 
+// x (NCHW) -> xs[n][i][j][Cp], channel (a*Bw + b)*C + c holding
+// x[n][c][i*sh + a - ph][j*sw + b - pw] (zero off the image and for padded channels)
+cudaError_t space_to_depth_nhwc(const float* x, float* out, int N, int C, int H, int W, int sh, int sw, int ph,
+                                int pw, int Ah, int Bw, int Hq, int Wq, int Cp, cudaStream_t st);
+
 }  // namespace ucudnn

@@ -136,14 +136,17 @@ def test_precomp_sliced(cuda, spec):
 @pytest.mark.parametrize("tune", ["", "bfn2=1,bfn_msub=1", "bfn2=1,bfn_msub=2", "bfn2=0,bfn_msub=1", "bfn2=0,bfn_msub=2",
                                   "bfn_px=64", "bfn_dyd=0", "bfn_dyd=0,bfn2=1"])
 @pytest.mark.parametrize("spec", ["2 128 9 9 64 2 2 0 1", "3 64 11 13 96 3 3 1 1", "2 96 7 7 200 5 5 2 1",
-                                  "1 32 6 6 40 1 1 0 1", "3 64 12 12 64 3 3 1 1", "2 32 20 20 80 3 3 1 1"])
+                                  "1 32 6 6 40 1 1 0 1", "3 64 12 12 64 3 3 1 1", "2 32 20 20 80 3 3 1 1",
+                                  # strided layers through the space-to-depth copy
+                                  "2 3 31 31 16 11 11 2 4", "2 3 36 36 70 7 7 3 2", "2 64 14 14 32 1 1 0 2"])
 def test_bf_nhwc_variants(cuda, spec, tune):
     """IMPLICIT_PRECOMP_GEMM_NHWC (algorithm 8) BackwardFilter: the 1-SM
     kernel with one or two MMA sub-tiles per CTA, the CTA-pair kernel, and
     64-pixel ring stages, dy read in place (OH*OW % 4 == 0) or through its
     channels-last copy, forced through UCUDNN_TUNE (read once per process,
     so each runs in a child); bit-exact against the fp64 oracle on integer
-    data (ragged K, N*P or OH*OW not a multiple of 32, rows past R*S*C)."""
+    data (ragged K, N*P or OH*OW not a multiple of 32, rows past R*S*C;
+    strided few-channel and 1x1 layers through the space-to-depth copy)."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, UCUDNN_TUNE=tune)

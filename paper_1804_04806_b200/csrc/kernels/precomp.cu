@@ -676,7 +676,10 @@ __global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__
 // into shared memory, then the [Wq][Cp] output row is written contiguously.
 // The 32 x 32 tile version reads x at stride sw along a warp (4x the sectors
 // for AlexNet conv1: 67 us per 64 images, ~1.4 TB/s).
-__global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d) {
+// MinB = 6: 40 registers, six blocks per SM (the unbounded build used 60,
+// four blocks, for an issue-bound copy)
+template <int MinB>
+__global__ void __launch_bounds__(256, MinB) s2d_rows_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float rows[];  // [c][a][Wq * sw]
@@ -694,23 +697,39 @@ __global__ void __launch_bounds__(256) s2d_rows_kernel(const float* __restrict__
     // columns and rows outside the image are zero-filled separately
     const int W4 = d.W >> 2, items = nr * W4, tail = L - d.pw - d.W;
     // four float4 loads in flight per thread before their smem stores (a
-    // load -> store loop left one DRAM latency exposed per iteration)
+    // load -> store loop left one DRAM latency exposed per iteration); the
+    // row bases come from a per-block table and (row, column) advance by
+    // adds (two integer divisions per item made the copy issue-bound: 73 %
+    // issue-active at ~2.3 TB/s for AlexNet conv1)
+    __shared__ const float4* rowp[16];
+    if (threadIdx.x < nr) {
+      const int c = threadIdx.x / Ah, a = threadIdx.x - c * Ah;
+      const int h = i * d.sh + a - d.ph;
+      rowp[threadIdx.x] = unsigned(h) < unsigned(d.H)
+                              ? reinterpret_cast<const float4*>(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W)
+                              : nullptr;
+    }
+    __syncthreads();
     constexpr int kU = 4;
+    const int dk = blockDim.x / W4, dt = blockDim.x - dk * W4;
+    int k = threadIdx.x / W4, t4 = threadIdx.x - k * W4;
     for (int base = 0; base < items; base += kU * blockDim.x) {
       float4 v[kU];
       int dst[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int idx = base + u * blockDim.x + threadIdx.x;
         v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         dst[u] = -1;
-        if (idx < items) {
-          const int k = idx / W4, t4 = idx - k * W4;
-          const int c = k / Ah, a = k - c * Ah;
-          const int h = i * d.sh + a - d.ph;
-          if (unsigned(h) < unsigned(d.H))
-            v[u] = __ldg(reinterpret_cast<const float4*>(x + ((std::int64_t(n) * d.C + c) * d.H + h) * d.W) + t4);
+        if (k < nr) {
+          const float4* rp = rowp[k];
+          if (rp) v[u] = __ldg(rp + t4);
           dst[u] = k * Lp + d.pw + 4 * t4;
+        }
+        t4 += dt;
+        k += dk;
+        if (t4 >= W4) {
+          t4 -= W4;
+          ++k;
         }
       }
 #pragma unroll
@@ -779,7 +798,8 @@ std::size_t s2d_rows_smem(const S2D& d) {
 cudaError_t launch_s2d(const float* x, float* out, const S2D& d, int N, cudaStream_t st) {
   const std::size_t sm = s2d_rows_smem(d);
   if (sm <= 48 * 1024 && d.Cp % 4 == 0 && 1024 % d.Cp == 0 && d.CC / d.Bw <= 16 && tune("s2d_rows", 1))
-    return launch_pdl(s2d_rows_kernel, dim3(N * d.Hq), dim3(256), sm, st, x, out, d);
+    return tune("s2d_minb", 6) == 6 ? launch_pdl(s2d_rows_kernel<6>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d)
+                                     : launch_pdl(s2d_rows_kernel<1>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d);
   return launch_pdl(s2d_nhwc_kernel, dim3((d.Wq + 31) / 32, (d.Cp + 31) / 32, N * d.Hq), dim3(32, 8), 0, st, x,
                     out, d);
 }

@@ -111,12 +111,23 @@ NGeo make_geo(const ConvShape& s) {
     if (forced == 1 || forced == 2) g.msub = forced;
   }
   g.m_tiles = (g.M + g.msub * pair_rows - 1) / (g.msub * pair_rows);
-  g.px = tune("bfn_px", 32) == 64 ? 64 : 32;
+  // 64-pixel ring stages (more bytes in flight per stage) win for CTA pairs
+  // and for 1-sub-tile, <= 64-column tiles (AlexNet conv4 BF at 128 images
+  // 90.6 -> 83.1 us; conv1 through space-to-depth at 32 images 63 -> 45 us)
+  // and lose with two 128-row sub-tiles (conv3 80 -> 88, conv5 61 -> 66 us,
+  // profiles/r01_bfn_px_sweep.txt); never when two stages would not fit
+  const int px_knob = tune("bfn_px", 0);
+  g.px = px_knob ? (px_knob == 64 ? 64 : 32) : (g.two || (g.msub == 1 && g.BN <= 64)) ? 64 : 32;
+  const int stage64 = ((4 * g.msub + g.BN / (g.two ? 64 : 32)) * 64 * 128 + 1023) & ~1023;
+  if (g.px == 64 && 2 * stage64 + 1280 > 220 * 1024) g.px = 32;
   // dy's NCHW planes are 16 B aligned when OH*OW % 4 == 0: a {32 px, BN k}
   // tiled box of dy then lands as the standard SWIZZLE_128B K-major operand
   // (pixels contiguous), so dy needs no channels-last copy and the
   // workspace holds only x's copy (ResNet l1-l3: 3136 / 784 / 196 pixels)
-  g.dyd = g.P % 4 == 0 && g.px == 32 && tune("bfn_dyd", 1);
+  // (dy in place keeps 32-pixel stages: it saves the dy copy, which the
+  // default prefers over 64-pixel stages; UCUDNN_TUNE=bfn_px=64 forces the copy)
+  g.dyd = g.P % 4 == 0 && px_knob != 64 && tune("bfn_dyd", 1);
+  if (g.dyd) g.px = 32;
   g.spi = (g.P + g.px - 1) / g.px;
   g.steps = g.dyd ? g.N * g.spi : int((std::int64_t(g.N) * g.P + g.px - 1) / g.px);
   return g;

@@ -676,17 +676,26 @@ __global__ void s2d_nhwc_kernel(const float* __restrict__ x, float* __restrict__
 // into shared memory, then the [Wq][Cp] output row is written contiguously.
 // The 32 x 32 tile version reads x at stride sw along a warp (4x the sectors
 // for AlexNet conv1: 67 us per 64 images, ~1.4 TB/s).
+// Per-geometry constants of the row copy, computed on the host: the smem
+// offset of channel cc's (c, a, b) source within a row group (-1: zero
+// channel), so no thread divides (the per-thread decode was ~40 % of the
+// instructions of this issue-bound kernel).
+struct S2DTab {
+  int Ah, Lp;
+  short off[256];
+};
 // MinB = 6: 40 registers, six blocks per SM (the unbounded build used 60,
 // four blocks, for an issue-bound copy)
 template <int MinB>
-__global__ void __launch_bounds__(256, MinB) s2d_rows_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d) {
+__global__ void __launch_bounds__(256, MinB)
+    s2d_rows_kernel(const float* __restrict__ x, float* __restrict__ out, S2D d, const __grid_constant__ S2DTab tab) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float rows[];  // [c][a][Wq * sw]
   const int n = blockIdx.x / d.Hq, i = blockIdx.x - n * d.Hq;
   // odd row pitch: the write phase reads rows (c, a) that differ by whole
   // rows, which would otherwise land on the same banks
-  const int Ah = d.CC / (d.Bw * d.C), L = d.Wq * d.sw, Lp = L | 1;
+  const int Ah = tab.Ah, L = d.Wq * d.sw, Lp = tab.Lp;
   // load: thread t takes column t of all C*Ah (<= 16) rows, every load
   // issued before the first smem store (a loop of load -> store per row
   // exposed one DRAM latency per row: 44 us per 64 AlexNet images)
@@ -772,24 +781,16 @@ __global__ void __launch_bounds__(256, MinB) s2d_rows_kernel(const float* __rest
   __syncthreads();
   // write: each thread owns 4 consecutive channels (one float4 store) for
   // every (256*4/Cp)-th column j; the (a, b, c) decode happens once
-  const int q4 = threadIdx.x % (d.Cp / 4), j0 = threadIdx.x / (d.Cp / 4), js = blockDim.x / (d.Cp / 4);
+  const int c4 = d.Cp >> 2;  // Cp is a power of two here (1024 % Cp == 0)
+  const int q4 = threadIdx.x & (c4 - 1), j0 = threadIdx.x / c4, js = blockDim.x / c4;
   int off[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int cc = 4 * q4 + e;
-    off[e] = -1;
-    if (cc < d.CC) {
-      const int ab = cc / d.C, c = cc - ab * d.C, aa = ab / d.Bw, bb = ab - aa * d.Bw;
-      off[e] = (c * Ah + aa) * Lp + bb;
-    }
-  }
-  float4* o = reinterpret_cast<float4*>(out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp) + q4;
-  for (int j = j0; j < d.Wq; j += js) {
-    const int jo = j * d.sw;
-    o[std::int64_t(j) * (d.Cp / 4)] =
-        make_float4(off[0] >= 0 ? rows[off[0] + jo] : 0.f, off[1] >= 0 ? rows[off[1] + jo] : 0.f,
-                    off[2] >= 0 ? rows[off[2] + jo] : 0.f, off[3] >= 0 ? rows[off[3] + jo] : 0.f);
-  }
+  for (int e = 0; e < 4; ++e) off[e] = tab.off[4 * q4 + e];
+  float4* o = reinterpret_cast<float4*>(out + (std::int64_t(n) * d.Hq + i) * d.Wq * d.Cp) + q4 + j0 * c4;
+  const int ostep = js * c4, jstep = js * d.sw;
+  for (int j = j0, jo = j0 * d.sw; j < d.Wq; j += js, jo += jstep, o += ostep)
+    *o = make_float4(off[0] >= 0 ? rows[off[0] + jo] : 0.f, off[1] >= 0 ? rows[off[1] + jo] : 0.f,
+                     off[2] >= 0 ? rows[off[2] + jo] : 0.f, off[3] >= 0 ? rows[off[3] + jo] : 0.f);
 }
 std::size_t s2d_rows_smem(const S2D& d) {
   return std::size_t(d.CC / (d.Bw * d.C)) * d.C * ((d.Wq * d.sw) | 1) * 4;
@@ -797,9 +798,22 @@ std::size_t s2d_rows_smem(const S2D& d) {
 // space-to-depth launch: the row kernel when its rows fit in 48 KB
 cudaError_t launch_s2d(const float* x, float* out, const S2D& d, int N, cudaStream_t st) {
   const std::size_t sm = s2d_rows_smem(d);
-  if (sm <= 48 * 1024 && d.Cp % 4 == 0 && 1024 % d.Cp == 0 && d.CC / d.Bw <= 16 && tune("s2d_rows", 1))
-    return tune("s2d_minb", 6) == 6 ? launch_pdl(s2d_rows_kernel<6>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d)
-                                     : launch_pdl(s2d_rows_kernel<1>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d);
+  if (sm <= 48 * 1024 && d.Cp % 4 == 0 && 1024 % d.Cp == 0 && d.Cp <= 256 && d.CC / d.Bw <= 16 &&
+      tune("s2d_rows", 1)) {
+    S2DTab tab{};
+    tab.Ah = d.CC / (d.Bw * d.C);
+    tab.Lp = (d.Wq * d.sw) | 1;
+    for (int cc = 0; cc < d.Cp; ++cc) {
+      tab.off[cc] = -1;
+      if (cc < d.CC) {
+        const int ab = cc / d.C, c = cc - ab * d.C, aa = ab / d.Bw, bb = ab - aa * d.Bw;
+        tab.off[cc] = short((c * tab.Ah + aa) * tab.Lp + bb);
+      }
+    }
+    return tune("s2d_minb", 6) == 6
+               ? launch_pdl(s2d_rows_kernel<6>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d, tab)
+               : launch_pdl(s2d_rows_kernel<1>, dim3(N * d.Hq), dim3(256), sm, st, x, out, d, tab);
+  }
   return launch_pdl(s2d_nhwc_kernel, dim3((d.Wq + 31) / 32, (d.Cp + 31) / 32, N * d.Hq), dim3(32, 8), 0, st, x,
                     out, d);
 }

@@ -57,6 +57,16 @@ def test_forced_mixed_plan_matches_oracle(cuda, tmp_path, op):
     assert np.array_equal(out.cpu().double().numpy(), want)
 
 
+def assert_plan_result(h, algo, got, ref):
+    """Bit-exact on integer data unless the timing put a micro-batch on FFT (2)
+    or Winograd F(4x4,3x3) (4): those round in their transforms even on
+    integers and are held to their stated normwise bound (test_algos_gpu.TOL)."""
+    if {alg for alg, _ in h.plan(algo)} & {2, 4}:
+        assert np.linalg.norm(got - ref) <= 1e-2 * np.linalg.norm(ref)
+    else:
+        assert np.array_equal(got, ref)
+
+
 def test_wd_mode_plans_network_and_uses_arena(cuda):
     s = ConvShape(4, 16, 10, 10, 32, 3, 3, 1, 1, 1, 1)
     h = Handle(policy="powerOfTwo", mode="wd", total_workspace=64 << 20)
@@ -72,7 +82,7 @@ def test_wd_mode_plans_network_and_uses_arena(cuda):
         h.run(op, s, ia, ib, outs[op], algos[op])
     torch.cuda.synchronize()
     for op, (ia, ib) in enumerate(((x, w), (dy, w), (x, dy))):
-        assert np.array_equal(outs[op].cpu().double().numpy(), conv_ref(op, s, ia, ib))
+        assert_plan_result(h, algos[op], outs[op].cpu().double().numpy(), conv_ref(op, s, ia, ib))
     rep = h.machine_report()
     assert "mode wd" in rep and "kernel-count 3" in rep and rep.endswith("end\n")
 
@@ -112,7 +122,7 @@ def test_parallel_benchmark_devices(cuda, tmp_path):
             ws = torch.empty(max(h.workspace_size(algo, op, s), 4) // 4 + 1, device=cuda)
             h.run(op, s, torch.from_numpy(a).float().to(cuda), torch.from_numpy(b).float().to(cuda), out, algo, ws)
             torch.cuda.synchronize()
-            assert np.array_equal(out.cpu().double().numpy(), conv_ref(op, s, a, b))
+            assert_plan_result(h, algo, out.cpu().double().numpy(), conv_ref(op, s, a, b))
         h.close()
     assert tables[0] == tables[1] and len(tables[0]) == 3 * 8 * 9
 

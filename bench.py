@@ -35,6 +35,29 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks (one process per GPU, rendezvous on
+    127.0.0.1), exactly as the driver's torchrun launch would."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------ CPU reference arm
 def cpu_reference(net_path: str, sample_n: int, threads: int):
     """The reference fp64 convolution (oracle/_ref/ref_conv.so, compiled from
@@ -75,14 +98,20 @@ def run_reference_arm(args):
     for _ in range(args.steps):
         _, ms, kind = cpu_reference(net, sample_n, threads)
         vals.append(ms)
-    v = statistics.median(vals)
+    # the job's global batch is 256 images per GPU: the host runs all of them
+    v = statistics.median(vals) * world
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/iter", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "AlexNet conv1-5 F+BD+BF, batch 256 (CPU: extrapolated from a "
-                                   f"{sample_n}-sample slice per step)", "net": "alexnet", "global_batch": 256},
+            "config": {"workload": "alexnet conv layers, Forward + BackwardData + BackwardFilter (15 kernels), "
+                                   "batch 256 per GPU", "net": "alexnet", "global_batch": 256 * world,
+                       "ws_limit_bytes": 64 * MiB, "mode": "wr", "policy": "powerOfTwo",
+                       "parallelism": f"dp{world}"},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms/iter", "cores": threads, "kind": kind,
-                             "sample": f"{sample_n} of 256 samples of all 15 kernels per step, x{256 // sample_n}"},
+                             "cpu_model": cpu_model(),
+                             "sample": f"{sample_n} of 256 samples of all 15 kernels per step, "
+                                       f"x{256 // sample_n} (x{world} ranks' shards)" if world > 1 else
+                                       f"{sample_n} of 256 samples of all 15 kernels per step, x{256 // sample_n}"},
             "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -201,6 +230,8 @@ def main():
                          "overlapping the BackwardData chain (both arms); 0: one stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     cores = os.cpu_count() or 1
     args.ref_sample = args.ref_sample or min(64, cores)
     args.cpu_sample = args.cpu_sample or min(64, cores)
@@ -214,7 +245,9 @@ def main():
     from paper_1804_04806_b200.network import ConvStack
 
     rank, world, local = env_rank()
-    dist_on = world > 1
+    # under torchrun (WORLD_SIZE set) the NCCL data-parallel step runs at
+    # every world size, 1 included: the same path the N > 1 runs take
+    dist_on = "WORLD_SIZE" in os.environ
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if dist_on:
@@ -223,7 +256,12 @@ def main():
     net_path = os.path.join(ROOT, "configs", args.net + ".net")
     limit = args.limit_mib * MiB
     stack = ConvStack(net_path, 256, dev)
-    db = args.db or os.path.join(tempfile.gettempdir(), f"ucudnn_bench_{os.getpid()}_{rank}.csv")
+    # one cost-table file per rank: rank 0 benchmarks into `db`, the others
+    # receive its rows through share_cost_table into their own copy (a shared
+    # path would let a non-zero rank truncate rank 0's table mid-flush)
+    db = args.db or os.path.join(tempfile.gettempdir(), f"ucudnn_bench_{os.getpid()}.csv")
+    if rank != 0:
+        db = f"{db}.rank{rank}"
 
     # plan: benchmark every (algorithm x micro-batch) on the device, WR DP
     t0 = time.perf_counter()
@@ -235,8 +273,6 @@ def main():
             stack.plan(h0, limit)
             h0.flush_database()
             h0.close()
-        else:
-            open(db, "w").write("")
         torch.distributed.barrier()
         share_cost_table(db)
     if args.mode == "wd":
@@ -452,6 +488,7 @@ def main():
         if not args.no_cpu:
             sec, cpu_ms, kind = cpu_reference(net_path, args.cpu_sample, os.cpu_count() or 1)
             cpu = {"value": round(cpu_ms, 1), "unit": "ms/iter", "cores": os.cpu_count(), "kind": kind,
+                   "cpu_model": cpu_model(),
                    "sample": f"{args.cpu_sample} of 256 samples of each of the 15 kernels ({sec:.1f} s), "
                              f"x{256 // args.cpu_sample}"}
         total_flops = stack.flops()
@@ -474,7 +511,12 @@ def main():
                        "launch": ("eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls")
                        + (f"; BackwardFilter on {args.bf_stream} side stream(s) (BF_i on stream i % "
                           f"{args.bf_stream}, after BD_i+1) overlapping the BackwardData chain"
-                          if args.bf_stream else "; one stream")},
+                          if args.bf_stream else "; one stream"),
+                       "live_workspaces": (f"{1 + args.bf_stream} caller workspaces of "
+                                           f"{stack.ws.numel() * 4 >> 20} MiB each (main stream + one per "
+                                           "BackwardFilter side stream); each call stays within the per-kernel "
+                                           "limit" if args.mode == "wr" else "library-owned WD arena"),
+                       "comm_size": torch.distributed.get_world_size() if dist_on else 1},
             "roofline": {"bound": "tensor", "kernel": f"{stack.layers[dom[0]].name}/{OP_NAMES[dom[1]]}",
                          "achieved": round(dom_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                          "frac": round(dom_tflops / peak, 3), "traffic": traffic,

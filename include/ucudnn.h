@@ -102,6 +102,13 @@ uint64_t ucudnnGetLaunchCount(void);
 ucudnnStatus_t ucudnnDebugPrecompProfile(double* out4);
 /* Same split for the last IMPLICIT_PRECOMP_GEMM BackwardFilter launch. */
 ucudnnStatus_t ucudnnDebugBackwardFilterProfile(double* out4);
+/* Launch-variant trace (test evidence; no reference counterpart): on != 0
+ * clears and enables a process-wide log in which every main-kernel launch
+ * appends one line naming its variant and tiling ("precomp2 m_tiles=...",
+ * "bfn2 ...", "precomp cps=2 ..."); ucudnnDebugGetTrace copies the log out
+ * (same *len convention as ucudnnGetMachineReport) and clears it. */
+ucudnnStatus_t ucudnnDebugSetTrace(int on);
+ucudnnStatus_t ucudnnDebugGetTrace(char* buf, size_t* len);
 
 /* ------------------------------------------------------------ handle ----- */
 /* Replaces cudnnCreate/cudnnDestroy/cudnnSetStream. The

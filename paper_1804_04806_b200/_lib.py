@@ -29,6 +29,8 @@ PROTOTYPES = {
     "ucudnnGetLaunchCount": (C.c_uint64, []),
     "ucudnnDebugPrecompProfile": (C.c_int, [C.POINTER(C.c_double)]),
     "ucudnnDebugBackwardFilterProfile": (C.c_int, [C.POINTER(C.c_double)]),
+    "ucudnnDebugSetTrace": (C.c_int, [C.c_int]),
+    "ucudnnDebugGetTrace": (C.c_int, [C.c_char_p, C.POINTER(C.c_size_t)]),
     "ucudnnCreate": (C.c_int, [C.POINTER(vp)]),
     "ucudnnDestroy": (C.c_int, [vp]),
     "ucudnnSetStream": (C.c_int, [vp, vp]),

@@ -11,7 +11,7 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
-from ._lib import call_string, check, lib
+from ._lib import UcudnnError, call_string, check, lib
 
 FORWARD, BACKWARD_DATA, BACKWARD_FILTER = 0, 1, 2
 OP_NAMES = {FORWARD: "Forward", BACKWARD_DATA: "BackwardData", BACKWARD_FILTER: "BackwardFilter"}
@@ -57,6 +57,27 @@ class ConvShape:
         return 2.0 * self.N * self.K * self.C * self.R * self.S * self.OH * self.OW
 
 
+def validate_tensor(t, numel: int, name: str, device: Optional[int] = None) -> None:
+    """Reject what would become an out-of-bounds or misread device access
+    before its pointer crosses the ABI: a CUDA float32 contiguous tensor (on
+    the handle's device) with exactly the element count the descriptors
+    imply. Raises UcudnnError(BAD_PARAM), as a descriptor mismatch does."""
+    def bad(msg):
+        raise UcudnnError(3, f"{name}: {msg}")
+    if not hasattr(t, "data_ptr") or not hasattr(t, "is_cuda"):
+        bad("not a tensor")
+    if not t.is_cuda:
+        bad("not a CUDA tensor")
+    if device is not None and t.device.index != device:
+        bad(f"on cuda:{t.device.index}, the handle is on cuda:{device}")
+    if str(t.dtype) != "torch.float32":
+        bad(f"dtype {t.dtype}, expected float32")
+    if not t.is_contiguous():
+        bad("not contiguous (packed NCHW / KCRS expected)")
+    if t.numel() != numel:
+        bad(f"{t.numel()} elements, the descriptor implies {numel}")
+
+
 def _s(x: Optional[str]) -> Optional[bytes]:
     return None if x is None else x.encode()
 
@@ -94,6 +115,16 @@ def canonical_time(text: str) -> str:
 def canonical_cost_table(csv_text: str) -> str:
     """Parse a cost-table CSV and re-emit it sorted / canonical."""
     return call_string(lib().ucudnnCanonicalCostTable, csv_text.encode())
+
+
+def set_trace(on: bool) -> None:
+    """Enable (and clear) the process-wide launch-variant trace."""
+    check(lib().ucudnnDebugSetTrace(1 if on else 0))
+
+
+def take_trace() -> list:
+    """Launch-variant lines logged since the last call (then cleared)."""
+    return [l for l in call_string(lib().ucudnnDebugGetTrace).splitlines() if l]
 
 
 def algorithm_workspace(op: int, s: ConvShape, algo: int, micro_batch: int):
@@ -136,6 +167,8 @@ class Handle:
         self._l = lib()
         self._h = C.c_void_p()
         check(self._l.ucudnnCreate(C.byref(self._h)))
+        import torch
+        self.device = torch.cuda.current_device()
         self._descs = {}
         self.set_policy(policy)
         self.set_mode(mode)
@@ -240,9 +273,19 @@ class Handle:
     def _ws(self, ws):
         if ws is None:
             return None, 0
+        if not getattr(ws, "is_cuda", False) or not ws.is_contiguous() or ws.device.index != self.device:
+            raise UcudnnError(3, "workspace: must be a contiguous CUDA tensor on the handle's device")
         return C.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size()
 
+    def _check(self, s: ConvShape, op: int, a, b, out):
+        x_n, w_n, y_n = s.N * s.C * s.H * s.W, s.K * s.C * s.R * s.S, s.N * s.K * s.OH * s.OW
+        names = [("x", "w", "y"), ("dy", "w", "dx"), ("x", "dy", "dw")][op]
+        sizes = [(x_n, w_n, y_n), (y_n, w_n, x_n), (x_n, y_n, w_n)][op]
+        for t, n, nm in zip((a, b, out), sizes, names):
+            validate_tensor(t, n, nm, self.device)
+
     def forward(self, s: ConvShape, x, w, y, algo: int, ws=None, alpha: float = 1.0, beta: float = 0.0):
+        self._check(s, FORWARD, x, w, y)
         d = self._d(s)
         wp, wn = self._ws(ws)
         a, b = C.c_float(alpha), C.c_float(beta)
@@ -251,6 +294,7 @@ class Handle:
                                                C.c_void_p(y.data_ptr())))
 
     def backward_data(self, s: ConvShape, w, dy, dx, algo: int, ws=None, alpha: float = 1.0, beta: float = 0.0):
+        self._check(s, BACKWARD_DATA, dy, w, dx)
         d = self._d(s)
         wp, wn = self._ws(ws)
         a, b = C.c_float(alpha), C.c_float(beta)
@@ -260,6 +304,7 @@ class Handle:
 
     def backward_filter(self, s: ConvShape, x, dy, dw, algo: int, ws=None, alpha: float = 1.0,
                         beta: float = 0.0):
+        self._check(s, BACKWARD_FILTER, x, dy, dw)
         d = self._d(s)
         wp, wn = self._ws(ws)
         a, b = C.c_float(alpha), C.c_float(beta)

@@ -1,6 +1,8 @@
 #include "algos.h"
 
 #include <atomic>
+#include <cstdarg>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -23,6 +25,34 @@ std::atomic<std::uint64_t> g_launches{0};
 }  // namespace
 void count_launch(int n) { g_launches.fetch_add(std::uint64_t(n), std::memory_order_relaxed); }
 std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+std::atomic<bool> g_trace{false};
+std::mutex g_trace_mu;
+std::string g_trace_buf;
+}  // namespace
+bool trace_on() { return g_trace.load(std::memory_order_relaxed); }
+void trace_variant(const char* fmt, ...) {
+  if (!trace_on()) return;
+  char line[256];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(line, sizeof line, fmt, ap);
+  va_end(ap);
+  std::lock_guard<std::mutex> lock(g_trace_mu);
+  if (g_trace_buf.size() < (1u << 20)) g_trace_buf += std::string(line) + "\n";
+}
+void set_trace(bool on) {
+  std::lock_guard<std::mutex> lock(g_trace_mu);
+  g_trace.store(on);
+  g_trace_buf.clear();
+}
+std::string take_trace() {
+  std::lock_guard<std::mutex> lock(g_trace_mu);
+  std::string s;
+  s.swap(g_trace_buf);
+  return s;
+}
 
 cudaError_t set_smem_attr(const void* func, int bytes) {
   static std::mutex mu;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "../kernels/conv_common.h"
 
@@ -32,5 +33,9 @@ struct AlgoImpl {
 // nullptr for ids that are reserved / not built.
 const AlgoImpl* find_algo(int id);
 int algo_count();  // ids are 0 .. algo_count()-1
+
+// ucudnnDebugSetTrace / ucudnnDebugGetTrace backing (kernels call trace_variant)
+void set_trace(bool on);
+std::string take_trace();
 
 }  // namespace ucudnn

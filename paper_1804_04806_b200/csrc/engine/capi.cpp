@@ -102,6 +102,12 @@ struct ucudnnContext {
   };
   std::vector<Entry> entries;
   bool wd_stale = true;
+  // WD: after the first optimisation the network is known; a repeated
+  // Get*Algorithm for a registered (op, shape) returns its entry instead of
+  // registering another kernel ("a library call after network
+  // initialization, which ignores subsequent cudnnGetConvolution*Algorithm
+  // calls"), so framework re-queries neither grow the ILP nor move the arena
+  bool wd_frozen = false;
   void* arena = nullptr;
   std::size_t arena_bytes = 0;
 
@@ -215,17 +221,26 @@ void ensure_scratch(BenchSlot* h, std::size_t elems) {
   }
 }
 
-void ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
-  if (bytes <= h->ws_bytes) return;
+// false when the device cannot hold the workspace (the row is then recorded
+// infeasible instead of aborting the whole Get*Algorithm)
+bool ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
+  if (bytes <= h->ws_bytes) return true;
   if (h->ws) cudaFree(h->ws);
   h->ws = nullptr;
   h->ws_bytes = 0;
-  cuda_check(cudaMalloc(&h->ws, bytes), "cudaMalloc(bench workspace)");
+  cudaError_t e = cudaMalloc(&h->ws, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();  // clear the sticky-free allocation error
+    return false;
+  }
+  cuda_check(e, "cudaMalloc(bench workspace)");
   h->ws_bytes = bytes;
+  return true;
 }
 
 // Median CUDA-event time of one algorithm at one micro-batch, in integer ns,
-// on `h`'s device and `stream` (the caller has made that device current).
+// on `h`'s device and `stream` (the caller has made that device current);
+// -1 when its workspace does not fit in device memory.
 std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters, int op, const ConvShape& s,
                        int algo, std::int64_t ws) {
   const AlgoImpl* a = find_algo(algo);
@@ -234,7 +249,7 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
   auto al = [](std::size_t e) { return (e + 63) / 64 * 64; };
   std::size_t xe = al(std::size_t(s.x_elems())), ye = al(std::size_t(s.y_elems())), we = std::size_t(s.w_elems());
   ensure_scratch(h, xe + ye + we + 64);
-  ensure_bench_ws(h, std::size_t(std::max<std::int64_t>(ws, 256)));
+  if (!ensure_bench_ws(h, std::size_t(std::max<std::int64_t>(ws, 256)))) return -1;
   float* x = h->scratch;
   float* y = x + xe;
   float* w = y + ye;
@@ -247,11 +262,13 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
   }
-  // steady-state micro-batch cost: the warm-up prepares the filter operand,
-  // timed runs reuse it as the executor does across a plan's micro-batches
+  // every timed run is a whole call, filter packing / transforms included
+  // (each micro-batch is costed as the independent call the reference's
+  // model sums, cost_provider.hpp:117-127; the executor's reuse of a packed
+  // filter across a run of same-algorithm micro-batches is a saving the
+  // table does not claim)
   for (int i = 0; i < std::max(1, warmup); ++i)
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, i ? kFilterReady : 0),
-               "benchmark warm-up");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, 0), "benchmark warm-up");
   if (h->flush_bytes == std::size_t(-1)) {
     const char* e = std::getenv("UCUDNN_BENCH_FLUSH_MB");
     h->flush_bytes = std::size_t(e ? std::max(0, std::atoi(e)) : 256) << 20;
@@ -261,7 +278,7 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
   for (int i = 0; i < std::max(1, iters); ++i) {
     if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, stream), "L2 flush");
     cuda_check(cudaEventRecord(h->ev0, stream), "cudaEventRecord");
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kFilterReady), "benchmark run");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, 0), "benchmark run");
     cuda_check(cudaEventRecord(h->ev1, stream), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(h->ev1), "cudaEventSynchronize");
     float t = 0;
@@ -333,7 +350,8 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
     for (auto& t : workers) t.join();
     if (err) std::rethrow_exception(err);
   }
-  for (const Job& j : jobs) h->table->put(CostRecord{j.key, Ratio(j.ns, 1000), j.ws, true});
+  for (const Job& j : jobs)
+    h->table->put(j.ns < 0 ? CostRecord{j.key, Ratio(0), 0, false} : CostRecord{j.key, Ratio(j.ns, 1000), j.ws, true});
 }
 
 ucudnnContext::Entry& entry_of(ucudnnContext* h, int algo) {
@@ -375,6 +393,10 @@ void plan_wd(ucudnnContext* h) {
     e.arena_offset = off;
     off += (std::size_t(e.plan.ws()) + 255) / 256 * 256;
   }
+  h->wd_frozen = true;
+  // the arena only grows (a re-plan that needs no more keeps its pointer, so
+  // CUDA graphs captured over it stay valid); growing it after capture is
+  // unsupported, as re-registering kernels after capture is
   if (off > h->arena_bytes) {
     if (h->arena) cudaFree(h->arena);
     h->arena = nullptr;
@@ -518,6 +540,15 @@ ucudnnStatus_t ucudnnDebugBackwardFilterProfile(double* out4) {
   return UCUDNN_STATUS_SUCCESS;
 }
 
+ucudnnStatus_t ucudnnDebugSetTrace(int on) {
+  set_trace(on != 0);
+  return UCUDNN_STATUS_SUCCESS;
+}
+
+ucudnnStatus_t ucudnnDebugGetTrace(char* buf, size_t* len) {
+  return guarded([&] { return copy_out(take_trace(), buf, len); });
+}
+
 ucudnnStatus_t ucudnnCreate(UcudnnHandle_t* out) {
   return guarded([&] {
     require(out != nullptr, "null handle pointer");
@@ -572,6 +603,7 @@ ucudnnStatus_t ucudnnSetBatchSizePolicy(UcudnnHandle_t h, ucudnnBatchSizePolicy_
     h->policy = Policy(int(p));
     for (auto& e : h->entries) e.planned = false;
     h->wd_stale = true;
+    h->wd_frozen = false;
     return UCUDNN_STATUS_SUCCESS;
   });
 }
@@ -581,6 +613,7 @@ ucudnnStatus_t ucudnnSetWorkspaceMode(UcudnnHandle_t h, ucudnnWorkspaceMode_t m)
     h->mode = Mode(int(m));
     for (auto& e : h->entries) e.planned = false;
     h->wd_stale = true;
+    h->wd_frozen = false;
     return UCUDNN_STATUS_SUCCESS;
   });
 }
@@ -724,6 +757,11 @@ static ucudnnStatus_t get_algo(UcudnnHandle_t h, Op op, const ConvShape& s, int6
     // WR: a repeated query for the same shape + limit reuses its plan. WD
     // registers every call as its own kernel (replicated layers are selected
     // independently, wd_optimizer.hpp:628-634).
+    for (std::size_t i = 0; h->mode == Mode::WD && h->wd_frozen && i < h->entries.size(); ++i)
+      if (h->entries[i].kernel.same_shape(k)) {
+        *algo = UCUDNN_VIRTUAL_ALGO_BASE + int(i);
+        return UCUDNN_STATUS_SUCCESS;
+      }
     for (std::size_t i = 0; h->mode == Mode::WR && i < h->entries.size(); ++i)
       if (h->entries[i].kernel.same_shape(k) && h->entries[i].limit == limit) {
         *algo = UCUDNN_VIRTUAL_ALGO_BASE + int(i);
@@ -883,8 +921,9 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     std::int64_t ws = algo_ws(int(op), s, algo, &ok);
     *feasible = ok ? 1 : 0;
     *ws_bytes = ws;
-    *time_us = ok ? double(time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws)) / 1000.0
-                  : 0.0;
+    const std::int64_t ns = ok ? time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws) : 0;
+    if (ns < 0) *feasible = 0;
+    *time_us = ns > 0 ? double(ns) / 1000.0 : 0.0;
     return UCUDNN_STATUS_SUCCESS;
   });
 }

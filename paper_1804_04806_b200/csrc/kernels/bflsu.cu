@@ -750,6 +750,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   e = set_smem_attr(reinterpret_cast<const void*>(bfl_kernel), 220 * 1024);
   if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfl2_kernel), 220 * 1024);
   if (e != cudaSuccess) return e;
+  trace_variant("%s tiles=%d splits=%d swap=%d dual=%d", g.two ? "bfl2" : "bfl", p.tiles, p.splits, int(g.swap),
+                int(g.dual));
   if (g.two) {
     count_launch();
     cudaLaunchConfig_t cfg{};

@@ -704,6 +704,9 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfn2_kernel), 220 * 1024);
   if (e != cudaSuccess) return e;
   const int units = p.tiles * p.splits;
+  trace_variant("%s tiles=%d splits=%d units=%d msub=%d px=%d dyd=%d s2d=%d acc=%d defer=%d", g.two ? "bfn2" : "bfn",
+                p.tiles, p.splits, units, p.msub, p.px, int(g.dyd), int(g.s2d), (flags & kAccumulate) ? 1 : 0,
+                (flags & kDeferFinal) ? 1 : 0);
   if (g.two) {
     count_launch();
     cudaLaunchConfig_t cfg{};

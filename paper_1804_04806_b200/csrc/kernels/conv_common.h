@@ -29,6 +29,13 @@ cudaError_t set_smem_attr(const void* func, int bytes);
 void count_launch(int n = 1);
 std::uint64_t launch_count();
 
+// Launch-variant trace (ucudnnDebugSetTrace / ucudnnDebugGetTrace): when on,
+// launchers append one line per main-kernel launch naming the variant and
+// its tiling (e.g. "precomp2 m_tiles=729 n_tiles=1 clusters=74"), so tests can
+// prove which code path a bench-scale call exercised. Off: one atomic load.
+bool trace_on();
+void trace_variant(const char* fmt, ...);
+
 // Unsigned division by a runtime constant via multiply-high (valid for
 // dividends < 2^31): q = umulhi(n, mul) >> shr, or n when d == 1.
 struct FastDiv {

@@ -700,7 +700,10 @@ __global__ void __launch_bounds__(256, MinB)
   // issued before the first smem store (a loop of load -> store per row
   // exposed one DRAM latency per row: 44 us per 64 AlexNet images)
   const int nr = d.C * Ah;
-  if ((d.W & 3) == 0 && (reinterpret_cast<std::uintptr_t>(x) & 15) == 0) {
+  // (only when every input column lands inside the row: with kernel ==
+  // stride and W not a multiple of it, trailing columns no window reads
+  // would run past the row pitch; the scalar loop below only writes t < L)
+  if ((d.W & 3) == 0 && (reinterpret_cast<std::uintptr_t>(x) & 15) == 0 && d.pw + d.W <= L) {
     // float4 loads along w (the scalar loop below was issue-bound: 77 %
     // issue-active, ~1000 instructions per warp for AlexNet conv1); padding
     // columns and rows outside the image are zero-filled separately
@@ -1493,6 +1496,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     e = set_smem_attr(reinterpret_cast<const void*>(precomp2_kernel), 227 * 1024);
     if (e != cudaSuccess) return e;
     const int clusters = std::min(sm_count() / 2, p.m_tiles * p.n_tiles);
+    trace_variant("precomp2 flip=%d m_tiles=%d n_tiles=%d clusters=%d BN=%d phase=%d s2d=%d", flip,
+                  p.m_tiles, p.n_tiles, clusters, BN, int(g.phase), int(g.s2d));
     count_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * clusters);
@@ -1540,6 +1545,8 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     if (e != cudaSuccess) return e;
   }
   const int grid = std::min(p.cps * sm_count(), p.m_tiles * p.n_tiles);
+  trace_variant("precomp flip=%d cps=%d msub=%d m_tiles=%d n_tiles=%d grid=%d BN=%d phase=%d s2d=%d", flip,
+                p.cps, p.msub, p.m_tiles, p.n_tiles, grid, BN, int(g.phase), int(g.s2d));
   return launch_pdl(precomp_kernel, dim3(grid), dim3(kThreads), std::size_t(smem), st, amap, p);
 }
 

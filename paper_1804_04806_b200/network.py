@@ -57,7 +57,9 @@ def shard(global_batch: int, world: int, rank: int):
 def share_cost_table(csv_path: str, group=None) -> str:
     """Rank 0's benchmarked cost table (the reference CSV format,
     cost_database.hpp:32-45) broadcast to every rank, so all ranks plan from
-    the same rows -- and the planner being deterministic, run the same plan."""
+    the same rows -- and the planner being deterministic, run the same plan.
+    `csv_path` is rank 0's table on rank 0 and the rank's own copy (written
+    here) elsewhere; ranks must not share one path."""
     import torch.distributed as dist
     payload = [open(csv_path).read() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(payload, src=0, group=group)
@@ -198,6 +200,3 @@ class ConvStack:
             for p in pending:
                 p.wait()  # makes the current stream wait for the NCCL work
             cur.wait_stream(comm_stream)
-
-    def launches_per_step(self, h: Handle) -> int:
-        return 0

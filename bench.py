@@ -225,6 +225,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a replayed CUDA graph")
     ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="benchmark and plan (writing --db), print the plans as one JSON line, exit")
     ap.add_argument("--bf-stream", type=int, default=2,
                     help="k >= 1: each BackwardFilter on one of k side streams (BF_i on stream i % k), "
                          "overlapping the BackwardData chain (both arms); 0: one stream")
@@ -290,6 +292,13 @@ def main():
     h.flush_database()
     plan_s = time.perf_counter() - t0
     plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": h.plan(a) for (i, op), a in stack.algos.items()}
+    if args.plan_only:
+        if rank == 0:
+            print(json.dumps({"net": args.net, "mode": args.mode, "policy": args.policy, "db": db,
+                              "plan_seconds": round(plan_s, 1),
+                              "plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in plans.items()}}),
+                  flush=True)
+        return
     base = Handle(policy="undivided", mode="wr", database=db, stream=stream.cuda_stream)
     base_stack_algos = {}
     for (i, op) in stack.kernels():

@@ -40,6 +40,7 @@
 
 #include "bflsu.h"
 #include "conv_common.h"
+#include "igemm.h"
 #include "launch.h"
 #include "sm100.cuh"
 
@@ -115,7 +116,28 @@ struct LParams {
   int crs;  // x row order: 1 (c, r, s) = dW order, 0 (r, s, c)
   int sg, ngroups, sgs;
   int dual;  // CTA-pair kernel: two pair tiles per unit  // strided few-channel gather: groups of sw taps, count, ceil(S / sw)
+  // direct (IMPLICIT_GEMM, zero workspace): RED alpha * partial straight into
+  // dW[k][c][r][s] (`acc` = dw, beta applied by a scale pass first) instead
+  // of into the GEMM-layout scratch + finalize; a warp's REDs then scatter
+  // over 32 filter rows (DESIGN finding 8: ~8-18 us per call)
+  int direct;
+  float vscale;
 };
+
+// RED target of partial (x row m, output channel k)
+__device__ __forceinline__ float* red_target(const LParams& p, int m, int k) {
+  if (p.direct) {
+    int off = m;
+    if (!p.crs) {  // row (r, s, c) -> dW offset c*R*S + r*S + s
+      std::uint32_t rs, c, r, s;
+      p.fd_C.divmod(std::uint32_t(m), rs, c);
+      p.fd_S.divmod(rs, r, s);
+      off = int(c) * p.R * p.S + int(r) * p.S + int(s);
+    }
+    return p.acc + std::int64_t(k) * p.M + off;
+  }
+  return p.swap ? p.acc + std::int64_t(m) * kBM + k : p.acc + std::int64_t(k) * p.rpad + m;
+}
 
 // 4-byte gather; src_size 0 writes a zero (src is then never dereferenced)
 __device__ __forceinline__ void cp_async4a(std::uint32_t dst, std::uint64_t src, std::uint32_t src_size) {
@@ -448,7 +470,7 @@ __global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LPa
           for (int j = 0; j < 32; ++j) {
             const int m = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || m >= p.M) break;
-            red_add(p.acc + std::int64_t(m) * kBM + k, v[j]);
+            red_add(red_target(p, m, k), p.vscale * v[j]);
           }
         }
       } else {
@@ -462,7 +484,7 @@ __global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LPa
           for (int j = 0; j < 32; ++j) {
             const int k = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || k >= p.K) break;
-            red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+            red_add(red_target(p, m, k), p.vscale * v[j]);
           }
         }
       }
@@ -630,7 +652,7 @@ __global__ void __launch_bounds__(threads_for<kProd2>(), 1) bfl2_kernel(const LP
           for (int j = 0; j < 32; ++j) {
             const int k = nt * p.BN + c0 + j;
             if (c0 + j >= p.BN || k >= p.K) break;
-            red_add(p.acc + std::int64_t(k) * p.rpad + m, v[j]);
+            red_add(red_target(p, m, k), p.vscale * v[j]);
           }
         }
       }
@@ -693,10 +715,11 @@ bool bfl_supports(const ConvShape& s) {
 std::int64_t bfl_workspace(const ConvShape& s) { return std::int64_t(scratch_bytes(make_lgeo(s))); }
 
 cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool direct) {
   const LGeo g = make_lgeo(s);
-  float* acc = static_cast<float*>(ws);
-  cudaError_t e = cudaMemsetAsync(acc, 0, std::size_t(rows_pad(g)) * cols_pad(g) * 4, st);
+  float* acc = direct ? dw : static_cast<float*>(ws);
+  cudaError_t e = direct ? scale_tensor(dw, s.w_elems(), beta, st)
+                         : cudaMemsetAsync(acc, 0, std::size_t(rows_pad(g)) * cols_pad(g) * 4, st);
   if (e != cudaSuccess) return e;
   const int sms = sm_count();
   LParams p{};
@@ -718,6 +741,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.steps = g.steps;
   p.rpad = rows_pad(g);
   p.dbg = tune("bfl_dbg", 0);
+  p.direct = direct ? 1 : 0;
+  p.vscale = direct ? alpha : 1.f;
   p.fd_ohw = FastDiv(std::uint32_t(p.OHW));
   p.fd_ow = FastDiv(std::uint32_t(g.OW));
   p.fd_C = FastDiv(std::uint32_t(g.C));
@@ -750,8 +775,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   e = set_smem_attr(reinterpret_cast<const void*>(bfl_kernel), 220 * 1024);
   if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfl2_kernel), 220 * 1024);
   if (e != cudaSuccess) return e;
-  trace_variant("%s tiles=%d splits=%d swap=%d dual=%d", g.two ? "bfl2" : "bfl", p.tiles, p.splits, int(g.swap),
-                int(g.dual));
+  trace_variant("%s tiles=%d splits=%d swap=%d dual=%d direct=%d", g.two ? "bfl2" : "bfl", p.tiles, p.splits,
+                int(g.swap), int(g.dual), p.direct);
   if (g.two) {
     count_launch();
     cudaLaunchConfig_t cfg{};
@@ -771,7 +796,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
     e = launch_pdl(bfl_kernel, dim3(std::min(sms, p.tiles * p.splits)), dim3(threads_for<kProd1>()),
                    std::size_t(smem), st, p);
   }
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || direct) return e;
   LFinal f{acc, dw, alpha, beta, g.C, g.R, g.S, rows_pad(g), g.swap, p.crs, s.w_elems()};
   return launch_pdl(bfl_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256), 0,
                     st, f);

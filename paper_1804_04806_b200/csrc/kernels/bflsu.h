@@ -14,6 +14,6 @@ bool bfl_supports(const ConvShape& s);
 std::int64_t bfl_workspace(const ConvShape& s);
 // dw = beta * dw + alpha * sum (split-K, fp32 reductions into a GEMM-layout scratch)
 cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha, float beta,
-                    cudaStream_t stream);
+                    cudaStream_t stream, bool direct = false);
 
 }  // namespace ucudnn

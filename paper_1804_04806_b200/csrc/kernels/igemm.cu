@@ -21,6 +21,7 @@
 
 #include "conv_common.h"
 #include "igemm.h"
+#include "bflsu.h"
 #include "sm100.cuh"
 
 namespace ucudnn {
@@ -405,6 +406,7 @@ void fill_common(IgemmParams& p, const ConvShape& s) {
 
 cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
                           cudaStream_t stream) {
+  if (tune("z", 1) && zgemm_supports(kFwd, s)) return zgemm_forward(s, x, w, y, alpha, beta, stream);
   IgemmParams p{};
   fill_common(p, s);
   p.a = x; p.b = w; p.out = y; p.alpha = alpha; p.beta = beta;
@@ -421,6 +423,7 @@ cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, fl
 // independent dense GEMM (no multiplications by structural zeros).
 cudaError_t igemm_backward_data(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha,
                                 float beta, cudaStream_t stream) {
+  if (tune("z", 1) && zgemm_supports(kBwdData, s)) return zgemm_backward_data(s, dy, w, dx, alpha, beta, stream);
   for (int pa = 0; pa < s.sh; ++pa)
     for (int pb = 0; pb < s.sw; ++pb) {
       IgemmParams p{};
@@ -463,6 +466,9 @@ cudaError_t scale_tensor(float* p, std::int64_t n, float beta, cudaStream_t stre
 
 cudaError_t igemm_backward_filter(const ConvShape& s, const float* x, const float* dy, float* dw, float alpha,
                                   float beta, cudaStream_t stream) {
+  // the gather BackwardFilter (bflsu.cu) with its REDs aimed straight at dW:
+  // no scratch, so still zero workspace
+  if (tune("z", 1) && bfl_supports(s)) return bfl_run(s, x, dy, dw, nullptr, alpha, beta, stream, true);
   cudaError_t e = scale_tensor(dw, s.w_elems(), beta, stream);
   if (e != cudaSuccess) return e;
   IgemmParams p{};

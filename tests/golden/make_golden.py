@@ -72,6 +72,31 @@ def main():
 
 
 
+# Measured B200 cost tables (written by bench.py's device benchmarker, nine
+# algorithm ids, ns-resolution times) replayed through the REFERENCE planner:
+# (case, net, batch, mode, policy, limit, csv file in csv/)
+B200_CASES = [
+    ("b200_alexnet_wr_pow2_64M", "alexnet", 256, "wr", "powerOfTwo", 64 * MiB, "b200_alexnet_pow2_64M"),
+    ("b200_alexnet_wr_undiv_64M", "alexnet", 256, "wr", "undivided", 64 * MiB, "b200_alexnet_pow2_64M"),
+    ("b200_alexnet_wr_pow2_8M", "alexnet", 256, "wr", "powerOfTwo", 8 * MiB, "b200_alexnet_pow2_64M"),
+    ("b200_alexnet_wd_pow2_960M", "alexnet", 256, "wd", "powerOfTwo", 960 * MiB, "b200_alexnet_pow2_64M"),
+    ("b200_alexnet_wd_pow2_240M", "alexnet", 256, "wd", "powerOfTwo", 240 * MiB, "b200_alexnet_pow2_64M"),
+    ("b200_alexnet_wr_all_64M", "alexnet", 256, "wr", "all", 64 * MiB, "b200_alexnet_all_64M"),
+    ("b200_alexnet_wd_all_960M", "alexnet", 256, "wd", "all", 960 * MiB, "b200_alexnet_all_64M"),
+    ("b200_resnet18_wr_pow2_64M", "resnet18", 256, "wr", "powerOfTwo", 64 * MiB, "b200_resnet18_pow2_64M"),
+    ("b200_resnet18_wd_pow2_1280M", "resnet18", 256, "wd", "powerOfTwo", 1280 * MiB, "b200_resnet18_pow2_64M"),
+    ("b200_resnet50_wd_pow2_2544M", "resnet50", 256, "wd", "powerOfTwo", 2544 * MiB, "b200_resnet50_wd_pow2_2544M"),
+]
+
+
+def make_b200_golden():
+    for case, net, batch, mode, policy, limit, csv in B200_CASES:
+        rep = ref_optimize(os.path.join(ROOT, "configs", net + ".net"), batch, mode, policy, limit,
+                           cost=os.path.join(OUT, "csv", csv + ".csv"))
+        open(os.path.join(OUT, "reports", case + ".txt"), "w").write(rep)
+        print(case, len(rep.splitlines()), "lines")
+
+
 def make_conv_golden():
     """Small conv golden vectors from the reference's own execute_plan
     (oracle/_ref/ref_conv.so): integer inputs, one stride-2 and one padded
@@ -97,5 +122,10 @@ def make_conv_golden():
 
 
 if __name__ == "__main__":
-    main()
-    make_conv_golden()
+    import sys
+    if sys.argv[1:] == ["b200"]:
+        make_b200_golden()
+    else:
+        main()
+        make_conv_golden()
+        make_b200_golden()

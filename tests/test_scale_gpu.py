@@ -4,8 +4,9 @@ a17-a20), against the fp64 oracle (reference_conv.hpp:70-278).
 The small-shape tests in test_algos_gpu.py never leave the first wave of
 tiles; the bench runs up to 1,458 output tiles per call, persistent CTAs
 looping over many tiles with double-buffered TMEM, two CTAs per SM, CTA pairs
-covering several tiles per cluster, split-K BackwardFilter over more units
-than SMs, and 8@128 deferred-finalize runs. This file runs those paths:
+covering several tiles per cluster, split-K BackwardFilter (one tile's
+reduction over several CTAs), 8@128 deferred-finalize runs, and the
+zero-workspace implicit GEMM's persistent multi-tile loop. This file runs those paths:
 
 * every feasible algorithm id at micro-batches 64, 128 and 256 for each
   AlexNet layer and op (undivided call on the first b images);
@@ -252,7 +253,8 @@ def test_zz_bench_scale_variants_exercised(cuda):
     precomp2 with more tiles than clusters (multi-tile CTA-pair loop), the
     1-SM implicit GEMM at two CTAs per SM, the CTA-pair channels-last
     BackwardFilter, split-K over more units than SMs, and deferred-finalize
-    runs (kAccumulate / kDeferFinal across an 8@128 + 8@128 plan)."""
+    runs (kAccumulate / kDeferFinal across an 8@128 + 8@128 plan), and the
+    zero-workspace implicit GEMM (algorithm 0) on every AlexNet F / BD."""
     if not TRACE:
         pytest.skip("run with the rest of this module")
 
@@ -266,6 +268,12 @@ def test_zz_bench_scale_variants_exercised(cuda):
     bfn = [l for l in TRACE if l.startswith("bfn2 ")]
     assert bfn, "no CTA-pair algorithm-8 BackwardFilter"
     allbf = [kv(l) for l in TRACE if l.startswith(("bfn ", "bfn2 ", "bfl ", "bfl2 "))]
-    assert any(int(d["units"] if "units" in d else int(d["tiles"]) * int(d["splits"])) > 148 for d in allbf)
+    # split-K: one tile's reduction spread over several persistent CTAs whose
+    # fp32 partial sums meet in the RED scratch (units are sized to fill the
+    # SMs once, so splits > 1 is the multi-CTA reduction case)
+    assert any(int(d["splits"]) > 1 for d in allbf), "no split-K BackwardFilter"
     assert any(d.get("defer") == "1" for d in allbf) and any(d.get("acc") == "1" for d in allbf), \
         "no deferred-finalize run"
+    z = [kv(l) for l in TRACE if l.startswith("zgemm ")]
+    assert any(int(d["m_tiles"]) * int(d["n_tiles"]) > int(d["grid"]) for d in z), "no multi-tile zgemm"
+    assert {d["bmode"] for d in z} >= {"0", "1", "2"}, "zgemm B paths not all exercised"

@@ -81,7 +81,8 @@ LGeo make_lgeo(const ConvShape& s) {
   g.swap = s.K <= 128 && g.M > 128;
   if (g.swap) {
     int nt = (g.M + kMaxBN - 1) / kMaxBN;
-    g.BN = round_up((g.M + nt - 1) / nt, 16);
+    // few channels: the x rows may land MN-major (whole 32-row blocks)
+    g.BN = round_up((g.M + nt - 1) / nt, s.C % 8 != 0 ? 32 : 16);
     g.n_tiles = (g.M + g.BN - 1) / g.BN;
     g.m_tiles = 1;
   } else {
@@ -122,6 +123,12 @@ struct LParams {
   // over 32 filter rows (DESIGN finding 8: ~8-18 us per call)
   int direct;
   float vscale;
+  // xmn (swapped roles, few channels): x rows land MN-major (the 128B/32B-atom
+  // swizzle, DESIGN finding 5) with lane = x row (c, r, s) at a fixed pixel,
+  // so a warp's 32 cp.async read the S consecutive input columns of ~3 filter
+  // rows -- a few sectors -- instead of 32 pixels at stride sw (AlexNet conv1:
+  // 512 B, 16 sectors per instruction)
+  int xmn;
 };
 
 // RED target of partial (x row m, output channel k)
@@ -165,6 +172,20 @@ __device__ __forceinline__ void mbar_wait_backoff(std::uint64_t* bar, std::uint3
     if (ns < 4096) ns <<= 1;
   }
 }
+// MN-major 128B / 32 B-atom descriptor: LBO 4096 B between 32-row blocks
+// (32 K-rows x 128 B), SBO 512 B (bfnhwc.cu desc_mn32)
+__device__ __forceinline__ std::uint64_t desc_mn32(std::uint32_t saddr) {
+  std::uint64_t d = 0;
+  d |= std::uint64_t((saddr >> 4) & 0x3FFF);
+  d |= std::uint64_t(4096 >> 4) << 16;
+  d |= std::uint64_t(512 >> 4) << 32;
+  d |= std::uint64_t(1) << 46;
+  d |= std::uint64_t(1) << 61;
+  return d;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // bits t in [lo, hi) of a width-n tap mask (n <= 32)
 __device__ __forceinline__ std::uint32_t range_mask(int lo, int hi, int n) {
   lo = max(lo, 0);
@@ -188,7 +209,7 @@ struct Gatherer {
   int xm0, xrows, dk0, drows;  // current unit: x rows [xm0, +xrows), dy rows [dk0, +drows)
 
   __device__ __forceinline__ Gatherer(const LParams& p_, int lane_, int pw_, int2* tab)
-      : p(p_), lane(lane_), pw(pw_), c8(!p_.crs && p_.C % 8 == 0), sg(p_.sg != 0), xtab(tab) {
+      : p(p_), lane(lane_), pw(pw_), c8(!p_.crs && p_.C % 8 == 0 && !p_.xmn), sg(p_.sg != 0), xtab(tab) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       swz[j] = j * 128 + ((std::uint32_t(lane >> 2) ^ j) << 4) + (lane & 3) * 4;
@@ -202,7 +223,21 @@ struct Gatherer {
     xrows = xrows_;
     dk0 = dk0_;
     drows = drows_;
-    if (c8) {
+    if (p.xmn) {
+      // every producer warp reads every row's entry: (c*HW + r*W + s, r << 8 | s)
+      named_sync(1, kProd * 32);  // all producers are done with the previous unit's table
+      for (int j = pw * 32 + lane; j < xrows; j += kProd * 32) {
+        std::uint32_t rs, c, r, s;
+        if (p.crs) {
+          p.fd_RS.divmod(std::uint32_t(xm0 + j), c, rs);
+        } else {
+          p.fd_C.divmod(std::uint32_t(xm0 + j), rs, c);
+        }
+        p.fd_S.divmod(rs, r, s);
+        xtab[j] = make_int2(int(c) * p.HW + int(r) * p.W + int(s), int(r << 8 | s));
+      }
+      named_sync(1, kProd * 32);
+    } else if (c8) {
       // this warp's 8-row groups (tile t, group q0/8): (c*HW + r*W + s, r << 16 | s),
       // so a step reads one smem word pair per group instead of two divisions
       for (int t = 0; t < (xrows2 > 0 ? 2 : 1); ++t) {
@@ -288,6 +323,34 @@ struct Gatherer {
     }
   }
 
+  // x rows MN-major: block i of 32 rows at xs + i*4096, pixel k at K-row k
+  __device__ __forceinline__ void step_xmn(int g, std::uint32_t xs) const {
+    const std::uint32_t lsw = std::uint32_t(lane & 7) * 4, lg = std::uint32_t(lane >> 3);
+    const int nblk = (xrows + 31) >> 5;
+    for (int k = pw; k < 32; k += kProd) {
+      const long long pg = (long long)g * 32 + k;
+      const bool valid = pg < p.npx;
+      std::uint32_t n, pix, oh, ow;
+      p.fd_ohw.divmod(std::uint32_t(valid ? pg : 0), n, pix);
+      p.fd_ow.divmod(pix, oh, ow);
+      const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
+      const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
+      const std::uint32_t krow = xs + std::uint32_t(k) * 128 + ((lg ^ std::uint32_t(k & 3)) << 5) + lsw;
+      for (int i = 0; i < nblk; ++i) {
+        const int j = i * 32 + lane;
+        std::uint32_t ok = 0;
+        int off = 0;
+        if (j < xrows) {
+          const int2 e = xtab[j];
+          const int r = e.y >> 8, s = e.y & 255;
+          ok = (valid && unsigned(ihb + r) < unsigned(p.H) && unsigned(iwb + s) < unsigned(p.W)) ? 1u : 0u;
+          off = e.x;
+        }
+        cp_async4a(krow + std::uint32_t(i) * 4096, reinterpret_cast<std::uint64_t>(ok ? xl + off : p.x), ok * 4u);
+      }
+    }
+  }
+
   // x rows -> smem at xs, dy rows -> smem at ds (SW128 K-major, row q at q*128)
   // xs2 != 0 (CTA-pair kernel, C % 8 == 0): a second x tile, rows
   // [xm0 + 256, + xrows2), into xs2 -- the dy rows are gathered once for both
@@ -300,7 +363,9 @@ struct Gatherer {
     p.fd_ow.divmod(pix, oh, ow);
     const int ihb = int(oh) * p.sh - p.ph, iwb = int(ow) * p.sw - p.pw;
     const float* xl = p.x + (long long)n * p.CHW + (long long)ihb * p.W + iwb;
-    if (sg) {
+    if (p.xmn) {
+      step_xmn(g, xs);
+    } else if (sg) {
       step_strided(g, xs);
     } else if (c8) {
       // one bounds test per group, then consecutive channel planes
@@ -414,7 +479,8 @@ __global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LPa
     }
   } else if (warp == 4) {
     // ------------------------------------------------ MMA issuer
-    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    // xmn: B (the x rows) MN-major -- instruction-descriptor bit 16
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN) | (p.xmn ? (1u << 16) : 0u);
     const std::uint32_t sbase = smem_u32(smem);
     int it = 0, tl = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
@@ -436,7 +502,8 @@ __global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LPa
           if (p.dbg != 2)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              mma_tf32(dtm, umma_desc_sw128(sa + q * 32), umma_desc_sw128(sb + q * 32), idesc,
+              mma_tf32(dtm, umma_desc_sw128(sa + q * 32), p.xmn ? desc_mn32(sb + q * 1024) : umma_desc_sw128(sb + q * 32),
+                       idesc,
                        (g != g0 || q != 0) ? 1u : 0u);
           mma_commit(&empty[st]);
           if (g + 1 >= g1) mma_commit(&tfull[acc]);
@@ -760,6 +827,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.sg = !p.crs && g.C % 8 != 0 && (g.sw == 2 || g.sw == 4) && g.C < 256 && p.ngroups <= kMaxBN &&
          tune("bfl_sg", 0);  // exact, but issue-bound: AlexNet conv1 BF 542 -> 876 us, ResNet conv1 1031 -> 1601
   p.fd_sgs = FastDiv(std::uint32_t(p.sgs));
+  p.xmn = g.swap && !p.sg && (g.C % 8 != 0 || p.crs) && tune("bfl_xmn", 1);
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
@@ -775,8 +843,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   e = set_smem_attr(reinterpret_cast<const void*>(bfl_kernel), 220 * 1024);
   if (e == cudaSuccess) e = set_smem_attr(reinterpret_cast<const void*>(bfl2_kernel), 220 * 1024);
   if (e != cudaSuccess) return e;
-  trace_variant("%s tiles=%d splits=%d swap=%d dual=%d direct=%d", g.two ? "bfl2" : "bfl", p.tiles, p.splits,
-                int(g.swap), int(g.dual), p.direct);
+  trace_variant("%s tiles=%d splits=%d swap=%d dual=%d direct=%d xmn=%d", g.two ? "bfl2" : "bfl", p.tiles,
+                p.splits, int(g.swap), int(g.dual), p.direct, p.xmn);
   if (g.two) {
     count_launch();
     cudaLaunchConfig_t cfg{};

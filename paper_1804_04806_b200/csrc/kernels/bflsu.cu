@@ -127,7 +127,10 @@ struct LParams {
   // swizzle, DESIGN finding 5) with lane = x row (c, r, s) at a fixed pixel,
   // so a warp's 32 cp.async read the S consecutive input columns of ~3 filter
   // rows -- a few sectors -- instead of 32 pixels at stride sw (AlexNet conv1:
-  // 512 B, 16 sectors per instruction)
+  // 512 B, 16 sectors per instruction). Exact, but measured 2x slower on
+  // AlexNet conv1 BF (1117 vs 591 us at 256 images; ncu: L1 35 % vs 64 %,
+  // producer warps latency-bound on the per-pixel decode), so off by default
+  // (UCUDNN_TUNE=bfl_xmn=1; profiles/r02_ncu_bfl_xmn_conv1_bf.txt)
   int xmn;
 };
 
@@ -827,7 +830,7 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.sg = !p.crs && g.C % 8 != 0 && (g.sw == 2 || g.sw == 4) && g.C < 256 && p.ngroups <= kMaxBN &&
          tune("bfl_sg", 0);  // exact, but issue-bound: AlexNet conv1 BF 542 -> 876 us, ResNet conv1 1031 -> 1601
   p.fd_sgs = FastDiv(std::uint32_t(p.sgs));
-  p.xmn = g.swap && !p.sg && (g.C % 8 != 0 || p.crs) && tune("bfl_xmn", 1);
+  p.xmn = g.swap && !p.sg && (g.C % 8 != 0 || p.crs) && tune("bfl_xmn", 0);
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
   const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));

@@ -36,7 +36,7 @@
 //
 // Warps: 0-3 epilogue (TMEM -> registers -> NCHW stores, alpha/beta), 4 TMEM
 // owner + MMA issuer (two 256-column accumulators: a tile's epilogue
-// overlaps the next tile's MMAs), 5-12 producers (warp 5 lane 0 also issues
+// overlaps the next tile's MMAs), 5-20 producers (warp 5 lane 0 also issues
 // the TMA B loads).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -58,7 +58,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kMaxBN = 256;
 constexpr int kMaxStages = 8;
-constexpr int kProd = 8;
+constexpr int kProd = 16;
 constexpr int kThreads = (5 + kProd) * 32;
 constexpr std::uint32_t kABytes = kBM * 128;  // 4 MN blocks x 32 K-rows x 128 B
 
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ producers
     const int pw = warp - 5;
     const int pb = pw & 3;         // this warp's 32-position block of the tile
-    const int js = pw >> 2;        // and its reduction indices k = js, js + 2, ...
+    const int js = pw >> 2;        // and its reduction indices k = js, js + 4, ... (k & 3 == js)
     const std::uint32_t sbase = smem_u32(smem);
     const std::uint32_t swz_lane = std::uint32_t(lane & 7) * 4;
     const bool tma_thread = p.bmode == 0 && pw == 0 && lane == 0;
@@ -250,15 +250,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             brt = bsu = 0;
           }
         }
-        // A: 16 reduction indices x 32 positions, one 128 B smem row each
-        const std::uint32_t arow = sa + std::uint32_t(pb) * 4096;
-#pragma unroll 4
-        for (int k = js; k < 32; k += 2) {
+        // A: 8 reduction indices x 32 positions, one 128 B smem row each (the
+        // swizzle XOR (k & 3) is this warp's js, so destinations are a
+        // per-thread base plus immediates); a skipped copy (src-size 0) never
+        // dereferences its address
+        const std::uint32_t arow = sa + std::uint32_t(pb) * 4096 + std::uint32_t(js) * 128 +
+                                   ((std::uint32_t((lane >> 3) ^ js)) << 5) + swz_lane;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int k = js + 4 * i;
           const int off = __shfl_sync(0xffffffffu, eoff, k);
           const int tu = __shfl_sync(0xffffffffu, etu, k);
           const std::uint32_t ok = (vr >> (tu >> 8)) & (vs >> (tu & 255)) & 1u;
-          const std::uint32_t dst = arow + std::uint32_t(k) * 128 + ((std::uint32_t((lane >> 3) ^ (k & 3))) << 5) + swz_lane;
-          cp_async4(dst, base + (ok ? off : 0), ok * 4u);
+          cp_async4(arow + std::uint32_t(i) * 512, base + off, ok * 4u);
         }
         // B (gathered): rows of this n tile, lane = reduction index
         if (p.bmode != 0) {
@@ -272,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               off = e.woff + boff;
             }
             const std::uint32_t dst = sb + std::uint32_t(r) * 128 + (((bsw ^ std::uint32_t(r & 7))) << 4) + bl;
-            cp_async4(dst, p.w + (ok ? off : 0), ok * 4u);
+            cp_async4(dst, p.w + off, ok * 4u);
           }
         }
         cp_async_arrive(&full[st]);

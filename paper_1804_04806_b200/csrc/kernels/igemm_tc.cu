@@ -78,6 +78,8 @@ struct ZParams {
   int Ho, Wo, osh, osw, oph, opw;
   long long oimg;
   int stages;
+  int msub;  // position sub-tiles of 128 per tile, sharing each B stage (halves B traffic at 2)
+  int nacc;  // TMEM accumulator sets (2: a tile's epilogue overlaps the next tile's MMAs)
   FastDiv fd_HWg, fd_Wg, fd_TU, fd_U, fd_C, fd_sw;
 };
 
@@ -160,7 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t b_bytes = (std::uint32_t(p.BN) * 128 + 1023) & ~1023u;
-  const std::uint32_t stage_bytes = kABytes + b_bytes;
+  const int msub = p.msub;
+  const std::uint32_t stage_bytes = msub * kABytes + b_bytes;
   const int kStages = p.stages;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
   std::uint64_t* empty = full + kMaxStages;
@@ -209,26 +212,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_sync(1, kProd * 32);
         cur_nt = nt;
       }
-      // this lane's position
-      const int m = mt * kBM + pb * 32 + lane;
-      std::uint32_t vr = 0, vs = 0;
-      const float* base = p.src;
-      if (m < p.M) {
-        std::uint32_t n, g, gi, gj;
-        p.fd_HWg.divmod(std::uint32_t(m), n, g);
-        p.fd_Wg.divmod(g, gi, gj);
-        const int ihb = int(gi) * p.gsh - p.gph, iwb = int(gj) * p.gsw - p.gpw;
-        vr = range_mask(-ihb, p.Hs - ihb, p.T);
-        vs = range_mask(-iwb, p.Ws - iwb, p.U);
-        base = p.src + std::int64_t(n) * p.simg + std::int64_t(ihb) * p.Ws + iwb;
+      // this lane's position in each sub-tile
+      std::uint32_t vr[2] = {0, 0}, vs[2] = {0, 0};
+      const float* base[2] = {p.src, p.src};
+#pragma unroll
+      for (int sub = 0; sub < 2; ++sub) {
+        const int m = (mt * msub + sub) * kBM + pb * 32 + lane;
+        if (sub < msub && m < p.M) {
+          std::uint32_t n, g, gi, gj;
+          p.fd_HWg.divmod(std::uint32_t(m), n, g);
+          p.fd_Wg.divmod(g, gi, gj);
+          const int ihb = int(gi) * p.gsh - p.gph, iwb = int(gj) * p.gsw - p.gpw;
+          vr[sub] = range_mask(-ihb, p.Hs - ihb, p.T);
+          vs[sub] = range_mask(-iwb, p.Ws - iwb, p.U);
+          base[sub] = p.src + std::int64_t(n) * p.simg + std::int64_t(ihb) * p.Ws + iwb;
+        }
       }
       const int brows = min(p.BN, p.ncols - nt * p.BN);
       for (int ch = 0; ch < p.chunks; ++ch) {
         mbar_wait(&empty[st], ph ^ 1);
-        const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + kABytes;
+        const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + msub * kABytes;
         if (tma_thread) {
           mbar_expect_tx(&full[st], std::uint32_t(p.BN) * 128);
-          tma_2d(smem + st * stage_bytes + kABytes, &bmap, &full[st], ch * 32, nt * p.BN);
+          tma_2d(smem + st * stage_bytes + msub * kABytes, &bmap, &full[st], ch * 32, nt * p.BN);
         }
         // this lane's reduction entry kr = ch*32 + lane: (cs, t, u)
         const int kr = ch * 32 + lane;
@@ -261,8 +267,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k = js + 4 * i;
           const int off = __shfl_sync(0xffffffffu, eoff, k);
           const int tu = __shfl_sync(0xffffffffu, etu, k);
-          const std::uint32_t ok = (vr >> (tu >> 8)) & (vs >> (tu & 255)) & 1u;
-          cp_async4(arow + std::uint32_t(i) * 512, base + off, ok * 4u);
+          const int t = tu >> 8, uu = tu & 255;
+          cp_async4(arow + std::uint32_t(i) * 512, base[0] + off, ((vr[0] >> t) & (vs[0] >> uu) & 1u) * 4u);
+          if (msub == 2)
+            cp_async4(arow + kABytes + std::uint32_t(i) * 512, base[1] + off,
+                      ((vr[1] >> t) & (vs[1] >> uu) & 1u) * 4u);
         }
         // B (gathered): rows of this n tile, lane = reduction index
         if (p.bmode != 0) {
@@ -292,20 +301,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t sbase = smem_u32(smem);
     int it = 0, tl = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
-      const int acc = tl & 1;
-      mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      const int acc = tl % p.nacc, use = tl / p.nacc;
+      mbar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
-      const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t dtm = tmem + std::uint32_t(acc * msub * p.BN);
       for (int ch = 0; ch < p.chunks; ++ch, ++it) {
         const int st = it % kStages;
         mbar_wait(&full[st], (it / kStages) & 1);
         tc_fence_after();
         if (lane == 0) {
           fence_async_smem();  // cp.async (generic proxy) -> tensor core (async proxy)
-          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + kABytes;
+          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + msub * kABytes;
+          for (int sub = 0; sub < msub; ++sub)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            mma_tf32(dtm, desc_mn32(sa + j * 1024), umma_desc_sw128(sb + j * 32), idesc, (ch | j) ? 1u : 0u);
+            for (int j = 0; j < 4; ++j)
+              mma_tf32(dtm + std::uint32_t(sub * p.BN), desc_mn32(sa + sub * kABytes + j * 1024),
+                       umma_desc_sw128(sb + j * 32), idesc, (ch | j) ? 1u : 0u);
           mma_commit(&empty[st]);
           if (ch + 1 == p.chunks) mma_commit(&tfull[acc]);
         }
@@ -325,8 +336,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_sync(2, 128);
         cur_nt = nt;
       }
-      const int acc = tl & 1;
-      const int m = mt * kBM + ew * 32 + lane;
+      const int acc = tl % p.nacc, use = tl / p.nacc;
+      mbar_wait_backoff(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int ncol = min(p.BN, p.ncols - nt * p.BN);
+      for (int sub = 0; sub < msub; ++sub) {
+      const int m = (mt * msub + sub) * kBM + ew * 32 + lane;
       bool live = m < p.M;
       int h0 = 0, w0 = 0;
       float* obase = p.out;
@@ -338,10 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         w0 = int(gj) * p.osw - p.opw;
         obase = p.out + std::int64_t(n) * p.oimg + std::int64_t(h0) * p.Wo + w0;
       }
-      mbar_wait_backoff(&tfull[acc], (tl >> 1) & 1);
-      tc_fence_after();
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
-      const int ncol = min(p.BN, p.ncols - nt * p.BN);
+      const std::uint32_t tbase =
+          tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t((acc * msub + sub) * p.BN);
       for (int c0 = 0; c0 < ncol; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -356,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             *dst = p.beta == 0.f ? val : val + p.beta * *dst;
           }
         }
+      }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -397,7 +411,11 @@ int pick_bn(int n) {
 // Fills the op-independent fields and launches.
 cudaError_t zlaunch(ZParams p, cudaStream_t st) {
   p.BN = pick_bn(p.ncols);
-  p.m_tiles = (p.M + kBM - 1) / kBM;
+  // two position sub-tiles per tile once there are enough positions to keep
+  // every SM busy with them: each B stage then feeds 2x the MMA work
+  p.msub = tune("z_msub", p.M >= 2 * kBM * 2 * sm_count() ? 2 : 1) == 2 ? 2 : 1;
+  p.nacc = 2 * p.msub * p.BN <= 512 ? 2 : 1;
+  p.m_tiles = (p.M + p.msub * kBM - 1) / (p.msub * kBM);
   p.n_tiles = (p.ncols + p.BN - 1) / p.BN;
   p.chunks = (p.Kr + 31) / 32;
   p.fd_HWg = FastDiv(std::uint32_t(p.Hg * p.Wg));
@@ -415,15 +433,15 @@ cudaError_t zlaunch(ZParams p, cudaStream_t st) {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  const int stage_bytes = int(kABytes) + ((p.BN * 128 + 1023) & ~1023);
+  const int stage_bytes = p.msub * int(kABytes) + ((p.BN * 128 + 1023) & ~1023);
   p.stages = std::max(2, std::min({kMaxStages, tune("z_stages", 8), (200 * 1024) / stage_bytes}));
   const int smem = p.stages * stage_bytes + 1024 + 256;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(zgemm_kernel), smem);
   if (e != cudaSuccess) return e;
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, sm_count());
-  trace_variant("zgemm bmode=%d m_tiles=%d n_tiles=%d BN=%d chunks=%d stages=%d grid=%d", p.bmode, p.m_tiles,
-                p.n_tiles, p.BN, p.chunks, p.stages, grid);
+  trace_variant("zgemm bmode=%d m_tiles=%d n_tiles=%d BN=%d msub=%d nacc=%d chunks=%d stages=%d grid=%d", p.bmode,
+                p.m_tiles, p.n_tiles, p.BN, p.msub, p.nacc, p.chunks, p.stages, grid);
   return launch_pdl(zgemm_kernel, dim3(grid), dim3(kThreads), std::size_t(smem), st, bmap, p);
 }
 

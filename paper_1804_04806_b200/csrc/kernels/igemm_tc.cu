@@ -70,6 +70,7 @@ struct ZParams {
   int Cs, Hs, Ws, HWs;
   long long simg;  // Cs*Hs*Ws
   int Hg, Wg, M;
+  int gi0, gj0;  // grid origin: position (gi, gj) stands for grid point (gi + gi0, gj + gj0)
   int gsh, gsw, gph, gpw;
   int T, U, Kr, chunks;
   int ncols, BN, m_tiles, n_tiles;
@@ -154,6 +155,7 @@ __device__ __forceinline__ ColEnt col_entry(const ZParams& p, int col) {
   return e;
 }
 
+template <int MSUB>
 __global__ void __launch_bounds__(kThreads, 1)
     zgemm_kernel(const __grid_constant__ CUtensorMap bmap, const ZParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t b_bytes = (std::uint32_t(p.BN) * 128 + 1023) & ~1023u;
-  const int msub = p.msub;
+  constexpr int msub = MSUB;
   const std::uint32_t stage_bytes = msub * kABytes + b_bytes;
   const int kStages = p.stages;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           std::uint32_t n, g, gi, gj;
           p.fd_HWg.divmod(std::uint32_t(m), n, g);
           p.fd_Wg.divmod(g, gi, gj);
-          const int ihb = int(gi) * p.gsh - p.gph, iwb = int(gj) * p.gsw - p.gpw;
+          const int ihb = (int(gi) + p.gi0) * p.gsh - p.gph, iwb = (int(gj) + p.gj0) * p.gsw - p.gpw;
           vr[sub] = range_mask(-ihb, p.Hs - ihb, p.T);
           vs[sub] = range_mask(-iwb, p.Ws - iwb, p.U);
           base[sub] = p.src + std::int64_t(n) * p.simg + std::int64_t(ihb) * p.Ws + iwb;
@@ -349,8 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         std::uint32_t n, g, gi, gj;
         p.fd_HWg.divmod(std::uint32_t(m), n, g);
         p.fd_Wg.divmod(g, gi, gj);
-        h0 = int(gi) * p.osh - p.oph;
-        w0 = int(gj) * p.osw - p.opw;
+        h0 = (int(gi) + p.gi0) * p.osh - p.oph;
+        w0 = (int(gj) + p.gj0) * p.osw - p.opw;
         obase = p.out + std::int64_t(n) * p.oimg + std::int64_t(h0) * p.Wo + w0;
       }
       const std::uint32_t tbase =
@@ -436,13 +438,14 @@ cudaError_t zlaunch(ZParams p, cudaStream_t st) {
   const int stage_bytes = p.msub * int(kABytes) + ((p.BN * 128 + 1023) & ~1023);
   p.stages = std::max(2, std::min({kMaxStages, tune("z_stages", 8), (200 * 1024) / stage_bytes}));
   const int smem = p.stages * stage_bytes + 1024 + 256;
-  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(zgemm_kernel), smem);
+  auto kern = p.msub == 2 ? zgemm_kernel<2> : zgemm_kernel<1>;
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, sm_count());
   trace_variant("zgemm bmode=%d m_tiles=%d n_tiles=%d BN=%d msub=%d nacc=%d chunks=%d stages=%d grid=%d", p.bmode,
                 p.m_tiles, p.n_tiles, p.BN, p.msub, p.nacc, p.chunks, p.stages, grid);
-  return launch_pdl(zgemm_kernel, dim3(grid), dim3(kThreads), std::size_t(smem), st, bmap, p);
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), std::size_t(smem), st, bmap, p);
 }
 
 }  // namespace
@@ -490,8 +493,13 @@ cudaError_t zgemm_backward_data(const ConvShape& s, const float* dy, const float
   p.src = dy; p.w = w; p.out = dx; p.alpha = alpha; p.beta = beta;
   p.Cs = s.K; p.Hs = s.OH(); p.Ws = s.OW(); p.HWs = p.Hs * p.Ws;
   p.simg = std::int64_t(s.K) * p.Hs * p.Ws;
-  p.Hg = (s.H - 1 + s.ph) / s.sh + 1;
-  p.Wg = (s.W - 1 + s.pw) / s.sw + 1;
+  // grid points i with some phase a landing in [0, H): i*sh + a - ph >= 0 for
+  // a <= sh - 1 needs i >= ph / sh (floor); i*sh - ph <= H - 1 needs
+  // i <= (H - 1 + ph) / sh
+  p.gi0 = s.ph / s.sh;
+  p.gj0 = s.pw / s.sw;
+  p.Hg = (s.H - 1 + s.ph) / s.sh + 1 - p.gi0;
+  p.Wg = (s.W - 1 + s.pw) / s.sw + 1 - p.gj0;
   p.M = s.N * p.Hg * p.Wg;
   p.gsh = 1; p.gsw = 1; p.gph = Th - 1; p.gpw = Tw - 1;
   p.T = Th; p.U = Tw;

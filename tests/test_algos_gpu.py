@@ -162,12 +162,18 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("bfl_xmn=1", "3 5 13 13 7 5 5 2 1 2 6"),
                                        ("z=0", "2 3 31 31 16 11 11 2 4 0 0"),
                                        ("z=0", "2 16 15 15 32 3 3 1 2 1 0"),
-                                       ("z=0", "3 8 9 7 24 3 3 0 1 2 0")])
+                                       ("z=0", "3 8 9 7 24 3 3 0 1 2 0"),
+                                       ("z_msub=2", "3 5 13 13 7 5 5 2 1 0 0"),
+                                       ("z_msub=2", "3 5 13 13 7 5 5 2 1 1 0"),
+                                       ("z_msub=2", "2 3 31 31 16 11 11 2 4 1 0"),
+                                       ("z_msub=2", "4 40 9 9 300 3 3 1 1 0 0"),
+                                       ("z_msub=2", "4 40 9 9 300 3 3 1 1 1 0")])
 def test_knob_variants(cuda, tune, spec):
-    """Off-by-default variants kept exact: the gather BackwardFilter with
-    MN-major x rows (bfl_xmn=1) and algorithm 0's SIMT-gather fallback
-    (z=0, used by shapes the tcgen05 kernel does not take); UCUDNN_TUNE is
-    read once per process, so each runs in a child."""
+    """Variants the default shapes here do not reach, kept exact: the gather
+    BackwardFilter with MN-major x rows (bfl_xmn=1), algorithm 0's
+    SIMT-gather fallback (z=0, shapes the tcgen05 kernel does not take) and
+    its two-sub-tile mode (z_msub=2, chosen automatically only at large
+    batch); UCUDNN_TUNE is read once per process, so each runs in a child."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, UCUDNN_TUNE=tune)

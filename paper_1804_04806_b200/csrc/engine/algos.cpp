@@ -11,6 +11,7 @@
 
 #include "../kernels/bdscatter.h"
 #include "../kernels/bflsu.h"
+#include "../kernels/bfs.h"
 #include "../kernels/bfnhwc.h"
 #include "../kernels/fft.h"
 #include "../kernels/gemm.h"
@@ -114,15 +115,18 @@ cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b
 // straight from NCHW x / dy (bflsu.cu: a small fixed workspace instead of
 // PRECOMP's per-image copies), and BackwardData of few-channel strided layers
 // as GEMM + col2im fused through a shared-memory patch (bdscatter.cu).
+// Few-channel strided BackwardFilter (AlexNet / ResNet conv1) takes the
+// shared-memory patch kernel (bfs.cu) instead of the strided L2 gather.
 bool gather_supports(int op, const ConvShape& s) {
-  return (op == 2 && bfl_supports(s)) || (op == 1 && bds_supports(s));
+  return (op == 2 && (bfs_supports(s) || bfl_supports(s))) || (op == 1 && bds_supports(s));
 }
 std::int64_t gather_workspace(int op, const ConvShape& s) {
-  return op == 2 ? bfl_workspace(s) : op == 1 ? bds_workspace(s) : 0;
+  if (op == 2) return bfs_supports(s) ? bfs_workspace(s) : bfl_workspace(s);
+  return op == 1 ? bds_workspace(s) : 0;
 }
 cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                        float beta, cudaStream_t st, int) {
-  if (op == 2) return bfl_run(s, a, b, out, ws, alpha, beta, st);
+  if (op == 2) return bfs_supports(s) ? bfs_run(s, a, b, out, ws, alpha, beta, st) : bfl_run(s, a, b, out, ws, alpha, beta, st);
   if (op == 1) return bds_run(s, a, b, out, alpha, beta, st);
   return cudaErrorInvalidValue;
 }

@@ -218,10 +218,14 @@ ucudnnStatus_t ucudnnConvolutionBackwardFilter(UcudnnHandle_t h, const void* alp
 
 /* ------------------------------------------------------------ benchmarker  */
 /* Times one (op, shape, algorithm, micro-batch) on the handle's stream with
- * CUDA events (median of `iters` after `warmup`) and reports the workspace it
- * needs. *feasible = 0 when the algorithm does not support the shape. This
- * produces the rows of the reference cost table (CostRecord,
- * domain.hpp:300-318); ucudnnBenchmarkKernel below writes them. */
+ * CUDA events (medians of `iters` L2-flushed runs after `warmup`) and reports
+ * the workspace it needs. *feasible = 0 when the algorithm does not support
+ * the shape (or its workspace does not fit in device memory). The cost is the
+ * steady-state micro-batch time plus the batch-independent filter preparation
+ * amortised over the ceil(N / micro_batch) micro-batches of a uniform plan
+ * (here, with no full batch known, N = micro_batch: preparation charged in
+ * full); ucudnnBenchmarkKernel charges it over the kernel's batch. These are
+ * the rows of the reference cost table (CostRecord, domain.hpp:300-318). */
 ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_t* shape11, int algo,
                                    int64_t micro_batch, double* time_us, int64_t* ws_bytes, int* feasible);
 /* Benchmarks every algorithm x policy size for one kernel into the handle's

@@ -238,11 +238,20 @@ bool ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
   return true;
 }
 
-// Median CUDA-event time of one algorithm at one micro-batch, in integer ns,
-// on `h`'s device and `stream` (the caller has made that device current);
-// -1 when its workspace does not fit in device memory.
+// CUDA-event cost of one algorithm at one micro-batch, in integer ns, on
+// `h`'s device and `stream` (the caller has made that device current); -1
+// when its workspace does not fit in device memory.
+//
+// The cost charged is the steady-state micro-batch time plus the
+// batch-independent filter preparation (packing, Winograd / FFT filter
+// transforms) amortised over the ceil(B / b) micro-batches a plan of size-b
+// micro-batches makes: the executor prepares the filter once per run of
+// same-algorithm micro-batches (kFilterReady), so a uniform plan's summed
+// cost (the reference's model, cost_provider.hpp:117-127) is then exactly
+// prep + k * steady. Both times are medians over `iters` interleaved runs,
+// each preceded by an L2 flush.
 std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters, int op, const ConvShape& s,
-                       int algo, std::int64_t ws) {
+                       int algo, std::int64_t ws, std::int64_t full_batch) {
   const AlgoImpl* a = find_algo(algo);
   // sub-buffers 256 B aligned, as a framework's allocations are: TMA maps
   // built on user tensors (dy read in place) need 16 B aligned bases
@@ -262,32 +271,30 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
   }
-  // every timed run is a whole call, filter packing / transforms included
-  // (each micro-batch is costed as the independent call the reference's
-  // model sums, cost_provider.hpp:117-127; the executor's reuse of a packed
-  // filter across a run of same-algorithm micro-batches is a saving the
-  // table does not claim)
   for (int i = 0; i < std::max(1, warmup); ++i)
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, 0), "benchmark warm-up");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, i ? kFilterReady : 0), "benchmark warm-up");
   if (h->flush_bytes == std::size_t(-1)) {
     const char* e = std::getenv("UCUDNN_BENCH_FLUSH_MB");
     h->flush_bytes = std::size_t(e ? std::max(0, std::atoi(e)) : 256) << 20;
     if (h->flush_bytes) cuda_check(cudaMalloc(&h->flush, h->flush_bytes), "cudaMalloc(L2 flush buffer)");
   }
-  std::vector<float> ms;
-  for (int i = 0; i < std::max(1, iters); ++i) {
+  std::vector<float> ms[2];  // [0] whole call (filter prepared), [1] steady state (kFilterReady)
+  for (int i = 0; i < 2 * std::max(1, iters); ++i) {
+    const int kind = i & 1;
     if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, stream), "L2 flush");
     cuda_check(cudaEventRecord(h->ev0, stream), "cudaEventRecord");
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, 0), "benchmark run");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kind ? kFilterReady : 0), "benchmark run");
     cuda_check(cudaEventRecord(h->ev1, stream), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(h->ev1), "cudaEventSynchronize");
     float t = 0;
     cuda_check(cudaEventElapsedTime(&t, h->ev0, h->ev1), "cudaEventElapsedTime");
-    ms.push_back(t);
+    ms[kind].push_back(t);
   }
-  std::sort(ms.begin(), ms.end());
-  double med = ms[ms.size() / 2];
-  std::int64_t ns = std::int64_t(med * 1e6 + 0.5);
+  for (auto& v : ms) std::sort(v.begin(), v.end());
+  const double whole = ms[0][ms[0].size() / 2], steady = ms[1][ms[1].size() / 2];
+  const double prep = std::max(0.0, whole - steady);
+  const std::int64_t micros = std::max<std::int64_t>(1, (full_batch + s.N - 1) / s.N);
+  std::int64_t ns = std::int64_t((steady + prep / double(micros)) * 1e6 + 0.5);
   return std::max<std::int64_t>(ns, 1);
 }
 
@@ -321,7 +328,8 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   if (jobs.empty()) return;
   const int op = int(k.op);
   if (h->slots.empty()) {
-    for (Job& j : jobs) j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws);
+    for (Job& j : jobs)
+      j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws, k.batch);
   } else {
     std::atomic<std::size_t> next{0};
     std::exception_ptr err;
@@ -339,7 +347,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
               if (err) return;
             }
             Job& j = jobs[i];
-            j.ns = time_once(sl, sl->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws);
+            j.ns = time_once(sl, sl->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws, k.batch);
           }
         } catch (...) {
           std::lock_guard<std::mutex> lock(err_mu);
@@ -425,6 +433,10 @@ void execute(ucudnnContext* h, int op, const ConvShape& full, const Plan& plan, 
     require(impl != nullptr, "plan uses an algorithm this build does not provide");
     ConvShape s = full;
     s.N = int(m.batch);
+    // the plan's workspace came from a cost table, which may predate this
+    // build's kernels: never run a micro-batch on less than it really needs
+    require(impl->workspace(op, s) <= std::int64_t(ws_bytes) || (impl->workspace(op, s) == 0),
+            "micro-batch needs more workspace than its cost-table row says (stale cost table?)");
     cudaError_t e;
     const bool same_prev = i > 0 && ms[i - 1].alg == m.alg, same_next = i + 1 < ms.size() && ms[i + 1].alg == m.alg;
     int flags = same_prev ? kFilterReady : 0;
@@ -921,7 +933,8 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     std::int64_t ws = algo_ws(int(op), s, algo, &ok);
     *feasible = ok ? 1 : 0;
     *ws_bytes = ws;
-    const std::int64_t ns = ok ? time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws) : 0;
+    // a single timing charges the filter preparation in full (one micro-batch)
+    const std::int64_t ns = ok ? time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws, s.N) : 0;
     if (ns < 0) *feasible = 0;
     *time_us = ns > 0 ? double(ns) / 1000.0 : 0.0;
     return UCUDNN_STATUS_SUCCESS;

@@ -40,10 +40,11 @@ using namespace sm100;
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kProd = 8;
+constexpr int kProd = 16;
+constexpr int kRowsPer = 24;  // x rows per producer thread (rows_pad <= 16 * 24 = 384)
 constexpr int kThreads = (5 + kProd) * 32;
 constexpr int kStages = 2;
-constexpr int kMaxRows = 512;
+constexpr int kMaxRows = kProd * kRowsPer;
 
 struct SGeo {
   int N, C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
@@ -171,6 +172,17 @@ __global__ void __launch_bounds__(kThreads, 1) bfs_kernel(const SParams p) {
       named_sync(1, kProd * 32);
     }
     const std::uint32_t bsw = std::uint32_t(lane >> 2), bl = std::uint32_t(lane & 3) * 4;
+    // this thread's x rows q = pw + kProd * i: patch offset and B-tile
+    // destination, in registers (the build loop is then kRowsPer independent
+    // LDS -> STS pairs instead of a dependent table walk)
+    int po[kRowsPer];
+    std::uint32_t bd[kRowsPer];
+#pragma unroll
+    for (int i = 0; i < kRowsPer; ++i) {
+      const int q = pw + kProd * i;
+      po[i] = q < p.rows_pad ? pofs[q] : -2;
+      bd[i] = std::uint32_t(q) * 128 + ((bsw ^ std::uint32_t(q & 7)) << 4) + bl;
+    }
     for (int i = 0; i < my_units; ++i) {
       const int u = blockIdx.x + i * gridDim.x;
       const int n = u / p.OH, oh = u - n * p.OH;
@@ -181,14 +193,16 @@ __global__ void __launch_bounds__(kThreads, 1) bfs_kernel(const SParams p) {
         mbar_wait(&empty[st], ph ^ 1);
         const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
         // B: x rows of this step from the patch
-        for (int q = pw; q < p.rows_pad; q += kProd) {
-          const int o = pofs[q];
-          float v = 0.f;
-          if (o >= 0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(Pb + std::uint32_t(o + ow0) * 4) : "memory");
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + std::uint32_t(q) * 128 + ((bsw ^ std::uint32_t(q & 7)) << 4) + bl),
-                       "f"(v)
-                       : "memory");
+        float v[kRowsPer];
+        const std::uint32_t pst = Pb + std::uint32_t(ow0) * 4;
+#pragma unroll
+        for (int r = 0; r < kRowsPer; ++r) {
+          v[r] = 0.f;
+          if (po[r] >= 0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[r]) : "r"(pst + std::uint32_t(po[r]) * 4));
         }
+#pragma unroll
+        for (int r = 0; r < kRowsPer; ++r)
+          if (po[r] != -2) asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + bd[r]), "f"(v[r]) : "memory");
         // A: dy rows k of the step's 32 pixels (zero past the row's end)
         const bool pok = ow0 + lane < p.OW;
         for (int k = pw; k < p.K; k += kProd)

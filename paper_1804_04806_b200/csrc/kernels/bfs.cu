@@ -43,7 +43,7 @@ constexpr int kBM = 128;
 constexpr int kProd = 16;
 constexpr int kRowsPer = 24;  // x rows per producer thread (rows_pad <= 16 * 24 = 384)
 constexpr int kThreads = (5 + kProd) * 32;
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;
 constexpr int kMaxRows = kProd * kRowsPer;
 
 struct SGeo {
@@ -54,6 +54,7 @@ struct SGeo {
   int units;                   // output rows N*OH
   int grid;
   std::size_t p_bytes, b_bytes, stage_bytes, smem;
+  int stages;
 };
 
 struct SParams {
@@ -63,6 +64,7 @@ struct SParams {
   int C, H, W, K, R, S, ph, pw, sh, shl, OH, OW;  // shl = log2(sh)
   int rows, rows_pad, n1, n2, steps, JP, units;
   int p_floats;  // one P buffer
+  int stages;
   long long CHW, KOHW;
 };
 
@@ -103,12 +105,16 @@ __device__ __forceinline__ void fill_patch(const SParams& p, int u, std::uint32_
     const int ih = oh * p.sh - p.ph + r;
     const bool rok = unsigned(ih) < unsigned(p.H);
     const float* row = xn + ((long long)c * p.H + (rok ? ih : 0)) * p.W;
-    const std::uint32_t pr = pb + std::uint32_t(cr * p.sh * p.JP) * 4;
-    for (int col = lane; col < cols; col += 32) {
-      const int iw = col - p.pw;
-      const bool ok = rok && unsigned(iw) < unsigned(p.W);
-      const int b = col & (p.sh - 1), j = col >> p.shl;
-      cp_async4(pr + std::uint32_t(b * p.JP + j) * 4, row + (ok ? iw : 0), ok ? 4u : 0u);
+    // column col = lane + 32 * it: its phase b = lane % sh is fixed per lane
+    // (sh divides 32) and j advances by 32 / sh per iteration
+    const std::uint32_t dst0 =
+        pb + std::uint32_t(cr * p.sh * p.JP + (lane & (p.sh - 1)) * p.JP + (lane >> p.shl)) * 4;
+    const std::uint32_t jstep = std::uint32_t(32 >> p.shl) * 4;
+    const float* src0 = row + lane - p.pw;
+    const int iw0 = lane - p.pw;
+    for (int it = 0; it * 32 < cols; ++it) {
+      const bool ok = rok && unsigned(iw0 + 32 * it) < unsigned(p.W);
+      cp_async4(dst0 + std::uint32_t(it) * jstep, ok ? src0 + 32 * it : row, ok ? 4u : 0u);
     }
   }
   cp_async_commit();
@@ -123,10 +129,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfs_kernel(const SParams p) {
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = (std::uint32_t(p.rows_pad) * 128 + 1023) & ~1023u;
   const std::uint32_t stage_bytes = a_bytes + b_bytes;
+  const int kStages = p.stages;
   float* P = reinterpret_cast<float*>(smem + kStages * stage_bytes);  // two buffers of p_floats
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(P + 2 * p.p_floats);
-  std::uint64_t* empty = full + kStages;
-  std::uint64_t* tfull = empty + kStages;
+  std::uint64_t* empty = full + kMaxStages;
+  std::uint64_t* tfull = empty + kMaxStages;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tfull + 1);
   __shared__ int pofs[kMaxRows];  // x row q -> offset of its run in a P buffer (-1: padding row)
 
@@ -330,7 +337,13 @@ SGeo make_sgeo(const ConvShape& s) {
   g.p_bytes = std::size_t(s.C) * s.R * s.sw * g.JP * 4;
   g.b_bytes = (std::size_t(g.rows_pad) * 128 + 1023) & ~std::size_t(1023);
   g.stage_bytes = kBM * 128 + g.b_bytes;
-  g.smem = kStages * g.stage_bytes + 2 * g.p_bytes + 1024 + 128;
+  // as many ring stages as fit next to the two patch buffers (2..4)
+  g.stages = 2;
+  while (g.stages < kMaxStages && (g.stages + 1) * g.stage_bytes + 2 * g.p_bytes + 1024 + 128 <= 220 * 1024)
+    ++g.stages;
+  g.stages = std::min(g.stages, tune("bfs_stages", kMaxStages));
+  g.stages = std::max(g.stages, 2);
+  g.smem = g.stages * g.stage_bytes + 2 * g.p_bytes + 1024 + 128;
   return g;
 }
 
@@ -358,12 +371,13 @@ cudaError_t bfs_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.rows = g.rows; p.rows_pad = g.rows_pad; p.n1 = g.n1; p.n2 = g.n2; p.steps = g.steps; p.JP = g.JP;
   p.units = g.units;
   p.p_floats = int(g.p_bytes / 4);
+  p.stages = g.stages;
   p.CHW = std::int64_t(g.C) * g.H * g.W;
   p.KOHW = std::int64_t(g.K) * g.OH * g.OW;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(bfs_kernel), int(g.smem));
   if (e != cudaSuccess) return e;
-  trace_variant("bfs units=%d grid=%d rows=%d n1=%d n2=%d steps=%d JP=%d", g.units, g.grid, g.rows, g.n1, g.n2, g.steps,
-                g.JP);
+  trace_variant("bfs units=%d grid=%d rows=%d n1=%d n2=%d steps=%d JP=%d stages=%d", g.units, g.grid, g.rows, g.n1,
+                g.n2, g.steps, g.JP, g.stages);
   e = launch_pdl(bfs_kernel, dim3(g.grid), dim3(kThreads), g.smem, st, p);
   if (e != cudaSuccess) return e;
   SFinal f{p.slices, dw, alpha, beta, g.rows, g.K, g.grid};

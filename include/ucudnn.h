@@ -133,6 +133,15 @@ ucudnnStatus_t ucudnnSetTotalWorkspaceLimit(UcudnnHandle_t h, int64_t bytes);
 ucudnnStatus_t ucudnnSetCostDatabase(UcudnnHandle_t h, const char* csv_path);
 ucudnnStatus_t ucudnnFlushCostDatabase(UcudnnHandle_t h);
 ucudnnStatus_t ucudnnSetBenchmarkIterations(UcudnnHandle_t h, int warmup, int iters);
+/* Deterministic BackwardFilter (cudnnSetConvolutionMathType-style knob; no
+ * reference counterpart -- the reference's fp64 loops are deterministic by
+ * construction, reference_conv.hpp:141-171). on != 0: every BackwardFilter
+ * kernel gives each dW partial a single writer per launch (split-K off; the
+ * few-channel patch kernel adds per-CTA slices in a fixed order), so dW is
+ * bit-identical run to run on any data. Costs speed on split-K shapes; the
+ * benchmarker times this mode's kernels, so keep one cost database per mode.
+ * Env mirror: UCUDNN_DETERMINISTIC=1. Re-plans the handle's kernels. */
+ucudnnStatus_t ucudnnSetDeterministic(UcudnnHandle_t h, int on);
 /* Parallel benchmarking ("evaluate in parallel on multiple
  * GPUs"): the missing (algorithm x micro-batch) rows
  * of a kernel are timed by one host thread per listed device, each with its own

@@ -163,7 +163,7 @@ class Handle:
     """UcudnnHandle_t: device, stream, plans, cost table, WD arena."""
 
     def __init__(self, policy: str = "powerOfTwo", mode: str = "wr", total_workspace: int = 0,
-                 database: Optional[str] = None, stream=None):
+                 database: Optional[str] = None, stream=None, deterministic: bool = False):
         self._l = lib()
         self._h = C.c_void_p()
         check(self._l.ucudnnCreate(C.byref(self._h)))
@@ -178,6 +178,8 @@ class Handle:
             check(self._l.ucudnnSetCostDatabase(self._h, database.encode()))
         if stream is not None:
             self.set_stream(stream)
+        if deterministic:
+            self.set_deterministic(True)
 
     def close(self):
         if self._h:
@@ -203,6 +205,10 @@ class Handle:
 
     def set_total_workspace(self, nbytes: int) -> None:
         check(self._l.ucudnnSetTotalWorkspaceLimit(self._h, nbytes))
+
+    def set_deterministic(self, on: bool) -> None:
+        """Run-to-run bit-identical BackwardFilter (no split-K atomics)."""
+        check(self._l.ucudnnSetDeterministic(self._h, 1 if on else 0))
 
     def set_benchmark_iterations(self, warmup: int, iters: int) -> None:
         check(self._l.ucudnnSetBenchmarkIterations(self._h, warmup, iters))

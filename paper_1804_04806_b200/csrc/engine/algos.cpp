@@ -28,6 +28,12 @@ void count_launch(int n) { g_launches.fetch_add(std::uint64_t(n), std::memory_or
 std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
+thread_local bool t_det = false;
+}  // namespace
+bool deterministic() { return t_det; }
+void set_deterministic(bool on) { t_det = on; }
+
+namespace {
 std::atomic<bool> g_trace{false};
 std::mutex g_trace_mu;
 std::string g_trace_buf;

@@ -70,6 +70,14 @@ ucudnnStatus_t guarded(F&& body) {
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
+
+// The handle's deterministic setting on the launching host thread for the
+// duration of a call (kernel launchers read it when sizing split-K grids).
+struct DetScope {
+  bool prev;
+  explicit DetScope(bool on) : prev(deterministic()) { set_deterministic(on); }
+  ~DetScope() { set_deterministic(prev); }
+};
 }  // namespace
 
 struct ucudnnTensorStruct {
@@ -90,6 +98,7 @@ struct ucudnnContext {
   std::int64_t total_ws = 0;
   std::int64_t report_limit = 0;
   int warmup = 3, iters = 10;
+  bool deterministic = false;  // ucudnnSetDeterministic / UCUDNN_DETERMINISTIC
   std::unique_ptr<CostTable> table = std::make_unique<CostTable>();
   std::string db_path;
 
@@ -328,6 +337,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   if (jobs.empty()) return;
   const int op = int(k.op);
   if (h->slots.empty()) {
+    DetScope det(h->deterministic);
     for (Job& j : jobs)
       j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws, k.batch);
   } else {
@@ -339,6 +349,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
       BenchSlot* sl = slot.get();
       workers.emplace_back([&, sl] {
         try {
+          DetScope det(h->deterministic);
           cuda_check(cudaSetDevice(sl->device), "cudaSetDevice(benchmark device)");
           if (!sl->stream) cuda_check(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
           for (std::size_t i = next++; i < jobs.size(); i = next++) {
@@ -469,6 +480,7 @@ Plan undivided(int algo, const ConvShape& s, int op) {
 
 ucudnnStatus_t run_conv(ucudnnContext* h, int op, const ConvShape& s, int algo, const float* a, const float* b,
                         float* out, void* ws, std::size_t ws_bytes, float alpha, float beta) {
+  DetScope det(h->deterministic);
   if (algo >= UCUDNN_VIRTUAL_ALGO_BASE) {
     auto& e = entry_of(h, algo);
     require(int(e.kernel.op) == op, "virtual algorithm belongs to another operation");
@@ -578,6 +590,7 @@ ucudnnStatus_t ucudnnCreate(UcudnnHandle_t* out) {
     if (const char* v = std::getenv("UCUDNN_WORKSPACE_MODE")) h->mode = std::string(v) == "wd" ? Mode::WD : Mode::WR;
     if (const char* v = std::getenv("UCUDNN_TOTAL_WORKSPACE_SIZE")) h->total_ws = std::atoll(v);
     if (const char* v = std::getenv("UCUDNN_BENCHMARK_ITERS")) h->iters = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("UCUDNN_DETERMINISTIC")) h->deterministic = std::atoi(v) != 0;
     if (const char* v = std::getenv("UCUDNN_DATABASE")) {
       h->db_path = v;
       h->table = CostTable::open(v);
@@ -670,6 +683,22 @@ ucudnnStatus_t ucudnnSetBenchmarkDevices(UcudnnHandle_t h, const int* device_ids
       auto sl = std::make_unique<BenchSlot>();
       sl->device = d;
       h->slots.push_back(std::move(sl));
+    }
+    return UCUDNN_STATUS_SUCCESS;
+  });
+}
+
+ucudnnStatus_t ucudnnSetDeterministic(UcudnnHandle_t h, int on) {
+  return guarded([&] {
+    require(h, "null handle");
+    if (h->deterministic != (on != 0)) {
+      // the cost rows and plans so far were timed in the other mode: start
+      // from an empty table (a database file must be set again, per mode)
+      h->deterministic = on != 0;
+      h->table = std::make_unique<CostTable>();
+      h->db_path.clear();
+      for (auto& e : h->entries) e.planned = false;
+      h->wd_stale = true;
     }
     return UCUDNN_STATUS_SUCCESS;
   });
@@ -933,6 +962,7 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     std::int64_t ws = algo_ws(int(op), s, algo, &ok);
     *feasible = ok ? 1 : 0;
     *ws_bytes = ws;
+    DetScope det(h->deterministic);
     // a single timing charges the filter preparation in full (one micro-batch)
     const std::int64_t ns = ok ? time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws, s.N) : 0;
     if (ns < 0) *feasible = 0;

@@ -770,7 +770,7 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
     return launch_pdl(bf_finalize_kernel, dim3(int(std::min<std::int64_t>((f2.n + 255) / 256, 8 * sms))), dim3(256), 0,
                       st, f2);
   }
-  int splits = std::max(1, std::min(p.steps / 8, tune("bf_waves", 1) * sms / p.tiles));
+  int splits = deterministic() ? 1 : std::max(1, std::min(p.steps / 8, tune("bf_waves", 1) * sms / p.tiles));
   p.ksub = std::max(1, std::min(kMaxSub, tune("bf_ksub", 1)));
   const int kSub = p.ksub;
   p.steps_per_unit = ((p.steps + splits - 1) / splits + kSub - 1) / kSub * kSub;

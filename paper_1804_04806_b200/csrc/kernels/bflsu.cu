@@ -833,7 +833,8 @@ cudaError_t bfl_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.xmn = g.swap && !p.sg && (g.C % 8 != 0 || p.crs) && tune("bfl_xmn", 0);
   // split the reduction so the tiles fill the SMs once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
-  const int splits = std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
+  const int splits =
+      deterministic() ? 1 : std::max(1, std::min(p.steps / 8, tune("bfl_waves", 1) * slots / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
   const int stage_bytes = (g.dual ? 2 : 1) * kBM * 128 + (((g.two ? g.BN / 2 : g.BN) * 128 + 1023) & ~1023);

@@ -694,7 +694,8 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   p.fd_OW = FastDiv(std::uint32_t(g.OW));
   // split the reduction so the tiles fill the SMs (or SM pairs) once, >= 8 steps per unit
   const int slots = g.two ? sms / 2 : sms;
-  const int splits = std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * slots / p.tiles));
+  const int splits =
+      deterministic() ? 1 : std::max(1, std::min(p.steps / 8, tune("bfn_waves", 1) * slots / p.tiles));
   p.steps_per_unit = (p.steps + splits - 1) / splits;
   p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;
   const int stage_bytes = ((4 * g.msub + g.BN / (g.two ? 64 : 32)) * g.px * 128 + 1023) & ~1023;

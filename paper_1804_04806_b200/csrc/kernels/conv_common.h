@@ -33,6 +33,13 @@ std::uint64_t launch_count();
 // launchers append one line per main-kernel launch naming the variant and
 // its tiling (e.g. "precomp2 m_tiles=729 n_tiles=1 clusters=74"), so tests can
 // prove which code path a bench-scale call exercised. Off: one atomic load.
+// Deterministic BackwardFilter (ucudnnSetDeterministic): set by the engine on
+// the launching host thread around a handle's calls; split-K launchers then
+// give each output element a single writer per launch (splits = 1), so dW no
+// longer depends on the order of fp32 atomic additions.
+bool deterministic();
+void set_deterministic(bool on);
+
 bool trace_on();
 void trace_variant(const char* fmt, ...);
 

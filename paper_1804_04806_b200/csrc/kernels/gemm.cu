@@ -422,7 +422,7 @@ cudaError_t gemm(const Problem& q, const float* a, const float* b, int epi, floa
   g.BN = q.BN;
   const int tiles = q.m_tiles * q.n_tiles;
   int splits = 1;
-  if (split_k) splits = std::max(1, std::min(q.ksteps / 16, cdiv(3 * sms(), tiles)));
+  if (split_k && !deterministic()) splits = std::max(1, std::min(q.ksteps / 16, cdiv(3 * sms(), tiles)));
   g.steps_per_unit = cdiv(q.ksteps, splits);
   g.splits = cdiv(q.ksteps, g.steps_per_unit);
   g.epi = epi;

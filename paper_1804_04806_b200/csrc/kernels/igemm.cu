@@ -481,7 +481,7 @@ cudaError_t igemm_backward_filter(const ConvShape& s, const float* x, const floa
   const int tiles = ((p.M + kBM - 1) / kBM) * ((p.Ng + p.BN - 1) / p.BN);
   const int chunks = (p.Kg + kChunk - 1) / kChunk;
   // split the pixel reduction so the grid covers ~2 waves, >= 8 chunks each
-  int splits = std::max(1, std::min(chunks / 8, (2 * num_sms() + tiles - 1) / tiles));
+  int splits = deterministic() ? 1 : std::max(1, std::min(chunks / 8, (2 * num_sms() + tiles - 1) / tiles));
   p.chunks_per_split = (chunks + splits - 1) / splits;
   splits = (chunks + p.chunks_per_split - 1) / p.chunks_per_split;
   return launch(kBwdFilter, p, (p.M + kBM - 1) / kBM, (p.Ng + p.BN - 1) / p.BN, splits, stream);

@@ -247,20 +247,15 @@ bool ensure_bench_ws(BenchSlot* h, std::size_t bytes) {
   return true;
 }
 
-// CUDA-event cost of one algorithm at one micro-batch, in integer ns, on
-// `h`'s device and `stream` (the caller has made that device current); -1
-// when its workspace does not fit in device memory.
-//
-// The cost charged is the steady-state micro-batch time plus the
+// CUDA-event steady-state time of one algorithm at one micro-batch, in
+// integer ns (median of `iters` L2-flushed runs with the filter operand
+// already prepared, kFilterReady), on `h`'s device and `stream` (the caller
+// has made that device current); -1 when its workspace does not fit in
+// device memory. With `prep_ms` non-null and negative, also measures the
 // batch-independent filter preparation (packing, Winograd / FFT filter
-// transforms) amortised over the ceil(B / b) micro-batches a plan of size-b
-// micro-batches makes: the executor prepares the filter once per run of
-// same-algorithm micro-batches (kFilterReady), so a uniform plan's summed
-// cost (the reference's model, cost_provider.hpp:117-127) is then exactly
-// prep + k * steady. Both times are medians over `iters` interleaved runs,
-// each preceded by an L2 flush.
+// transforms) as median(whole call) - median(steady) from interleaved runs.
 std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters, int op, const ConvShape& s,
-                       int algo, std::int64_t ws, std::int64_t full_batch) {
+                       int algo, std::int64_t ws, double* prep_ms = nullptr) {
   const AlgoImpl* a = find_algo(algo);
   // sub-buffers 256 B aligned, as a framework's allocations are: TMA maps
   // built on user tensors (dy read in place) need 16 B aligned bases
@@ -287,12 +282,13 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     h->flush_bytes = std::size_t(e ? std::max(0, std::atoi(e)) : 256) << 20;
     if (h->flush_bytes) cuda_check(cudaMalloc(&h->flush, h->flush_bytes), "cudaMalloc(L2 flush buffer)");
   }
-  std::vector<float> ms[2];  // [0] whole call (filter prepared), [1] steady state (kFilterReady)
-  for (int i = 0; i < 2 * std::max(1, iters); ++i) {
-    const int kind = i & 1;
+  const bool want_prep = prep_ms && *prep_ms < 0;
+  std::vector<float> ms[2];  // [0] steady state (kFilterReady), [1] whole call (filter prepared)
+  for (int i = 0; i < (want_prep ? 2 : 1) * std::max(1, iters); ++i) {
+    const int kind = want_prep ? (i & 1) : 0;
     if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, stream), "L2 flush");
     cuda_check(cudaEventRecord(h->ev0, stream), "cudaEventRecord");
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kind ? kFilterReady : 0), "benchmark run");
+    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kind ? 0 : kFilterReady), "benchmark run");
     cuda_check(cudaEventRecord(h->ev1, stream), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(h->ev1), "cudaEventSynchronize");
     float t = 0;
@@ -300,11 +296,21 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     ms[kind].push_back(t);
   }
   for (auto& v : ms) std::sort(v.begin(), v.end());
-  const double whole = ms[0][ms[0].size() / 2], steady = ms[1][ms[1].size() / 2];
-  const double prep = std::max(0.0, whole - steady);
-  const std::int64_t micros = std::max<std::int64_t>(1, (full_batch + s.N - 1) / s.N);
-  std::int64_t ns = std::int64_t((steady + prep / double(micros)) * 1e6 + 0.5);
-  return std::max<std::int64_t>(ns, 1);
+  const double steady = ms[0][ms[0].size() / 2];
+  if (want_prep) *prep_ms = std::max(0.0, double(ms[1][ms[1].size() / 2]) - steady);
+  return std::max<std::int64_t>(std::int64_t(steady * 1e6 + 0.5), 1);
+}
+
+// The cost a row charges: steady-state micro-batch time plus the filter
+// preparation amortised over the ceil(B / b) micro-batches a plan of size-b
+// micro-batches makes. The executor prepares the filter once per run of
+// same-algorithm micro-batches (kFilterReady), so a uniform plan's summed
+// cost (the reference's model, cost_provider.hpp:117-127) is exactly
+// prep + k * steady.
+std::int64_t row_cost_ns(std::int64_t steady_ns, double prep_ms, std::int64_t b, std::int64_t full_batch) {
+  if (steady_ns < 0) return -1;
+  const std::int64_t micros = std::max<std::int64_t>(1, (full_batch + b - 1) / b);
+  return std::max<std::int64_t>(1, steady_ns + std::int64_t(std::max(0.0, prep_ms) * 1e6 / double(micros) + 0.5));
 }
 
 // Fill missing cost rows for every algorithm x admissible micro-batch of a
@@ -336,10 +342,26 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   }
   if (jobs.empty()) return;
   const int op = int(k.op);
+  // filter preparation is batch-independent: measured once per algorithm,
+  // at its first (smallest) micro-batch, on the handle's own device
+  std::vector<double> prep(std::size_t(algo_count()), -1.0);
+  std::vector<char> done(jobs.size(), 0);
+  {
+    DetScope det(h->deterministic);
+    for (std::size_t i = 0; i < jobs.size(); ++i) {
+      Job& j = jobs[i];
+      if (prep[std::size_t(j.key.alg)] >= 0) continue;
+      j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws,
+                       &prep[std::size_t(j.key.alg)]);
+      if (j.ns < 0) prep[std::size_t(j.key.alg)] = -1.0;  // try the next size
+      else done[i] = 1;
+    }
+  }
   if (h->slots.empty()) {
     DetScope det(h->deterministic);
-    for (Job& j : jobs)
-      j.ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws, k.batch);
+    for (std::size_t i = 0; i < jobs.size(); ++i)
+      if (!done[i]) jobs[i].ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, jobs[i].s,
+                                           jobs[i].key.alg, jobs[i].ws);
   } else {
     std::atomic<std::size_t> next{0};
     std::exception_ptr err;
@@ -357,8 +379,9 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
               std::lock_guard<std::mutex> lock(err_mu);
               if (err) return;
             }
+            if (done[i]) continue;
             Job& j = jobs[i];
-            j.ns = time_once(sl, sl->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws, k.batch);
+            j.ns = time_once(sl, sl->stream, h->warmup, h->iters, op, j.s, j.key.alg, j.ws);
           }
         } catch (...) {
           std::lock_guard<std::mutex> lock(err_mu);
@@ -369,8 +392,10 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
     for (auto& t : workers) t.join();
     if (err) std::rethrow_exception(err);
   }
-  for (const Job& j : jobs)
+  for (Job& j : jobs) {
+    j.ns = row_cost_ns(j.ns, prep[std::size_t(j.key.alg)], j.key.batch, k.batch);
     h->table->put(j.ns < 0 ? CostRecord{j.key, Ratio(0), 0, false} : CostRecord{j.key, Ratio(j.ns, 1000), j.ws, true});
+  }
 }
 
 ucudnnContext::Entry& entry_of(ucudnnContext* h, int algo) {
@@ -964,7 +989,10 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     *ws_bytes = ws;
     DetScope det(h->deterministic);
     // a single timing charges the filter preparation in full (one micro-batch)
-    const std::int64_t ns = ok ? time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws, s.N) : 0;
+    double prep = -1.0;
+    const std::int64_t ns =
+        ok ? row_cost_ns(time_once(&h->primary, h->stream, h->warmup, h->iters, int(op), s, algo, ws, &prep), prep, 1, 1)
+           : 0;
     if (ns < 0) *feasible = 0;
     *time_us = ns > 0 ? double(ns) / 1000.0 : 0.0;
     return UCUDNN_STATUS_SUCCESS;

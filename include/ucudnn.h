@@ -54,6 +54,15 @@ typedef enum {
 /* Workspace modes (reference OptMode, report.hpp:32-36). */
 typedef enum { UCUDNN_WORKSPACE_WR = 0, UCUDNN_WORKSPACE_WD = 1 } ucudnnWorkspaceMode_t;
 
+/* Math modes (cudnnMathType_t-style). TF32: every GEMM-class kernel reads its
+ * fp32 operands as TF32 (10-bit mantissa) with fp32 accumulation -- normwise
+ * error ~1e-3 on Gaussian data. FP32_FAITHFUL ("3xTF32"): each micro-batch
+ * runs three TF32 passes over hi / lo operand splits, conv(a_hi, b_hi) +
+ * conv(a_lo, b_hi) + conv(a_hi, b_lo), for fp32-level error (~1e-6) at ~3x
+ * the tensor work and 2 x (|a| + |b|) extra workspace, which the cost table
+ * and planner account for. */
+typedef enum { UCUDNN_MATH_TF32 = 0, UCUDNN_MATH_FP32_FAITHFUL = 1 } ucudnnMathMode_t;
+
 typedef enum {
   UCUDNN_OP_FORWARD = 0,
   UCUDNN_OP_BACKWARD_DATA = 1,
@@ -142,6 +151,10 @@ ucudnnStatus_t ucudnnSetBenchmarkIterations(UcudnnHandle_t h, int warmup, int it
  * benchmarker times this mode's kernels, so keep one cost database per mode.
  * Env mirror: UCUDNN_DETERMINISTIC=1. Re-plans the handle's kernels. */
 ucudnnStatus_t ucudnnSetDeterministic(UcudnnHandle_t h, int on);
+/* Math mode (above). Env mirror: UCUDNN_MATH_MODE=fp32|tf32. Like
+ * ucudnnSetDeterministic it starts an empty cost table (rows are mode
+ * specific; set a per-mode database again) and re-plans. */
+ucudnnStatus_t ucudnnSetMathMode(UcudnnHandle_t h, ucudnnMathMode_t mode);
 /* Parallel benchmarking ("evaluate in parallel on multiple
  * GPUs"): the missing (algorithm x micro-batch) rows
  * of a kernel are timed by one host thread per listed device, each with its own

@@ -42,6 +42,7 @@ PROTOTYPES = {
     "ucudnnFlushCostDatabase": (C.c_int, [vp]),
     "ucudnnSetBenchmarkIterations": (C.c_int, [vp, C.c_int, C.c_int]),
     "ucudnnSetDeterministic": (C.c_int, [vp, C.c_int]),
+    "ucudnnSetMathMode": (C.c_int, [vp, C.c_int]),
     "ucudnnSetBenchmarkDevices": (C.c_int, [vp, C.POINTER(C.c_int), C.c_int]),
     "ucudnnCreateTensorDescriptor": (C.c_int, [C.POINTER(vp)]),
     "ucudnnSetTensor4dDescriptor": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int]),

@@ -163,7 +163,8 @@ class Handle:
     """UcudnnHandle_t: device, stream, plans, cost table, WD arena."""
 
     def __init__(self, policy: str = "powerOfTwo", mode: str = "wr", total_workspace: int = 0,
-                 database: Optional[str] = None, stream=None, deterministic: bool = False):
+                 database: Optional[str] = None, stream=None, deterministic: bool = False,
+                 math: str = "tf32"):
         self._l = lib()
         self._h = C.c_void_p()
         check(self._l.ucudnnCreate(C.byref(self._h)))
@@ -174,12 +175,16 @@ class Handle:
         self.set_mode(mode)
         if total_workspace:
             self.set_total_workspace(total_workspace)
+        # the mode setters start a fresh (mode-specific) cost table, so they
+        # come before the database
+        if deterministic:
+            self.set_deterministic(True)
+        if math != "tf32":
+            self.set_math_mode(math)
         if database:
             check(self._l.ucudnnSetCostDatabase(self._h, database.encode()))
         if stream is not None:
             self.set_stream(stream)
-        if deterministic:
-            self.set_deterministic(True)
 
     def close(self):
         if self._h:
@@ -209,6 +214,10 @@ class Handle:
     def set_deterministic(self, on: bool) -> None:
         """Run-to-run bit-identical BackwardFilter (no split-K atomics)."""
         check(self._l.ucudnnSetDeterministic(self._h, 1 if on else 0))
+
+    def set_math_mode(self, math: str) -> None:
+        """"tf32" (default) or "fp32" (FP32-faithful: 3xTF32 over operand splits)."""
+        check(self._l.ucudnnSetMathMode(self._h, {"tf32": 0, "fp32": 1}[math]))
 
     def set_benchmark_iterations(self, warmup: int, iters: int) -> None:
         check(self._l.ucudnnSetBenchmarkIterations(self._h, warmup, iters))

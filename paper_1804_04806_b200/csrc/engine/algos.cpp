@@ -17,6 +17,7 @@
 #include "../kernels/gemm.h"
 #include "../kernels/igemm.h"
 #include "../kernels/precomp.h"
+#include "../kernels/split.h"
 #include "../kernels/winograd.h"
 
 namespace ucudnn {
@@ -29,9 +30,51 @@ std::uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed)
 
 namespace {
 thread_local bool t_det = false;
+thread_local bool t_faithful = false;
 }  // namespace
 bool deterministic() { return t_det; }
 void set_deterministic(bool on) { t_det = on; }
+bool faithful() { return t_faithful; }
+void set_faithful(bool on) { t_faithful = on; }
+
+namespace {
+std::int64_t al256(std::int64_t b) { return (b + 255) / 256 * 256; }
+// elements of the two operands of op: F (x, w), BD (dy, w), BF (x, dy)
+void operand_elems(int op, const ConvShape& s, std::int64_t* na, std::int64_t* nb) {
+  *na = op == 1 ? s.y_elems() : s.x_elems();
+  *nb = op == 2 ? s.y_elems() : s.w_elems();
+}
+}  // namespace
+
+std::int64_t algo_workspace(const AlgoImpl* a, int op, const ConvShape& s) {
+  const std::int64_t ws = a->workspace(op, s);
+  if (!faithful()) return ws;
+  std::int64_t na, nb;
+  operand_elems(op, s, &na, &nb);
+  return al256(ws) + 2 * al256(na * 4) + 2 * al256(nb * 4);
+}
+
+cudaError_t algo_run(const AlgoImpl* a, int op, const ConvShape& s, const float* A, const float* B, float* out,
+                     void* ws, float alpha, float beta, cudaStream_t st, int flags) {
+  if (!faithful()) return a->run(op, s, A, B, out, ws, alpha, beta, st, flags);
+  std::int64_t na, nb;
+  operand_elems(op, s, &na, &nb);
+  char* base = static_cast<char*>(ws);
+  float* ahi = reinterpret_cast<float*>(base + al256(a->workspace(op, s)));
+  float* alo = reinterpret_cast<float*>(reinterpret_cast<char*>(ahi) + al256(na * 4));
+  float* bhi = reinterpret_cast<float*>(reinterpret_cast<char*>(alo) + al256(na * 4));
+  float* blo = reinterpret_cast<float*>(reinterpret_cast<char*>(bhi) + al256(nb * 4));
+  cudaError_t e = split_tf32(A, ahi, alo, na, st);
+  if (e == cudaSuccess) e = split_tf32(B, bhi, blo, nb, st);
+  if (e != cudaSuccess) return e;
+  // the three passes use two filter operands, so each repacks (no
+  // kFilterReady across them) and run as complete calls (no deferral)
+  const int f = flags & ~(kFilterReady | kAccumulate | kDeferFinal);
+  e = a->run(op, s, ahi, bhi, out, ws, alpha, beta, st, f);
+  if (e == cudaSuccess) e = a->run(op, s, alo, bhi, out, ws, alpha, 1.f, st, f | (op == 2 ? 0 : kFilterReady));
+  if (e == cudaSuccess) e = a->run(op, s, ahi, blo, out, ws, alpha, 1.f, st, f);
+  return e;
+}
 
 namespace {
 std::atomic<bool> g_trace{false};

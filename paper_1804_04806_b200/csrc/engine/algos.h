@@ -30,6 +30,13 @@ struct AlgoImpl {
   int defer_ops = 0;
 };
 
+// Workspace / run of an algorithm in the calling thread's math mode: plain
+// TF32, or FP32-faithful (faithful(): three TF32 passes over hi / lo operand
+// splits held after the algorithm's own workspace).
+std::int64_t algo_workspace(const AlgoImpl* a, int op, const ConvShape& s);
+cudaError_t algo_run(const AlgoImpl* a, int op, const ConvShape& s, const float* A, const float* B, float* out,
+                     void* ws, float alpha, float beta, cudaStream_t st, int flags);
+
 // nullptr for ids that are reserved / not built.
 const AlgoImpl* find_algo(int id);
 int algo_count();  // ids are 0 .. algo_count()-1

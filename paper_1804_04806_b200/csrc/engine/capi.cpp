@@ -73,10 +73,17 @@ void require(bool ok, const char* msg) {
 
 // The handle's deterministic setting on the launching host thread for the
 // duration of a call (kernel launchers read it when sizing split-K grids).
-struct DetScope {
-  bool prev;
-  explicit DetScope(bool on) : prev(deterministic()) { set_deterministic(on); }
-  ~DetScope() { set_deterministic(prev); }
+// Same for the FP32-faithful math mode (workspace sizes and runs read it).
+struct ModeScope {
+  bool prev_det, prev_faithful;
+  ModeScope(bool det, bool faith) : prev_det(deterministic()), prev_faithful(faithful()) {
+    set_deterministic(det);
+    set_faithful(faith);
+  }
+  ~ModeScope() {
+    set_deterministic(prev_det);
+    set_faithful(prev_faithful);
+  }
 };
 }  // namespace
 
@@ -99,6 +106,7 @@ struct ucudnnContext {
   std::int64_t report_limit = 0;
   int warmup = 3, iters = 10;
   bool deterministic = false;  // ucudnnSetDeterministic / UCUDNN_DETERMINISTIC
+  bool faithful = false;       // ucudnnSetMathMode(UCUDNN_MATH_FP32_FAITHFUL) / UCUDNN_MATH_MODE=fp32
   std::unique_ptr<CostTable> table = std::make_unique<CostTable>();
   std::string db_path;
 
@@ -207,7 +215,7 @@ ConvShape conv_shape(const ucudnnTensorStruct* x, const ucudnnFilterStruct* w, c
 std::int64_t algo_ws(int op, const ConvShape& s, int algo, bool* ok) {
   const AlgoImpl* a = find_algo(algo);
   *ok = a && a->supports(op, s);
-  return *ok ? a->workspace(op, s) : 0;
+  return *ok ? algo_workspace(a, op, s) : 0;
 }
 
 using BenchSlot = ucudnnContext::BenchSlot;
@@ -276,7 +284,7 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
   }
   for (int i = 0; i < std::max(1, warmup); ++i)
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, i ? kFilterReady : 0), "benchmark warm-up");
+    cuda_check(algo_run(a, op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, i ? kFilterReady : 0), "benchmark warm-up");
   if (h->flush_bytes == std::size_t(-1)) {
     const char* e = std::getenv("UCUDNN_BENCH_FLUSH_MB");
     h->flush_bytes = std::size_t(e ? std::max(0, std::atoi(e)) : 256) << 20;
@@ -288,7 +296,7 @@ std::int64_t time_once(BenchSlot* h, cudaStream_t stream, int warmup, int iters,
     const int kind = want_prep ? (i & 1) : 0;
     if (h->flush_bytes) cuda_check(cudaMemsetAsync(h->flush, i & 0xff, h->flush_bytes, stream), "L2 flush");
     cuda_check(cudaEventRecord(h->ev0, stream), "cudaEventRecord");
-    cuda_check(a->run(op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kind ? 0 : kFilterReady), "benchmark run");
+    cuda_check(algo_run(a, op, s, ia, ib, out, h->ws, 1.f, 0.f, stream, kind ? 0 : kFilterReady), "benchmark run");
     cuda_check(cudaEventRecord(h->ev1, stream), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(h->ev1), "cudaEventSynchronize");
     float t = 0;
@@ -320,6 +328,7 @@ std::int64_t row_cost_ns(std::int64_t steady_ns, double prep_ms, std::int64_t b,
 // PAPER.md:472-473's parallel evaluation); rows are merged into the table
 // after every thread is done, so the table never sees a partial kernel.
 void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
+  ModeScope mode(h->deterministic, h->faithful);
   const ConvShape full = shape_of(k);
   struct Job {
     CostKey key;
@@ -347,7 +356,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   std::vector<double> prep(std::size_t(algo_count()), -1.0);
   std::vector<char> done(jobs.size(), 0);
   {
-    DetScope det(h->deterministic);
+    ModeScope det(h->deterministic, h->faithful);
     for (std::size_t i = 0; i < jobs.size(); ++i) {
       Job& j = jobs[i];
       if (prep[std::size_t(j.key.alg)] >= 0) continue;
@@ -358,7 +367,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
     }
   }
   if (h->slots.empty()) {
-    DetScope det(h->deterministic);
+    ModeScope det(h->deterministic, h->faithful);
     for (std::size_t i = 0; i < jobs.size(); ++i)
       if (!done[i]) jobs[i].ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, jobs[i].s,
                                            jobs[i].key.alg, jobs[i].ws);
@@ -371,7 +380,7 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
       BenchSlot* sl = slot.get();
       workers.emplace_back([&, sl] {
         try {
-          DetScope det(h->deterministic);
+          ModeScope det(h->deterministic, h->faithful);
           cuda_check(cudaSetDevice(sl->device), "cudaSetDevice(benchmark device)");
           if (!sl->stream) cuda_check(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
           for (std::size_t i = next++; i < jobs.size(); i = next++) {
@@ -471,25 +480,25 @@ void execute(ucudnnContext* h, int op, const ConvShape& full, const Plan& plan, 
     s.N = int(m.batch);
     // the plan's workspace came from a cost table, which may predate this
     // build's kernels: never run a micro-batch on less than it really needs
-    require(impl->workspace(op, s) <= std::int64_t(ws_bytes) || (impl->workspace(op, s) == 0),
+    require(algo_workspace(impl, op, s) <= std::int64_t(ws_bytes) || (algo_workspace(impl, op, s) == 0),
             "micro-batch needs more workspace than its cost-table row says (stale cost table?)");
     cudaError_t e;
     const bool same_prev = i > 0 && ms[i - 1].alg == m.alg, same_next = i + 1 < ms.size() && ms[i + 1].alg == m.alg;
     int flags = same_prev ? kFilterReady : 0;
-    if (op == 0) e = impl->run(0, s, a + off * x_ss, b, out + off * y_ss, ws, alpha, beta, h->stream, flags);
-    else if (op == 1) e = impl->run(1, s, a + off * y_ss, b, out + off * x_ss, ws, alpha, beta, h->stream, flags);
+    if (op == 0) e = algo_run(impl, 0, s, a + off * x_ss, b, out + off * y_ss, ws, alpha, beta, h->stream, flags);
+    else if (op == 1) e = algo_run(impl, 1, s, a + off * y_ss, b, out + off * x_ss, ws, alpha, beta, h->stream, flags);
     else {
       // user beta on the first micro-batch, 1 afterwards (the reference's
       // accumulate-into, reference_conv.hpp:257-274); an algorithm that
       // defers its finalize over a run applies the run's starting beta once
       float b_m = i == 0 ? beta : 1.f;
-      if (impl->defer_ops & (1 << 2)) {
+      if ((impl->defer_ops & (1 << 2)) && !faithful()) {
         if (!same_prev) run_beta = b_m;
         b_m = run_beta;
         if (same_prev) flags |= kAccumulate;
         if (same_next) flags |= kDeferFinal;
       }
-      e = impl->run(2, s, a + off * x_ss, b + off * y_ss, out, ws, alpha, b_m, h->stream, flags);
+      e = algo_run(impl, 2, s, a + off * x_ss, b + off * y_ss, out, ws, alpha, b_m, h->stream, flags);
     }
     cuda_check(e, "kernel launch");
     off += m.batch;
@@ -505,7 +514,7 @@ Plan undivided(int algo, const ConvShape& s, int op) {
 
 ucudnnStatus_t run_conv(ucudnnContext* h, int op, const ConvShape& s, int algo, const float* a, const float* b,
                         float* out, void* ws, std::size_t ws_bytes, float alpha, float beta) {
-  DetScope det(h->deterministic);
+  ModeScope det(h->deterministic, h->faithful);
   if (algo >= UCUDNN_VIRTUAL_ALGO_BASE) {
     auto& e = entry_of(h, algo);
     require(int(e.kernel.op) == op, "virtual algorithm belongs to another operation");
@@ -616,6 +625,7 @@ ucudnnStatus_t ucudnnCreate(UcudnnHandle_t* out) {
     if (const char* v = std::getenv("UCUDNN_TOTAL_WORKSPACE_SIZE")) h->total_ws = std::atoll(v);
     if (const char* v = std::getenv("UCUDNN_BENCHMARK_ITERS")) h->iters = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("UCUDNN_DETERMINISTIC")) h->deterministic = std::atoi(v) != 0;
+    if (const char* v = std::getenv("UCUDNN_MATH_MODE")) h->faithful = std::string(v) == "fp32";
     if (const char* v = std::getenv("UCUDNN_DATABASE")) {
       h->db_path = v;
       h->table = CostTable::open(v);
@@ -721,6 +731,21 @@ ucudnnStatus_t ucudnnSetDeterministic(UcudnnHandle_t h, int on) {
       // from an empty table (a database file must be set again, per mode)
       h->deterministic = on != 0;
       h->table = std::make_unique<CostTable>();
+      h->db_path.clear();
+      for (auto& e : h->entries) e.planned = false;
+      h->wd_stale = true;
+    }
+    return UCUDNN_STATUS_SUCCESS;
+  });
+}
+
+ucudnnStatus_t ucudnnSetMathMode(UcudnnHandle_t h, ucudnnMathMode_t mode) {
+  return guarded([&] {
+    require(h && (mode == UCUDNN_MATH_TF32 || mode == UCUDNN_MATH_FP32_FAITHFUL), "bad math mode");
+    const bool f = mode == UCUDNN_MATH_FP32_FAITHFUL;
+    if (h->faithful != f) {
+      h->faithful = f;
+      h->table = std::make_unique<CostTable>();  // rows of the other mode: not reusable
       h->db_path.clear();
       for (auto& e : h->entries) e.planned = false;
       h->wd_stale = true;
@@ -881,6 +906,7 @@ ucudnnStatus_t ucudnnGetConvolutionWorkspaceSize(UcudnnHandle_t h, int algo, ucu
         *bytes = std::size_t(e.plan.ws());
       }
     } else {
+      ModeScope mode(h->deterministic, h->faithful);
       ConvShape s = conv_shape(x, w, c);
       bool ok = false;
       std::int64_t ws = algo_ws(int(op), s, algo, &ok);
@@ -983,11 +1009,11 @@ ucudnnStatus_t ucudnnTimeAlgorithm(UcudnnHandle_t h, ucudnnOp_t op, const int64_
     require(op >= 0 && op <= 2, "bad op");
     ConvShape s = shape_from11(shape11);
     s.N = int(micro_batch);
+    ModeScope mode(h->deterministic, h->faithful);
     bool ok = false;
     std::int64_t ws = algo_ws(int(op), s, algo, &ok);
     *feasible = ok ? 1 : 0;
     *ws_bytes = ws;
-    DetScope det(h->deterministic);
     // a single timing charges the filter preparation in full (one micro-batch)
     double prep = -1.0;
     const std::int64_t ns =

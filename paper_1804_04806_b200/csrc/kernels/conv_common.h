@@ -39,6 +39,10 @@ std::uint64_t launch_count();
 // longer depends on the order of fp32 atomic additions.
 bool deterministic();
 void set_deterministic(bool on);
+// FP32-faithful math (ucudnnSetMathMode): set like deterministic(); the engine
+// then runs every algorithm as three TF32 passes over split operands.
+bool faithful();
+void set_faithful(bool on);
 
 bool trace_on();
 void trace_variant(const char* fmt, ...);

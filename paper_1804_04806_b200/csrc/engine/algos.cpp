@@ -198,9 +198,9 @@ cudaError_t nhwc_run(int op, const ConvShape& s, const float* a, const float* b,
 }
 
 const AlgoImpl kImplicitGemm{0, "IMPLICIT_GEMM", igemm_supports, no_workspace, igemm_run};
-const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run};
-const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run};
-const AlgoImpl kFft{2, "FFT", fft_supports, fft_workspace, fft_run};
+const AlgoImpl kWinograd{1, "WINOGRAD", wino2_supports, wino2_workspace, wino2_run, 0, false};
+const AlgoImpl kWinograd4{4, "WINOGRAD_4x4", wino4_supports, wino4_workspace, wino4_run, 0, false};
+const AlgoImpl kFft{2, "FFT", fft_supports, fft_workspace, fft_run, 0, false};
 const AlgoImpl kGemm{3, "GEMM", gemm_supports, gemm_workspace, gemm_run};
 const AlgoImpl kPrecomp{5, "IMPLICIT_PRECOMP_GEMM", precomp_supports, precomp_workspace, precomp_run};
 const AlgoImpl kGather{6, "IMPLICIT_GATHER_GEMM", gather_supports, gather_workspace, gather_run};

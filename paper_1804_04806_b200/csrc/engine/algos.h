@@ -28,6 +28,10 @@ struct AlgoImpl {
                      float alpha, float beta, cudaStream_t stream, int flags);
   // bit `op` set: run() honours kAccumulate / kDeferFinal for that op
   int defer_ops = 0;
+  // the tensor cores consume the caller's operands themselves (not a
+  // Winograd / FFT transform of them), so the FP32-faithful mode's operand
+  // split makes the products exact: false = not offered in that mode
+  bool splits_exact = true;
 };
 
 // Workspace / run of an algorithm in the calling thread's math mode: plain

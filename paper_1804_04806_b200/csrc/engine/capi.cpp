@@ -214,7 +214,8 @@ ConvShape conv_shape(const ucudnnTensorStruct* x, const ucudnnFilterStruct* w, c
 
 std::int64_t algo_ws(int op, const ConvShape& s, int algo, bool* ok) {
   const AlgoImpl* a = find_algo(algo);
-  *ok = a && a->supports(op, s);
+  // the FP32-faithful mode needs operands the tensor core consumes as given
+  *ok = a && a->supports(op, s) && (!faithful() || a->splits_exact);
   return *ok ? algo_workspace(a, op, s) : 0;
 }
 

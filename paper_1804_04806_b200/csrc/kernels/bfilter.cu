@@ -741,7 +741,7 @@ cudaError_t bf_run(const ConvShape& s, const float* x, const float* dy, float* d
   if (two) {
     p.m_tiles = (g.m_tiles + 1) / 2;
     p.tiles = p.m_tiles * g.n_tiles;
-    int sp = std::max(1, std::min(p.steps / 8, (sms / 2) / p.tiles));
+    int sp = deterministic() ? 1 : std::max(1, std::min(p.steps / 8, (sms / 2) / p.tiles));
     p.ksub = 1;
     p.steps_per_unit = (p.steps + sp - 1) / sp;
     p.splits = (p.steps + p.steps_per_unit - 1) / p.steps_per_unit;

@@ -1,7 +1,8 @@
 """FP32-faithful math mode (ucudnnSetMathMode, "3xTF32"): every algorithm,
 run as three TF32 passes over hi / lo operand splits, lands at fp32-level
 error against the fp64 oracle (reference_conv.hpp:70-180) on Gaussian data,
-where the default TF32 mode sits at ~1e-3; its workspace grows by the
+where the default TF32 mode sits at ~1e-3 (Winograd / FFT, whose tensor
+cores multiply transformed operands, are not offered); its workspace grows by the
 operand splits, and a planned, micro-batched call in this mode stays
 faithful (BackwardFilter accumulating across micro-batches)."""
 import numpy as np
@@ -16,8 +17,7 @@ pytestmark = pytest.mark.gpu
 SHAPES = [ConvShape(4, 64, 13, 13, 96, 3, 3, 1, 1, 1, 1),
           ConvShape(4, 3, 31, 31, 32, 11, 11, 2, 2, 4, 4),
           ConvShape(4, 32, 14, 14, 64, 1, 1, 0, 0, 2, 2)]
-# F(4x4,3x3) and FFT round in their fp32 transforms
-TOL = {2: 2e-5, 4: 2e-5}
+TOL = {}
 
 
 def _sid(s):
@@ -50,6 +50,11 @@ def test_fp32_faithful_error(cuda, algo, op, s):
     if tf32 is None:
         pytest.skip("infeasible")
     fp32, ws_f = _run(Handle(math="fp32"), op, s, a, b, algo)
+    if algo in (1, 2, 4):
+        # Winograd / FFT multiply transforms of the operands, which the split
+        # cannot make TF32-exact: not offered in this mode
+        assert fp32 is None
+        return
     e_t = np.linalg.norm(tf32 - ref) / np.linalg.norm(ref)
     e_f = np.linalg.norm(fp32 - ref) / np.linalg.norm(ref)
     assert e_f <= TOL.get(algo, 5e-6), (e_f, e_t)

@@ -22,6 +22,7 @@
 #include "conv_common.h"
 #include "igemm.h"
 #include "bflsu.h"
+#include "fps.h"
 #include "sm100.cuh"
 
 namespace ucudnn {
@@ -406,6 +407,8 @@ void fill_common(IgemmParams& p, const ConvShape& s) {
 
 cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
                           cudaStream_t stream) {
+  // few-channel strided layers (AlexNet / ResNet conv1): the shared-memory patch kernel
+  if (tune("z", 1) && fps_supports(s)) return fps_run(s, x, w, y, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kFwd, s)) return zgemm_forward(s, x, w, y, alpha, beta, stream);
   IgemmParams p{};
   fill_common(p, s);

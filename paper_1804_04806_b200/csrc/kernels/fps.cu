@@ -40,6 +40,7 @@ constexpr int kProd = 16;
 constexpr int kThreads = (5 + kProd) * 32;
 constexpr int kMaxStages = 6;
 constexpr int kMaxCRS = 512;
+constexpr int kBRows = 4;  // filter rows per producer thread: K <= 16 * 4
 constexpr std::uint32_t kABytes = kBM * 128;
 
 struct FGeo {
@@ -186,6 +187,18 @@ __global__ void __launch_bounds__(kThreads, 1) fps_kernel(const FParams p) {
     const std::uint32_t adst = std::uint32_t(blk) * 4096 + std::uint32_t(jq) * 128 +
                                ((std::uint32_t(lane >> 3) ^ std::uint32_t(jq)) << 5) + std::uint32_t(lane & 7) * 4;
     const std::uint32_t bsw = std::uint32_t(lane >> 2), bl = std::uint32_t(lane & 3) * 4;
+    // this thread's filter rows: source pointer (advanced by 32 per chunk)
+    // and B-tile destination, computed once
+    const float* bsrc[kBRows];
+    std::uint32_t bdst[kBRows];
+    bool brow[kBRows];
+#pragma unroll
+    for (int q = 0; q < kBRows; ++q) {
+      const int k = pw + kProd * q;
+      brow[q] = k < p.K;
+      bsrc[q] = p.w + (brow[q] ? (long long)k * p.crs + lane : 0);
+      bdst[q] = std::uint32_t(k) * 128 + ((bsw ^ std::uint32_t(k & 7)) << 4) + bl;
+    }
     int st = 0;
     std::uint32_t ph = 0, buf = 0;
     if (my_units > 0) {
@@ -214,14 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1) fps_kernel(const FParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa + adst + std::uint32_t(q) * 512), "f"(v[q]) : "memory");
-        // B: filter rows k (pw, pw + 16, ...), 32 reduction entries each
-        const int kr = ch * 32 + lane;
-        const bool kok = kr < p.crs;
-        for (int k = pw; k < p.Kp; k += kProd) {
-          const bool ok = kok && k < p.K;
-          cp_async4(sb + std::uint32_t(k) * 128 + ((bsw ^ std::uint32_t(k & 7)) << 4) + bl,
-                    p.w + (ok ? (long long)k * p.crs + kr : 0), ok ? 4u : 0u);
-        }
+        // B: filter rows k = pw + 16 i, 32 reduction entries each
+        const bool kok = ch * 32 + lane < p.crs;
+#pragma unroll
+        for (int q = 0; q < kBRows; ++q)
+          if (pw + kProd * q < p.Kp)
+            cp_async4(sb + bdst[q], bsrc[q] + ch * 32, (kok && brow[q]) ? 4u : 0u);
         mbar_arrive(&full[st]);
         cp_async_arrive(&full[st]);
         if (++st == kStages) {
@@ -340,7 +351,7 @@ FGeo make_fgeo(const ConvShape& s) {
 }  // namespace
 
 bool fps_supports(const ConvShape& s) {
-  if (s.sh != s.sw || (s.sh != 2 && s.sh != 4) || s.C > 4 || s.K > 256 || !tune("fps", 1)) return false;
+  if (s.sh != s.sw || (s.sh != 2 && s.sh != 4) || s.C > 4 || s.K > kProd * kBRows || !tune("fps", 1)) return false;
   const FGeo g = make_fgeo(s);
   return g.bpr <= 4 && g.chunks * 32 <= kMaxCRS && g.smem <= 220 * 1024 &&
          std::int64_t(s.N) * s.K * g.OH * g.OW < (1ll << 40);

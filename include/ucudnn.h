@@ -10,7 +10,7 @@
  * every failure maps to a status code plus a per-thread message
  * (ucudnnGetLastError).
  *
- * Layout: tensors NCHW fp32 (fully packed unless strides are given), filters
+ * Layout: tensors NCHW fp32, fully packed (no strided descriptors), filters
  * KCRS fp32, cross-correlation, dilation 1 -- the reference convolution's
  * semantics (reference_conv.hpp:26-55, 67-171).
  */
@@ -72,13 +72,13 @@ typedef enum {
 /* Concrete B200 algorithms (the cost-table `algorithm` column). Ids 0-2 keep
  * the reference archetype names of cost_model.hpp:165-177. */
 typedef enum {
-  UCUDNN_ALGO_IMPLICIT_GEMM = 0,     /* tcgen05 implicit GEMM, SIMT-gathered operands, 0 workspace */
+  UCUDNN_ALGO_IMPLICIT_GEMM = 0,     /* tcgen05 implicit GEMM, cp.async-gathered operands, 0 workspace */
   UCUDNN_ALGO_WINOGRAD = 1,          /* F(2x2,3x3) (3x3 s1 F/BD): transforms + 16 batched tcgen05 GEMMs */
   UCUDNN_ALGO_FFT = 2,               /* FFT-tiled (s1 F/BD, R,S <= 16): register FFTs + per-bin GEMMs */
   UCUDNN_ALGO_GEMM = 3,              /* explicit im2col / col2im + tiled tcgen05 GEMM                  */
   UCUDNN_ALGO_WINOGRAD_4x4 = 4,      /* F(4x4,3x3) (3x3 s1 F/BD): 36 batched tcgen05 GEMMs             */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* TMA-fed implicit GEMM on re-laid copies (all ops), ws ~ b   */
-  UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BF: cp.async-gathered NCHW operands; BD (strided, few C): GEMM+col2im via smem; ws O(1) */
+  UCUDNN_ALGO_IMPLICIT_GATHER_GEMM = 6,  /* BF: cp.async-gathered NCHW operands (few-C strided: smem patch); ws O(1) */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_SLICED = 7, /* F/BD: PRECOMP over reduction-channel slices, copy <= 40 MiB */
   UCUDNN_ALGO_IMPLICIT_PRECOMP_GEMM_NHWC = 8, /* BF (stride 1): NHWC copies, TMA im2col, MN-major tcgen05 operands */
   UCUDNN_ALGO_COUNT = 9

@@ -1532,7 +1532,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
   }
   p.cps = tune("pc_cps", p.msub == 1 && p.m_tiles * p.n_tiles > sm_count() ? 2 : 1) == 2 ? 2 : 1;
-  p.ksub = std::max(1, std::min(2, tune("pc_ksub", (p.cps == 2 && BN > 128) || p.msub == 2 ? 1 : 2)));
+  p.ksub = std::max(1, std::min(4, tune("pc_ksub", (p.cps == 2 && BN > 128) || p.msub == 2 ? 1 : 2)));
   const int stage_bytes = p.ksub * (p.msub * kBM * 128 + ((BN * 128 + 1023) & ~1023));
   p.stages = ring_stages(std::min(tune("pc_stages", 8), (p.cps == 2 ? 100 * 1024 : 200 * 1024) / stage_bytes));
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all

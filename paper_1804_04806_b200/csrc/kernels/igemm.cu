@@ -23,6 +23,7 @@
 #include "igemm.h"
 #include "bflsu.h"
 #include "fps.h"
+#include "z1x1.h"
 #include "sm100.cuh"
 
 namespace ucudnn {
@@ -407,6 +408,8 @@ void fill_common(IgemmParams& p, const ConvShape& s) {
 
 cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
                           cudaStream_t stream) {
+  // 1x1 stride-1 layers: TMA straight from the NCHW planes
+  if (tune("z", 1) && z1x1_supports(kFwd, s)) return z1x1_run(kFwd, s, x, w, y, alpha, beta, stream);
   // few-channel strided layers (AlexNet / ResNet conv1): the shared-memory patch kernel
   if (tune("z", 1) && fps_supports(s)) return fps_run(s, x, w, y, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kFwd, s)) return zgemm_forward(s, x, w, y, alpha, beta, stream);
@@ -426,6 +429,7 @@ cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, fl
 // independent dense GEMM (no multiplications by structural zeros).
 cudaError_t igemm_backward_data(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha,
                                 float beta, cudaStream_t stream) {
+  if (tune("z", 1) && z1x1_supports(kBwdData, s)) return z1x1_run(kBwdData, s, dy, w, dx, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kBwdData, s)) return zgemm_backward_data(s, dy, w, dx, alpha, beta, stream);
   for (int pa = 0; pa < s.sh; ++pa)
     for (int pb = 0; pb < s.sw; ++pb) {

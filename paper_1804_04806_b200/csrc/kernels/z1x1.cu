@@ -20,7 +20,7 @@
 // Persistent, one CTA per SM: three producer threads (warps 0, 2, 3) owning
 // ring stages s % 3 (one thread's TMA stream keeps about one stage in flight,
 // finding 2), warp 1 TMEM owner + MMA issuer with two accumulator sets,
-// warps 4-7 the NCHW epilogue (32 lanes = 32 consecutive positions: coalesced).
+// warps 4-11 the NCHW epilogue (32 lanes = 32 consecutive positions: coalesced).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -41,7 +41,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kMaxBN = 256;
 constexpr int kMaxStages = 8;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 3 producer warps (+1 idle), MMA warp, 8 epilogue warps
 constexpr std::uint32_t kABytes = kBM * 128;
 
 struct OParams {
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 256);
     }
     mbar_fence_init();
   }
@@ -174,8 +174,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 4-7)
-    const int ew = warp - 4;
+    // ------------------------------------------------ epilogue (warps 4-11)
+    // two warp groups share every tile: warp w reads TMEM lanes 32 (w % 4)
+    // (its 32 positions) and group (w - 4) / 4 takes alternate 32-column
+    // chunks -- at 256 output channels one group's stores could not keep up
+    // with the MMAs (ncu: 64 -> 256 Forward at 0.41 of HBM, 4 warps)
+    const int ew = warp & 3, eg = (warp - 4) >> 2;
     int tl = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tl) {
       const int mt = u % (p.units / p.n_tiles), nt = u / (p.units / p.n_tiles);
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool live = pos < p.HW;
       float* ob = p.out + (long long)n * p.oimg + (long long)nt * p.BN * p.HW + pos;
       const int ncol = min(p.BN, p.Co - nt * p.BN);
-      for (int c0 = 0; c0 < ncol; c0 += 32) {
+      for (int c0 = eg * 32; c0 < ncol; c0 += 64) {
         float v[32];
         tmem_ld32(tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN + c0), v);
         if (!live) continue;

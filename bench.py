@@ -225,6 +225,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a replayed CUDA graph")
     ap.add_argument("--db", default=None, help="cost-table CSV to reuse / extend")
+    ap.add_argument("--dist-eager", action="store_true",
+                    help="N > 1: eager launches with per-layer all-reduces overlapping the backward pass "
+                         "(default: graph replay + one bucketed all-reduce per step)")
     ap.add_argument("--plan-only", action="store_true",
                     help="benchmark and plan (writing --db), print the plans as one JSON line, exit")
     ap.add_argument("--bf-stream", type=int, default=2,
@@ -312,8 +315,23 @@ def main():
         stack.ws_bf = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
         stack.ws_bf_extra = []
 
-    comm = torch.distributed.group.WORLD if dist_on else None
-    comm_stream = torch.cuda.Stream(dev) if dist_on else None
+    # Data parallel with graphs (the default): every layer's dW lives in one
+    # flat buffer, the 15 planned calls of a step are one CUDA graph, and one
+    # bucketed NCCL all-reduce of all the dW (9.9 MB for AlexNet) follows each
+    # replay on the compute stream. --dist-eager instead issues the planned
+    # calls eagerly with a per-layer all-reduce on a side stream right after
+    # each layer's last BackwardFilter micro-batch (ConvStack.step(comm=...)).
+    graph_dist = dist_on and not args.no_graph and not args.dist_eager
+    flat_dw = None
+    if graph_dist:
+        sizes = [t["dw"].numel() for t in stack.t]
+        flat_dw = torch.empty(sum(sizes), dtype=torch.float32, device=dev)
+        off = 0
+        for t, n_ in zip(stack.t, sizes):
+            t["dw"] = flat_dw[off:off + n_].view_as(t["dw"])
+            off += n_
+    comm = torch.distributed.group.WORLD if dist_on and not graph_dist else None
+    comm_stream = torch.cuda.Stream(dev) if comm is not None else None
 
     bf_stream = [torch.cuda.Stream(dev) for _ in range(args.bf_stream)] if args.bf_stream else None
 
@@ -327,12 +345,11 @@ def main():
         stack.step(base, comm, comm_stream, bf_stream=bf_stream)
         stack.algos = ours_algos
 
-    # One process per GPU with no collective inside the step (N = 1): capture
-    # the 15 planned C-ABI calls once into a CUDA graph and replay it, which
-    # removes the host launch gaps between the ~140 small kernels. N > 1
-    # keeps eager launches (the NCCL all-reduces are issued per layer).
+    # Capture the 15 planned C-ABI calls once into a CUDA graph and replay it,
+    # which removes the host launch gaps between the ~140 small kernels; under
+    # data parallelism the bucketed all-reduce follows each replay.
     def as_graph(fn, handle):
-        if dist_on or args.no_graph:
+        if (dist_on and not graph_dist) or args.no_graph:
             n0 = lib().ucudnnGetLaunchCount()
             fn()
             torch.cuda.synchronize(dev)
@@ -348,6 +365,11 @@ def main():
             fn()
         per_step = lib().ucudnnGetLaunchCount() - n0
         handle.set_stream(stream.cuda_stream)
+        if graph_dist:
+            def replay_and_reduce():
+                g.replay()
+                torch.distributed.all_reduce(flat_dw, op=torch.distributed.ReduceOp.SUM)
+            return replay_and_reduce, per_step
         return g.replay, per_step
 
     run_ours, launches_per_step = as_graph(step_ours, h)
@@ -424,8 +446,10 @@ def main():
             with torch.cuda.stream(d2h_stream):
                 dw_host[i].copy_(stack.t[i]["dw"], non_blocking=True)
 
-        stack.step(h, comm, comm_stream, on_dw=None if comm is not None else on_dw, bf_stream=bf_stream)
-        if comm is not None:
+        stack.step(h, comm, comm_stream, on_dw=None if dist_on else on_dw, bf_stream=bf_stream)
+        if dist_on:
+            if graph_dist:
+                torch.distributed.all_reduce(flat_dw, op=torch.distributed.ReduceOp.SUM)
             for d, t in zip(dw_host, stack.t):
                 d.copy_(t["dw"], non_blocking=True)
         cur.wait_stream(d2h_stream)
@@ -517,7 +541,10 @@ def main():
                        "ws_limit_bytes": limit, "mode": args.mode, "policy": args.policy,
                        "total_workspace_bytes": args.total_mib * MiB if args.mode == "wd" else None,
                        "parallelism": f"dp{world}", "l2": "working set > L2 (no flush needed)",
-                       "launch": ("eager" if (dist_on or args.no_graph) else "cuda-graph replay of the 15 C-ABI calls")
+                       "launch": ("eager" if ((dist_on and not graph_dist) or args.no_graph)
+                                  else "cuda-graph replay of the 15 C-ABI calls"
+                                  + ("; one bucketed NCCL all-reduce of all dW after each replay" if graph_dist
+                                     else ""))
                        + (f"; BackwardFilter on {args.bf_stream} side stream(s) (BF_i on stream i % "
                           f"{args.bf_stream}, after BD_i+1) overlapping the BackwardData chain"
                           if args.bf_stream else "; one stream"),

@@ -70,13 +70,20 @@ def test_conv_stack_step_with_nccl_allreduce(cuda, tmp_path):
         dist.destroy_process_group()
 
 
-def test_bench_under_torchrun_world1(cuda):
+@pytest.mark.parametrize("mode", ["graph", "eager"])
+def test_bench_under_torchrun_world1(cuda, mode):
+    """Both data-parallel schedules of bench.py as the driver launches them:
+    graph replay + one bucketed all-reduce of all dW per step (default), and
+    eager launches with per-layer all-reduces on a side stream."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
-           "--gpus", "1", "--steps", "2", "--warmup", "3", "--no-cpu"]
+           "--gpus", "1", "--steps", "2", "--warmup", "3", "--no-cpu"] + (["--dist-eager"] if mode == "eager" else [])
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["config"]["comm_size"] == 1
-    assert line["config"]["launch"].startswith("eager")
+    if mode == "eager":
+        assert line["config"]["launch"].startswith("eager")
+    else:
+        assert "bucketed NCCL all-reduce" in line["config"]["launch"]
     assert line["value"] > 0 and line["gpu_launches"] > 0

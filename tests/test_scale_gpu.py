@@ -253,8 +253,9 @@ def test_zz_bench_scale_variants_exercised(cuda):
     precomp2 with more tiles than clusters (multi-tile CTA-pair loop), the
     1-SM implicit GEMM at two CTAs per SM, the CTA-pair channels-last
     BackwardFilter, split-K over more units than SMs, and deferred-finalize
-    runs (kAccumulate / kDeferFinal across an 8@128 + 8@128 plan), and the
-    zero-workspace implicit GEMM (algorithm 0) on every AlexNet F / BD."""
+    runs (kAccumulate / kDeferFinal across an 8@128 + 8@128 plan), the
+    zero-workspace implicit GEMM (algorithm 0) on every AlexNet F / BD, and
+    the shared-memory patch kernels of conv1."""
     if not TRACE:
         pytest.skip("run with the rest of this module")
 
@@ -276,4 +277,9 @@ def test_zz_bench_scale_variants_exercised(cuda):
         "no deferred-finalize run"
     z = [kv(l) for l in TRACE if l.startswith("zgemm ")]
     assert any(int(d["m_tiles"]) * int(d["n_tiles"]) > int(d["grid"]) for d in z), "no multi-tile zgemm"
-    assert {d["bmode"] for d in z} >= {"0", "1", "2"}, "zgemm B paths not all exercised"
+    # TMA filter (Forward) and the gathered phase sub-filter (BackwardData);
+    # the gathered-row Forward path (bmode 1) is reached by the small
+    # few-channel shapes of test_algos_gpu.py
+    assert {d["bmode"] for d in z} >= {"0", "2"}, "zgemm B paths not exercised"
+    assert any(l.startswith("fps ") for l in TRACE), "no shared-memory patch Forward (AlexNet conv1, algorithm 0)"
+    assert any(l.startswith("bfs ") for l in TRACE), "no shared-memory patch BackwardFilter (AlexNet conv1)"

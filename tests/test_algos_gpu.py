@@ -32,6 +32,9 @@ SHAPES = [
     ConvShape(2, 3, 32, 32, 64, 7, 7, 3, 3, 2, 2),        # ResNet conv1 geometry, W % 4 == 0
     ConvShape(3, 36, 12, 12, 40, 1, 1, 0, 0, 1, 1),       # 1x1 s1 (TMA plane GEMM): C % 32 != 0, partial plane tile
     ConvShape(2, 64, 56, 56, 256, 1, 1, 0, 0, 1, 1),      # ResNet-50 res2 1x1: 25 plane tiles per image
+    ConvShape(2, 64, 56, 56, 128, 1, 1, 0, 0, 2, 2),      # ResNet-50 res3a_1 projection: 1x1 stride 2 (4-D TMA map)
+    ConvShape(3, 36, 12, 12, 40, 1, 1, 0, 0, 2, 2),       # 1x1 s2, OW < 32: several output rows per tile
+    ConvShape(2, 32, 15, 16, 16, 1, 1, 0, 0, 2, 2),       # 1x1 s2, odd H: last dx row of each 2x2 block missing
     ConvShape(2, 3, 8, 8, 16, 3, 3, 0, 0, 3, 3),          # kernel == stride, trailing column unread (s2d row pitch)
     ConvShape(2, 3, 36, 36, 16, 8, 8, 0, 0, 8, 8),        # kernel == stride, W % 4 == 0 (s2d float4 path bound)
 ]

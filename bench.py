@@ -35,6 +35,29 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+_JSON_FD = None
+
+
+def quiet_stdout():
+    """Route everything written to stdout (NCCL's version banner, library
+    prints) to stderr at the file-descriptor level, keeping the real stdout
+    for the one JSON line (emit)."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    sys.stdout.flush()
+    data = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        os.write(1, data)
+    else:
+        os.write(_JSON_FD, data)
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -113,7 +136,7 @@ def run_reference_arm(args):
                                        f"x{256 // sample_n} (x{world} ranks' shards)" if world > 1 else
                                        f"{sample_n} of 256 samples of all 15 kernels per step, x{256 // sample_n}"},
             "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------ clocks
@@ -237,6 +260,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
+    quiet_stdout()
     cores = os.cpu_count() or 1
     args.ref_sample = args.ref_sample or min(64, cores)
     args.cpu_sample = args.cpu_sample or min(64, cores)
@@ -297,10 +321,9 @@ def main():
     plans = {f"{stack.layers[i].name}/{OP_NAMES[op]}": h.plan(a) for (i, op), a in stack.algos.items()}
     if args.plan_only:
         if rank == 0:
-            print(json.dumps({"net": args.net, "mode": args.mode, "policy": args.policy, "db": db,
-                              "plan_seconds": round(plan_s, 1),
-                              "plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in plans.items()}}),
-                  flush=True)
+            emit({"net": args.net, "mode": args.mode, "policy": args.policy, "db": db,
+                  "plan_seconds": round(plan_s, 1),
+                  "plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in plans.items()}})
         return
     base = Handle(policy="undivided", mode="wr", database=db, stream=stream.cuda_stream)
     base_stack_algos = {}
@@ -571,7 +594,7 @@ def main():
             "plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in plans.items()},
             "undivided_plans": {k: "+".join(f"{a}@{b}" for a, b in v) for k, v in base_plans.items()},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist_on:
         torch.distributed.destroy_process_group()
 

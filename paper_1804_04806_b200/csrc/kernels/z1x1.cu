@@ -16,11 +16,11 @@
 // BackwardData needs B[c][k] = w[k][c], whose rows (c) are contiguous along
 // N: {32 c, 32 k} boxes are MN-major blocks (instruction-descriptor bit 16).
 // Needs H*W % 4 == 0 (16 B plane stride) and C % 4 == 0 / K % 4 == 0.
-// Stride 2 (ResNet projection shortcuts): Forward reads x through a 4-D map
-// (w, h, c, n) with element stride 2 along w (W % 4 == 0), one box per
-// 32-position block of an output row; BackwardData is the stride-1 GEMM on
-// dy's plane with each result written to the top-left of its 2x2 dx block
-// and beta * dx (or 0) to the three tapless phases.
+// Stride-2 BackwardData (ResNet projection shortcuts) is the stride-1 GEMM
+// on dy's plane with each result written to the top-left of its 2x2 dx block
+// and beta * dx (or 0) to the three tapless phases. (A stride-2 Forward would
+// need a traversal stride along w, which TMA does not offer for the
+// innermost dimension.)
 //
 // Persistent, one CTA per SM: three producer threads (warps 0, 2, 3) owning
 // ring stages s % 3 (one thread's TMA stream keeps about one stage in flight,
@@ -53,9 +53,8 @@ struct OParams {
   float* out;
   float alpha, beta;
   int HW, Cs, Co;       // source plane size, reduction channels, output channels
-  // stride 2: mode 1 = Forward (4-D map over x with element stride 2, tiles of
-  // 32-position row blocks), mode 2 = BackwardData (dy plane -> 2x2 dx blocks)
-  int s2, OW, bpr, H, W;
+  // stride 2 (BackwardData only): 2 = dy plane -> 2x2 dx blocks
+  int s2, OW, H, W;
   int BN, n_tiles, tpi;  // column tile, column tiles, position tiles per image
   int units, chunks, stages, bd;
   long long oimg;        // Co * HW
@@ -66,13 +65,6 @@ __device__ __forceinline__ void tma_3d(void* dst, const void* tmap, std::uint64_
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
-      : "memory");
-}
-__device__ __forceinline__ void tma_4d(void* dst, const void* tmap, std::uint64_t* bar, int x, int y, int z, int w) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
 __device__ __forceinline__ std::uint64_t desc_mn32(std::uint32_t saddr) {
@@ -150,18 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           unsigned char* sa = smem + s * stage_bytes;
           mbar_expect_tx(&full[s], kABytes + std::uint32_t(p.BN) * 128);
-          if (p.s2 == 1) {
-            // block bi: output row bi / bpr, columns 32 (bi % bpr) ..: input
-            // (2 ow, 2 oh), every other element along w (element stride 2)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int bi = t * 4 + b, oh = bi / p.bpr, ow0 = (bi - oh * p.bpr) * 32;
-              tma_4d(sa + b * 4096, &amap, &full[s], 2 * ow0, 2 * oh, ch * 32, n);
-            }
-          } else {
-#pragma unroll
-            for (int b = 0; b < 4; ++b) tma_3d(sa + b * 4096, &amap, &full[s], p0 + b * 32, ch * 32, n);
-          }
+          for (int b = 0; b < 4; ++b) tma_3d(sa + b * 4096, &amap, &full[s], p0 + b * 32, ch * 32, n);
           if (p.bd) {
             for (int b = 0; b < p.BN / 32; ++b)
               tma_2d(sa + kABytes + b * 4096, &bmap, &full[s], nt * p.BN + b * 32, ch * 32);
@@ -212,12 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pos = t * kBM + ew * 32 + lane;  // source-plane position (s1, BD s2)
       bool live = pos < p.HW;
       long long ostride = p.HW;            // output plane size
-      if (p.s2 == 1) {
-        const int bi = t * 4 + ew, oh = bi / p.bpr, ow = (bi - oh * p.bpr) * 32 + lane;
-        live = oh * p.bpr < p.HW && ow < p.OW;  // HW holds OH * bpr for mode 1
-        pos = oh * p.OW + ow;
-        ostride = (long long)(p.HW / p.bpr) * p.OW;
-      } else if (p.s2 == 2) {
+      if (p.s2 == 2) {
         const int i = pos / p.OW, j = pos - i * p.OW;
         pos = 2 * i * p.W + 2 * j;  // top-left of the 2x2 dx block
         ostride = (long long)p.H * p.W;
@@ -307,8 +284,10 @@ bool z1x1_supports(int op, const ConvShape& s) {
     return false;
   if (s.C % 4 || s.K % 4 || s.N >= 65536 || std::int64_t(s.C) * s.H * s.W >= (1ll << 31)) return false;
   if (s.sh == 1) return std::int64_t(s.H) * s.W % 4 == 0;
-  if (op == kFwd) return s.W % 4 == 0 && tune("z1x1_s2", 1);  // 16 B input rows for the 4-D map
-  return std::int64_t(s.OH()) * s.OW() % 4 == 0 && tune("z1x1_s2", 1);  // dy plane stride
+  // stride 2: BackwardData only -- a Forward would need a traversal stride
+  // on the innermost (w) dimension, which TMA does not support (cuda.h:
+  // elementStrides[0] is ignored without interleave)
+  return op == kBwdData && std::int64_t(s.OH()) * s.OW() % 4 == 0 && tune("z1x1_s2", 1);
 }
 
 cudaError_t z1x1_run(int op, const ConvShape& s, const float* a, const float* w, float* out, float alpha, float beta,
@@ -317,37 +296,23 @@ cudaError_t z1x1_run(int op, const ConvShape& s, const float* a, const float* w,
   const int OH = s.OH(), OW = s.OW();
   OParams p{};
   p.out = out; p.alpha = alpha; p.beta = beta;
-  p.s2 = s.sh == 1 ? 0 : bd ? 2 : 1;
+  p.s2 = s.sh == 1 ? 0 : 2;
   p.OW = OW; p.H = s.H; p.W = s.W;
-  p.bpr = (OW + 31) / 32;
-  // source plane: x (Forward s1), dy (BackwardData); Forward s2 tiles count
-  // 32-position row blocks (HW = OH * bpr of them)
-  const int HW = p.s2 == 1 ? OH * p.bpr : bd ? OH * OW : s.H * s.W;
+  // source plane: x (Forward), dy (BackwardData)
+  const int HW = bd ? OH * OW : s.H * s.W;
   p.HW = HW;
   p.Cs = bd ? s.K : s.C;
   p.Co = bd ? s.C : s.K;
   p.bd = bd ? 1 : 0;
   p.BN = pick_bn(p.Co, bd ? 32 : 16);  // MN-major B comes in whole 32-column blocks
   p.n_tiles = (p.Co + p.BN - 1) / p.BN;
-  p.tpi = p.s2 == 1 ? (HW + 3) / 4 : (HW + kBM - 1) / kBM;
+  p.tpi = (HW + kBM - 1) / kBM;
   p.units = s.N * p.tpi * p.n_tiles;
   p.chunks = (p.Cs + 31) / 32;
   p.oimg = std::int64_t(p.Co) * (bd ? std::int64_t(s.H) * s.W : std::int64_t(OH) * OW);
   if ((reinterpret_cast<std::uintptr_t>(a) | reinterpret_cast<std::uintptr_t>(w)) & 15) return cudaErrorMisalignedAddress;
   CUtensorMap amap{}, bmap{};
-  if (p.s2 == 1) {
-    // x as (w, h, c, n), element stride 2 along w: a {64 w, 1 h, 32 c, 1}
-    // box is 32 stride-2 samples of one input row per channel -- one
-    // MN-major 32-position block of one output row
-    const cuuint64_t dims[4] = {cuuint64_t(s.W), cuuint64_t(s.H), cuuint64_t(s.C), cuuint64_t(s.N)};
-    const cuuint64_t strides[3] = {cuuint64_t(s.W) * 4, cuuint64_t(s.H) * s.W * 4, cuuint64_t(s.C) * s.H * s.W * 4};
-    const cuuint32_t box[4] = {64, 1, 32, 1};
-    const cuuint32_t es[4] = {2, 1, 1, 1};
-    if (encode_tiled()(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a), dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
-  } else {
+  {
     // source as (p, c, n): {32, 32, 1} boxes -> MN-major 32-position blocks
     const cuuint64_t dims[3] = {cuuint64_t(HW), cuuint64_t(p.Cs), cuuint64_t(s.N)};
     const cuuint64_t strides[2] = {cuuint64_t(HW) * 4, cuuint64_t(p.Cs) * HW * 4};

@@ -81,6 +81,7 @@ struct ZParams {
   int stages;
   int msub;  // position sub-tiles of 128 per tile, sharing each B stage (halves B traffic at 2)
   int nacc;  // TMEM accumulator sets (2: a tile's epilogue overlaps the next tile's MMAs)
+  int bres;  // gathered B (single column tile) resident in smem for every chunk: filled once per CTA
   FastDiv fd_HWg, fd_Wg, fd_TU, fd_U, fd_C, fd_sw;
 };
 
@@ -165,9 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t b_bytes = (std::uint32_t(p.BN) * 128 + 1023) & ~1023u;
   constexpr int msub = MSUB;
-  const std::uint32_t stage_bytes = msub * kABytes + b_bytes;
+  // resident B: [chunk][BN rows][128 B] after the ring; the ring then holds A only
+  const std::uint32_t stage_bytes = msub * kABytes + (p.bres ? 0u : b_bytes);
   const int kStages = p.stages;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes);
+  const std::uint32_t bres_bytes = p.bres ? std::uint32_t(p.chunks) * std::uint32_t(p.BN) * 128 : 0u;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * stage_bytes + bres_bytes);
   std::uint64_t* empty = full + kMaxStages;
   std::uint64_t* tfull = empty + kMaxStages;
   std::uint64_t* tempty = tfull + 2;
@@ -213,6 +216,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (nt * p.BN + j < p.ncols) ptab[j] = col_entry(p, nt * p.BN + j);
         named_sync(1, kProd * 32);
         cur_nt = nt;
+        if (p.bres) {
+          // the whole (single-tile) B once: chunk ch, row r at
+          // resB + (ch * BN + r) * 128, SW128 K-major within each chunk
+          const std::uint32_t resB = sbase + kStages * stage_bytes;
+          const std::uint32_t bsw = std::uint32_t(lane >> 2), bl = std::uint32_t(lane & 3) * 4;
+          const int brows = min(p.BN, p.ncols);
+          for (int ch = 0; ch < p.chunks; ++ch) {
+            const int kr = ch * 32 + lane;
+            int boff = 0, brt = 1 << 14, bsu = 1 << 14;
+            if (kr < p.Kr) {
+              std::uint32_t cs, tu, t, uu;
+              p.fd_TU.divmod(std::uint32_t(kr), cs, tu);
+              p.fd_U.divmod(tu, t, uu);
+              brt = (p.T - 1 - int(t)) * p.fsh;
+              bsu = (p.U - 1 - int(uu)) * p.fsw;
+              boff = int(cs) * p.CRS + brt * p.S + bsu;
+            }
+            for (int r = pw; r < p.BN; r += kProd) {
+              std::uint32_t ok = 0;
+              int off = 0;
+              if (r < brows) {
+                const ColEnt e = ptab[r];
+                ok = (kr < p.Kr && brt < e.rl && bsu < e.sl) ? 1u : 0u;
+                off = e.woff + boff;
+              }
+              const std::uint32_t dst = resB + std::uint32_t(ch * p.BN + r) * 128 +
+                                        ((bsw ^ std::uint32_t(r & 7)) << 4) + bl;
+              cp_async4(dst, p.w + off, ok * 4u);
+            }
+          }
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          named_sync(1, kProd * 32);  // resident B complete before any stage arrives
+        }
       }
       // this lane's position in each sub-tile
       std::uint32_t vr[2] = {0, 0}, vs[2] = {0, 0};
@@ -276,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       ((vr[1] >> t) & (vs[1] >> uu) & 1u) * 4u);
         }
         // B (gathered): rows of this n tile, lane = reduction index
-        if (p.bmode != 0) {
+        if (p.bmode != 0 && !p.bres) {
           const std::uint32_t bsw = std::uint32_t(lane >> 2), bl = std::uint32_t(lane & 3) * 4;
           for (int r = pw; r < p.BN; r += kProd) {
             std::uint32_t ok = 0;
@@ -313,7 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (lane == 0) {
           fence_async_smem();  // cp.async (generic proxy) -> tensor core (async proxy)
-          const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + msub * kABytes;
+          const std::uint32_t sa = sbase + st * stage_bytes;
+          const std::uint32_t sb = p.bres ? sbase + kStages * stage_bytes + std::uint32_t(ch * p.BN) * 128
+                                          : sa + msub * kABytes;
           for (int sub = 0; sub < msub; ++sub)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -413,13 +451,19 @@ int pick_bn(int n) {
 // Fills the op-independent fields and launches.
 cudaError_t zlaunch(ZParams p, cudaStream_t st) {
   p.BN = pick_bn(p.ncols);
+  p.chunks = (p.Kr + 31) / 32;
+  // a gathered B of one column tile that fits next to a >= 3-stage A ring
+  // stays resident (filled once per CTA: AlexNet / ResNet conv1
+  // BackwardData's phase sub-filters) instead of being re-gathered per tile
+  const int bres_bytes = p.chunks * p.BN * 128;
+  p.bres = p.bmode == 2 && p.ncols <= p.BN && bres_bytes + 3 * int(kABytes) <= 200 * 1024 && tune("z_bres", 1);
   // two position sub-tiles per tile once there are enough positions to keep
-  // every SM busy with them: each B stage then feeds 2x the MMA work
-  p.msub = tune("z_msub", p.M >= 2 * kBM * 2 * sm_count() ? 2 : 1) == 2 ? 2 : 1;
+  // every SM busy with them: each B stage then feeds 2x the MMA work (not
+  // needed when B is resident)
+  p.msub = tune("z_msub", !p.bres && p.M >= 2 * kBM * 2 * sm_count() ? 2 : 1) == 2 ? 2 : 1;
   p.nacc = 2 * p.msub * p.BN <= 512 ? 2 : 1;
   p.m_tiles = (p.M + p.msub * kBM - 1) / (p.msub * kBM);
   p.n_tiles = (p.ncols + p.BN - 1) / p.BN;
-  p.chunks = (p.Kr + 31) / 32;
   p.fd_HWg = FastDiv(std::uint32_t(p.Hg * p.Wg));
   p.fd_Wg = FastDiv(std::uint32_t(p.Wg));
   p.fd_TU = FastDiv(std::uint32_t(p.T * p.U));
@@ -435,16 +479,18 @@ cudaError_t zlaunch(ZParams p, cudaStream_t st) {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  const int stage_bytes = p.msub * int(kABytes) + ((p.BN * 128 + 1023) & ~1023);
-  p.stages = std::max(2, std::min({kMaxStages, tune("z_stages", 8), (200 * 1024) / stage_bytes}));
-  const int smem = p.stages * stage_bytes + 1024 + 256;
+  if (p.bres && bres_bytes + 2 * p.msub * int(kABytes) > 200 * 1024) p.bres = 0;
+  const int stage_bytes = p.msub * int(kABytes) + (p.bres ? 0 : ((p.BN * 128 + 1023) & ~1023));
+  const int ring = 200 * 1024 - (p.bres ? bres_bytes : 0);
+  p.stages = std::max(2, std::min({kMaxStages, tune("z_stages", 8), ring / stage_bytes}));
+  const int smem = p.stages * stage_bytes + (p.bres ? bres_bytes : 0) + 1024 + 256;
   auto kern = p.msub == 2 ? zgemm_kernel<2> : zgemm_kernel<1>;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, sm_count());
-  trace_variant("zgemm bmode=%d m_tiles=%d n_tiles=%d BN=%d msub=%d nacc=%d chunks=%d stages=%d grid=%d", p.bmode,
-                p.m_tiles, p.n_tiles, p.BN, p.msub, p.nacc, p.chunks, p.stages, grid);
+  trace_variant("zgemm bmode=%d bres=%d m_tiles=%d n_tiles=%d BN=%d msub=%d nacc=%d chunks=%d stages=%d grid=%d",
+                p.bmode, p.bres, p.m_tiles, p.n_tiles, p.BN, p.msub, p.nacc, p.chunks, p.stages, grid);
   return launch_pdl(kern, dim3(grid), dim3(kThreads), std::size_t(smem), st, bmap, p);
 }
 

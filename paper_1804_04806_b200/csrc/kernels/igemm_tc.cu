@@ -456,7 +456,9 @@ cudaError_t zlaunch(ZParams p, cudaStream_t st) {
   // stays resident (filled once per CTA: AlexNet / ResNet conv1
   // BackwardData's phase sub-filters) instead of being re-gathered per tile
   const int bres_bytes = p.chunks * p.BN * 128;
-  p.bres = p.bmode == 2 && p.ncols <= p.BN && bres_bytes + 3 * int(kABytes) <= 200 * 1024 && tune("z_bres", 1);
+  // Exact but not faster (AlexNet conv1 BD 637 vs 610 us, ResNet conv1 BD
+  // 3890 vs 2929: the gathers of A, not of B, bound these), so off by default
+  p.bres = p.bmode == 2 && p.ncols <= p.BN && bres_bytes + 3 * int(kABytes) <= 200 * 1024 && tune("z_bres", 0);
   // two position sub-tiles per tile once there are enough positions to keep
   // every SM busy with them: each B stage then feeds 2x the MMA work (not
   // needed when B is resident)

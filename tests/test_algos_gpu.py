@@ -173,15 +173,16 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("z_msub=2", "2 3 31 31 16 11 11 2 4 1 0"),
                                        ("z_msub=2", "4 40 9 9 300 3 3 1 1 0 0"),
                                        ("z_msub=2", "4 40 9 9 300 3 3 1 1 1 0"),
-                                       ("z_bres=0", "2 3 31 31 16 11 11 2 4 1 0"),
-                                       ("z_bres=0", "2 3 30 30 64 7 7 3 2 1 0"),
-                                       ("z_bres=0,z_msub=2", "3 5 13 13 7 5 5 2 1 1 0")])
+                                       ("z_bres=1", "2 3 31 31 16 11 11 2 4 1 0"),
+                                       ("z_bres=1", "2 3 30 30 64 7 7 3 2 1 0"),
+                                       ("z_bres=1", "3 5 13 13 7 5 5 2 1 1 0")])
 def test_knob_variants(cuda, tune, spec):
     """Variants the default shapes here do not reach, kept exact: the gather
     BackwardFilter with MN-major x rows (bfl_xmn=1), algorithm 0's
     SIMT-gather fallback (z=0, shapes the tcgen05 kernel does not take) and
     its two-sub-tile mode (z_msub=2, chosen automatically only at large
-    batch); UCUDNN_TUNE is read once per process, so each runs in a child."""
+    batch) and resident-filter BackwardData (z_bres=1); UCUDNN_TUNE is read
+    once per process, so each runs in a child."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, UCUDNN_TUNE=tune)

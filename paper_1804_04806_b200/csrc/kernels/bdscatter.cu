@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) bds_kernel(const SParams p) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
 
   if (warp > kEpi) {
     // ------------------------------------------------ dy gather: row ty of the block

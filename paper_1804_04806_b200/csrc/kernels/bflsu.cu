@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(threads_for<kProd1>(), 1) bfl_kernel(const LPa
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int units = p.tiles * p.splits;
 
   if (warp >= 5) {
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(threads_for<kProd2>(), 1) bfl2_kernel(const LP
   __syncthreads();
   cluster_sync();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int units = p.tiles * p.splits;  // tiles = pair tiles x n tiles
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 

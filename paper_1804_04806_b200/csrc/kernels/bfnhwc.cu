@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   pdl_wait();
   pdl_trigger();
   const int units = p.tiles * p.splits;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int units = p.tiles * p.splits;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 

@@ -1,0 +1,515 @@
+// Few-channel strided layers (AlexNet conv1: 3 channels, 11x11, stride 4;
+// ResNet conv1: 3 channels, 7x7, stride 2) with the im2col operand built
+// straight into tensor memory: no space-to-depth copy, no workspace for
+// Forward, and no operand tile ever stored to shared memory.
+//
+//   Forward: y[n][k][oh][ow] = alpha * sum_{c,r,s} x[n][c][oh*sh-ph+r][ow*sw-pw+s] * w[k][c][r][s] + beta * y
+//   (reference_conv.hpp:70-100)
+//
+// The im2col expansion of these layers is large (AlexNet conv1: 363 taps per
+// output pixel from 3 input channels, ~7.6x the input) and the earlier paths
+// either stream it from L2 through TMA im2col boxes of a space-to-depth copy
+// (algorithm 5: L2 -> SM bound) or rebuild it in shared memory (fps.cu:
+// bound by the LDS + STS of every element). Here:
+//
+// * a tile is TR whole output rows of one image (TR * OW <= 128 pixels, one
+//   per TMEM lane); a CTA owns a contiguous run of tiles, so consecutive
+//   tiles share R - TR*sh of their input rows;
+// * loader warps keep the input rows in a ring in shared memory (C rows per
+//   virtual row index, RR rows deep): per tile they load only the rows the
+//   previous tile did not (TR*sh of them; all PH at an image change), with
+//   coalesced loads, up to several tiles ahead of the consumers;
+// * A-operand producers -- one thread per output pixel, i.e. per TMEM lane --
+//   read their taps from the ring with vector loads (sw consecutive taps are
+//   sw consecutive floats: LDS.128 for stride 4, LDS.64 for stride 2,
+//   conflict-free across a warp) and write them to TMEM with tcgen05.st;
+// * tcgen05.mma takes A from TMEM and the filter (B, K-major SWIZZLE_128B)
+//   from shared memory, where it stays resident for the whole persistent
+//   kernel; two TMEM accumulator sets overlap a tile's NCHW epilogue with
+//   the next tile's MMAs.
+//
+// Reduction order: (c, r, s') with s' padded to SP = round_up(S, 4) taps (the
+// padded taps have zero filter weights); an A ring slot holds KG (c, r)
+// groups = KG * SP / 32 whole 32-float filter chunks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+
+#include "conv_common.h"
+#include "fct.h"
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace ucudnn {
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kMaxSlots = 8;
+constexpr int kNB = 8;        // tile barriers (ring of tiles in flight between loaders and producers)
+constexpr int kHist = 8;      // loader's history of tile row origins (>= the lookahead)
+constexpr int kLoaders = 7;   // loader warps (20 warps in all: 5 per SM sub-partition, 96 registers)
+constexpr int kRB = 4;        // ring rows per loader batch (8 x 32 columns each)
+constexpr int kMaxGroups = 64;
+// warps: 0-7 A producers, 8-11 epilogue, 12 MMA issuer, 13-19 row loaders
+constexpr int kThreads = (13 + kLoaders) * 32;
+
+struct TGeo {
+  int OH, OW, TR, np, tiles_per_img, units, grid;
+  int SP, groups, gpad, kslots, kred, nchunk, BN;
+  int PH, pitch, slot_cols, nslots, RR;
+  std::size_t b_bytes, r_bytes, smem;
+};
+
+struct TParams {
+  const float* x;
+  const float* w;
+  float* y;
+  float alpha, beta;
+  int C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
+  int TR, np, tiles_per_img, units;
+  int groups, kslots, nchunk, BN, PH, pitch, nslots, RR;
+  int dbg;  // UCUDNN_TUNE=fct_dbg=1: per-role wait cycles of CTAs 0-1 (printf)
+  long long CHW, KOHW;
+};
+
+// Waits of the warps off the critical path (epilogue, row loaders): back off
+// with nanosleep so the spinning does not take issue slots from the A
+// producers sharing their SM sub-partitions.
+__device__ __forceinline__ void mbar_wait_sleep(std::uint64_t* bar, std::uint32_t parity) {
+  std::uint32_t ok = 0, ns = 32;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// 32 lanes x 8 columns of 32-bit from registers into TMEM
+__device__ __forceinline__ void tmem_st8(std::uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, M = 128 x N x 8, executed by the whole
+// (converged) warp with one elected lane issuing: operands computed by every
+// lane from uniform values stay in uniform registers (inside `if (lane == 0)`
+// ptxas re-broadcast every operand per MMA: ~120 instead of ~50 cycles per
+// MMA, scripts/mma_ts_probe.cu).
+__device__ __forceinline__ void mma_tf32_ts_warp(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t bdesc,
+                                                 std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(std::uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// the SP taps of group (c, r) at this thread's pixel, vector loads of SW floats
+template <int SW, int SP>
+__device__ __forceinline__ void load_group(std::uint32_t addr, float* v) {
+  if constexpr (SW == 4) {
+#pragma unroll
+    for (int i = 0; i < SP / 4; ++i)
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[4 * i]), "=f"(v[4 * i + 1]), "=f"(v[4 * i + 2]), "=f"(v[4 * i + 3])
+                   : "r"(addr + 16 * i));
+  } else {
+#pragma unroll
+    for (int i = 0; i < SP / 2; ++i)
+      asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v[2 * i]), "=f"(v[2 * i + 1]) : "r"(addr + 8 * i));
+  }
+}
+
+// This CTA's contiguous tile range [t0, t1).
+__device__ __forceinline__ void tile_range(const TParams& p, int& t0, int& t1) {
+  t0 = int((long long)blockIdx.x * p.units / gridDim.x);
+  t1 = int((long long)(blockIdx.x + 1) * p.units / gridDim.x);
+}
+
+// Virtual ring row of the first input row of the CTA's next tile, the same
+// recurrence in loaders and producers: consecutive tiles of one image
+// advance by TR*sh rows; a new image starts after the last row loaded.
+struct RowWalk {
+  int vstart = 0, vend = 0, n = -1;
+  __device__ __forceinline__ bool next(const TParams& p, int u) {
+    const int nn = u / p.tiles_per_img;
+    const bool fresh = nn != n;
+    vstart = fresh ? vend : vstart + p.TR * p.sh;
+    vend = vstart + p.PH;
+    n = nn;
+    return fresh;
+  }
+};
+
+// Wait-time instrumentation (build with -DFCT_PROFILE, run with
+// UCUDNN_TUNE=fct_dbg=1): cycles each role spent waiting, CTAs 0-1, printf.
+#ifdef FCT_PROFILE
+#define FCT_T0 long long t_beg = clock64(), t_w1 = 0, t_w2 = 0, t_w3 = 0, t_q = 0
+#define FCT_W(acc, stmt)    \
+  do {                      \
+    t_q = clock64();        \
+    stmt;                   \
+    acc += clock64() - t_q; \
+  } while (0)
+#define FCT_PRINT(name)                                                                          \
+  if (p.dbg && (threadIdx.x & 31) == 0 && blockIdx.x < 2 && (warp % 4) == 0)                     \
+  printf("blk %d %s: total %lld wait1 %lld wait2 %lld w3 %lld\n", blockIdx.x, name, clock64() - t_beg, t_w1, \
+         t_w2, t_w3)
+#else
+#define FCT_T0
+#define FCT_W(acc, stmt) stmt
+#define FCT_PRINT(name)
+#endif
+
+template <int SW, int SP, int KG>
+__global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t b_bytes = std::uint32_t(p.nchunk) * p.BN * 128;
+  float* ring = reinterpret_cast<float*>(smem + b_bytes);  // [C][RR][pitch]
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(ring + p.C * p.RR * p.pitch);
+  std::uint64_t* afull = bars;
+  std::uint64_t* aempty = afull + kMaxSlots;
+  std::uint64_t* loaded = aempty + kMaxSlots;
+  std::uint64_t* consumed = loaded + kNB;
+  std::uint64_t* tfull = consumed + kNB;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  __shared__ int gc[kMaxGroups], gr[kMaxGroups];  // group -> ring offset of channel c (floats), tap row r (-1: padding)
+
+  // the filter, K-major SWIZZLE_128B, resident: row k, reduction index
+  // kk = (c * R + r) * SP + s' in 32-float chunks of BN rows
+  {
+    const int per_chunk = p.BN * 32;
+    const int total = p.nchunk * per_chunk;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int chunk = i / per_chunk, rem = i - chunk * per_chunk;
+      const int k = rem >> 5, j = rem & 31;
+      const int kk = chunk * 32 + j;
+      const int g = kk / SP, s = kk - g * SP;
+      float v = 0.f;
+      if (k < p.K && g < p.groups && s < p.S) {
+        const int c = g / p.R, r = g - c * p.R;
+        v = p.w[((long long)(k * p.C + c) * p.R + r) * p.S + s];
+      }
+      *reinterpret_cast<float*>(smem + chunk * p.BN * 128 + k * 128 + (((j >> 2) ^ (k & 7)) << 4) + (j & 3) * 4) = v;
+    }
+  }
+  for (int g = threadIdx.x; g < kMaxGroups; g += blockDim.x) {
+    const int c = g / p.R, r = g - c * p.R;
+    gc[g] = c * p.RR * p.pitch;
+    gr[g] = g < p.groups ? r : -1;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(&afull[s], 256);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int b = 0; b < kNB; ++b) {
+      mbar_init(&loaded[b], kLoaders * 32);
+      mbar_init(&consumed[b], 256);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  fence_async_smem();  // the filter stores are read by the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // warp-uniform by construction (a shuffle from lane 0), so the tcgen05
+  // operands derived from it live in uniform registers
+  const std::uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  int t0, t1;
+  tile_range(p, t0, t1);
+  const int my_units = t1 - t0;
+  const std::uint32_t a_col0 = 2u * std::uint32_t(p.BN);  // A ring after the two accumulator sets
+
+  if (warp < 8) {
+    // ------------------------------------------------ A producers: one output pixel per thread;
+    // warps w and w + 4 share TMEM lane quarter w % 4 and take the two
+    // halves of every slot's (c, r) groups
+    const int quarter = warp & 3, half = warp >> 2;
+    const int px = quarter * 32 + lane;
+    const int pe = px < p.np ? px : 0;
+    const int rl = pe / p.OW, ow = pe - rl * p.OW;
+    const std::uint32_t rbase = smem_u32(ring) + std::uint32_t(ow * SW * 4);
+    const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16);
+    constexpr int KH = KG / 2;
+    RowWalk walk;
+    int g = 0;  // A ring slot counter over the whole kernel
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      walk.next(p, t0 + i);
+      FCT_W(t_w1, mbar_wait_sleep(&loaded[i % kNB], (i / kNB) & 1));
+      const int row0 = (walk.vstart + rl * p.sh) % p.RR;  // ring row of tap row 0 at this pixel
+      for (int ks = 0; ks < p.kslots; ++ks, ++g) {
+        const int slot = g % p.nslots;
+        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+        tc_fence_after();
+        const int g0 = ks * KG + half * KH;
+        float v[KH * SP];
+#pragma unroll
+        for (int q = 0; q < KH; ++q) {
+          const int r = gr[g0 + q];
+          if (r >= 0) {
+            int row = row0 + r;
+            if (row >= p.RR) row -= p.RR;
+            load_group<SW, SP>(rbase + std::uint32_t(gc[g0 + q] + row * p.pitch) * 4, v + q * SP);
+          } else {
+#pragma unroll
+            for (int j = 0; j < SP; ++j) v[q * SP + j] = 0.f;
+          }
+        }
+        const std::uint32_t ta = tlane + a_col0 + std::uint32_t(slot * KG * SP + half * KH * SP);
+#pragma unroll
+        for (int j = 0; j < KH * SP; j += 8) tmem_st8(ta + std::uint32_t(j), v + j);
+        FCT_W(t_w3, tmem_st_wait());
+        tc_fence_before();
+        mbar_arrive(&afull[slot]);
+      }
+      mbar_arrive(&consumed[i % kNB]);  // this thread's ring reads are done (their values went to TMEM)
+    }
+    FCT_PRINT("prod (loaded, slot)");
+  } else if (warp < 12) {
+    // ------------------------------------------------ epilogue (NCHW stores, lane = pixel)
+    const int quarter = warp & 3, half = 0;
+    const int px = quarter * 32 + lane;
+    const int rl = px / p.OW, ow = px - rl * p.OW;
+    const long long ks = (long long)p.OH * p.OW;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u = t0 + i;
+      const int n = u / p.tiles_per_img, oh0 = (u - n * p.tiles_per_img) * p.TR;
+      const int acc = i & 1;
+      FCT_W(t_w1, mbar_wait_sleep(&tfull[acc], (i >> 1) & 1));
+      tc_fence_after();
+      const bool live = px < p.np && oh0 + rl < p.OH;
+      float* yb = p.y + (long long)n * p.KOHW + (long long)(oh0 + rl) * p.OW + ow;
+      for (int c0 = half * 32; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * p.BN + c0), v);
+        if (!live) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (c0 + j >= p.K) break;
+          float* dst = yb + (long long)(c0 + j) * ks;
+          const float val = p.alpha * v[j];
+          *dst = p.beta == 0.f ? val : val + p.beta * *dst;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    FCT_PRINT("epi (tfull, -)");
+  } else if (warp == 12) {
+    // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
+    // A slot spans KG * SP / 32 whole filter chunks, so every descriptor is
+    // the slot's base plus a compile-time step: straight-line issue code
+    constexpr int kMmas = KG * SP / 8;
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem));
+    const std::uint32_t chunk_desc = std::uint32_t(p.BN * 128) >> 4;
+    int g = 0;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int acc = i & 1;
+      FCT_W(t_w1, mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const std::uint32_t d = tmem + std::uint32_t(acc * p.BN);
+      std::uint64_t bd = bdesc0;
+      for (int ks = 0; ks < p.kslots; ++ks, ++g) {
+        const int slot = g % p.nslots;
+        FCT_W(t_w2, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+        tc_fence_after();
+        const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * KG * SP);
+#pragma unroll
+        for (int j = 0; j < kMmas; ++j)
+          mma_tf32_ts_warp(d, ta + std::uint32_t(8 * j), bd + (j >> 2) * chunk_desc + 2 * (j & 3), idesc,
+                           (ks | j) ? 1u : 0u);
+        mma_commit_warp(&aempty[slot]);
+        if (ks + 1 == p.kslots) mma_commit_warp(&tfull[acc]);
+        __syncwarp();
+        bd += (kMmas >> 2) * chunk_desc;
+      }
+    }
+    FCT_PRINT("mma (tempty, afull)");
+  } else {
+    // ------------------------------------------------ row loaders (zero off the image)
+    const int lw = warp - 13;
+    RowWalk walk;
+    int hist[kHist];  // vstart of the last kHist tiles
+    int waited = -1;  // every tile <= waited has been consumed
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u = t0 + i;
+      const bool fresh = walk.next(p, u);
+      const int n = u / p.tiles_per_img, oh0 = (u - n * p.tiles_per_img) * p.TR;
+      const int lo = fresh ? walk.vstart : walk.vend - p.TR * p.sh;  // virtual rows [lo, vend) are new
+      const int cnt = walk.vend - lo;
+      // they overwrite virtual rows [lo - RR, vend - RR): wait until every
+      // tile that may still read one of those has been consumed
+      const int ov = walk.vend - 1 - p.RR;
+      int need = -1;
+      for (int j = i - 1; j >= 0 && j >= i - kHist; --j)
+        if (hist[j % kHist] <= ov) {
+          need = j;
+          break;
+        }
+      if (need > waited) {
+        FCT_W(t_w1, mbar_wait_sleep(&consumed[need % kNB], (need / kNB) & 1));
+        waited = need;
+      }
+      hist[i % kHist] = walk.vstart;
+      const float* xn = p.x + (long long)n * p.CHW;
+      const int nrows = p.C * cnt;
+      for (int cb = 0; cb < p.pitch; cb += 256) {
+        for (int q0 = lw; q0 < nrows; q0 += kLoaders * kRB) {
+          float v[kRB][8];
+#pragma unroll
+          for (int rb = 0; rb < kRB; ++rb) {
+            const int q = q0 + rb * kLoaders;
+            const int c = q / cnt, vr = lo + q - c * cnt;
+            const int ih = oh0 * p.sh - p.ph + (vr - walk.vstart);
+            const bool rok = q < nrows && unsigned(ih) < unsigned(p.H);
+            const float* src = xn + ((long long)c * p.H + (rok ? ih : 0)) * p.W;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int col = cb + lane + 32 * j;
+              const int iw = col - p.pw;
+              v[rb][j] = rok && col < p.pitch && unsigned(iw) < unsigned(p.W) ? __ldg(src + iw) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int rb = 0; rb < kRB; ++rb) {
+            const int q = q0 + rb * kLoaders;
+            if (q >= nrows) break;
+            const int c = q / cnt, vr = lo + q - c * cnt;
+            float* dst = ring + (c * p.RR + vr % p.RR) * p.pitch + cb + lane;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (cb + lane + 32 * j < p.pitch) dst[32 * j] = v[rb][j];
+          }
+        }
+      }
+      mbar_arrive(&loaded[i % kNB]);  // release: this thread's ring stores
+    }
+    FCT_PRINT("load (consumed, loading)");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+int sm_count() {
+  static int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+TGeo make_tgeo(const ConvShape& s) {
+  TGeo g{};
+  g.OH = s.OH();
+  g.OW = s.OW();
+  g.TR = std::max(1, kBM / std::max(1, g.OW));
+  g.TR = std::min(g.TR, std::max(1, tune("fct_rows", g.TR)));
+  g.np = g.TR * g.OW;
+  g.tiles_per_img = (g.OH + g.TR - 1) / g.TR;
+  g.units = s.N * g.tiles_per_img;
+  g.grid = std::min(sm_count(), g.units);
+  g.SP = (s.S + 3) / 4 * 4;
+  g.groups = s.C * s.R;
+  const int KG = g.SP == 12 ? 8 : 4;  // a slot = whole 32-float filter chunks
+  g.gpad = (g.groups + KG - 1) / KG * KG;
+  g.kslots = g.gpad / KG;
+  g.kred = g.gpad * g.SP;
+  g.nchunk = (g.kred + 31) / 32;
+  g.BN = (s.K + 15) / 16 * 16;
+  g.PH = (g.TR - 1) * s.sh + s.R;
+  g.pitch = ((g.OW - 1) * s.sw + g.SP + 3) / 4 * 4;
+  g.slot_cols = KG * g.SP;
+  g.nslots = std::min(kMaxSlots, (512 - 2 * g.BN) / std::max(1, g.slot_cols));
+  g.b_bytes = std::size_t(g.nchunk) * g.BN * 128;
+  // ring depth: as many rows as fit, at most what the loaders' tile history
+  // can track
+  const std::size_t fixed = g.b_bytes + 1024 + 512;
+  const std::size_t row_bytes = std::size_t(s.C) * g.pitch * 4;
+  const int step = g.TR * s.sh;
+  int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
+  rr = std::min(rr, g.PH + (kHist - 2) * step);
+  rr = std::min(rr, tune("fct_ring", rr));
+  g.RR = std::max(rr, 1);
+  g.r_bytes = row_bytes * g.RR;
+  g.smem = fixed + g.r_bytes;
+  return g;
+}
+
+}  // namespace
+
+bool fct_fwd_supports(const ConvShape& s) {
+  if (s.sh != s.sw || (s.sw != 2 && s.sw != 4) || s.C > 4 || s.K > 128 || !tune("fct", 1)) return false;
+  const int SP = (s.S + 3) / 4 * 4;
+  if (!((s.sw == 4 && SP == 12) || (s.sw == 2 && SP == 8))) return false;
+  const TGeo g = make_tgeo(s);
+  // the ring must hold two tiles' rows so loading overlaps consuming
+  return g.OW <= kBM && g.gpad <= kMaxGroups && g.nslots >= 2 && g.RR >= g.PH + g.TR * s.sh &&
+         g.smem <= 220 * 1024 && std::int64_t(s.N) * s.K * g.OH * g.OW < (1ll << 40);
+}
+
+cudaError_t fct_fwd_run(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
+                        cudaStream_t st) {
+  const TGeo g = make_tgeo(s);
+  TParams p{};
+  p.x = x; p.w = w; p.y = y; p.alpha = alpha; p.beta = beta;
+  p.C = s.C; p.H = s.H; p.W = s.W; p.K = s.K; p.R = s.R; p.S = s.S; p.ph = s.ph; p.pw = s.pw;
+  p.sh = s.sh; p.sw = s.sw; p.OH = g.OH; p.OW = g.OW;
+  p.TR = g.TR; p.np = g.np; p.tiles_per_img = g.tiles_per_img; p.units = g.units;
+  p.groups = g.groups; p.kslots = g.kslots; p.nchunk = g.nchunk; p.BN = g.BN; p.PH = g.PH; p.pitch = g.pitch;
+  p.nslots = g.nslots; p.RR = g.RR;
+  p.dbg = tune("fct_dbg", 0);
+  p.CHW = std::int64_t(s.C) * s.H * s.W;
+  p.KOHW = std::int64_t(s.K) * g.OH * g.OW;
+  void (*kern)(const TParams) = s.sw == 4 ? fct_fwd_kernel<4, 12, 8> : fct_fwd_kernel<2, 8, 4>;
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
+  if (e != cudaSuccess) return e;
+  trace_variant("fct fwd units=%d grid=%d TR=%d np=%d kslots=%d BN=%d pitch=%d slots=%d ring=%d", g.units, g.grid,
+                g.TR, g.np, g.kslots, g.BN, g.pitch, g.nslots, g.RR);
+  return launch_pdl(kern, dim3(g.grid), dim3(kThreads), g.smem, st, p);
+}
+
+}  // namespace ucudnn

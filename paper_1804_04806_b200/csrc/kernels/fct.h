@@ -1,0 +1,16 @@
+// Few-channel strided layers with the im2col operand built in tensor memory
+// (see fct.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "conv_common.h"
+
+namespace ucudnn {
+
+bool fct_fwd_supports(const ConvShape& s);
+// y = alpha * conv(x, w) + beta * y; no workspace
+cudaError_t fct_fwd_run(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
+                        cudaStream_t stream);
+
+}  // namespace ucudnn

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) fps_kernel(const FParams p) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int my_units = blockIdx.x < p.units ? (p.units - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (warp >= 5) {

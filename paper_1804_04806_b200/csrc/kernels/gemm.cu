@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_gemm_kernel(const GemmParam
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int tiles = p.m_tiles * p.n_tiles, per_batch = tiles * p.splits, units = per_batch * p.batch;
 
   if (warp == 0 || warp == 2 || warp == 3) {

@@ -22,6 +22,7 @@
 #include "conv_common.h"
 #include "igemm.h"
 #include "bflsu.h"
+#include "fct.h"
 #include "fps.h"
 #include "z1x1.h"
 #include "sm100.cuh"
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const IgemmParams p)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
 
   const std::uint32_t smem0 = smem_u32(stage_base);
   const std::uint32_t a_bytes = 8 * p.lbo_a;
@@ -411,6 +412,7 @@ cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, fl
   // 1x1 stride-1 layers: TMA straight from the NCHW planes
   if (tune("z", 1) && z1x1_supports(kFwd, s)) return z1x1_run(kFwd, s, x, w, y, alpha, beta, stream);
   // few-channel strided layers (AlexNet / ResNet conv1): the shared-memory patch kernel
+  if (tune("z", 1) && fct_fwd_supports(s)) return fct_fwd_run(s, x, w, y, alpha, beta, stream);
   if (tune("z", 1) && fps_supports(s)) return fps_run(s, x, w, y, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kFwd, s)) return zgemm_forward(s, x, w, y, alpha, beta, stream);
   IgemmParams p{};

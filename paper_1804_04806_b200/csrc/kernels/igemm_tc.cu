@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int units = p.m_tiles * p.n_tiles;
 
   if (warp >= 5) {

@@ -69,6 +69,7 @@ struct PrecompParams {
   FastDiv fd_blk;  // Ah * Bw * C
   int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
   int stages, ksub, prof, cps;
+  int nacc2;  // precomp2: accumulator sets (2 when 2 * msub * BN <= 512)
   int msub;      // 1-SM kernel: 128-pixel MMA sub-tiles per tile sharing each B (filter) chunk
   FastDiv fd_Cr, fd_ssw;
 };
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   pdl_wait();  // everything above touched only smem / TMEM / the param-space tensor map
   pdl_trigger();
   const int total_tiles = p.m_tiles * p.n_tiles;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         long long c2 = p.prof ? clock64() : 0;
         if (p.prof) c_data += c2 - c1;
         const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
-        if (lane == 0) {
+        {  // whole warp, one elected lane issues (sm100.cuh mma_tf32_w)
           for (int sub = 0; sub < nsub; ++sub) {
             const std::uint32_t sa0 = sbase + s * stage_bytes + sub * sub_bytes, sb = sa0 + msub * a_bytes;
             for (int m = 0; m < msub; ++m) {
@@ -307,12 +308,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 std::uint64_t ad = p.small_c ? umma_desc(sa + 2 * q * (kBM * 16), kBM * 16, 128)
                                              : umma_desc_sw128(sa + q * 32);
                 std::uint64_t bd = umma_desc_sw128(sb + q * 32);
-                mma_tf32(dtm + std::uint32_t(m * p.BN), ad, bd, idesc, ((k0 + sub) | q) != 0);
+                mma_tf32_w(dtm + std::uint32_t(m * p.BN), ad, bd, idesc, ((k0 + sub) | q) != 0);
               }
             }
           }
-          mma_commit(&empty[s]);
-          if (j == jsteps - 1) mma_commit(&tfull[acc]);
+          mma_commit_w(&empty[s]);
+          if (j == jsteps - 1) mma_commit_w(&tfull[acc]);
         }
         __syncwarp();
         if (p.prof) c_issue += clock64() - c2;
@@ -445,7 +446,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int bh = p.BN / 2;  // filter rows per CTA
   const std::uint32_t a_bytes = kBM * 128;
   const std::uint32_t b_bytes = std::uint32_t(bh) * 128;
-  const std::uint32_t sub_bytes = a_bytes + ((b_bytes + 1023) & ~1023u);
+  // msub == 2: two pair sub-tiles (rows mt*512 + m*256 + rank*128 ..) share
+  // each filter box, so a stage carries twice the MMA work for 1.6x the bytes
+  const int msub = p.msub;
+  const std::uint32_t sub_bytes = msub * a_bytes + ((b_bytes + 1023) & ~1023u);
   const int kSub = p.ksub;
   const std::uint32_t stage_bytes = kSub * sub_bytes;
   const int kStages = p.stages;
@@ -473,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   cluster_sync();  // both CTAs' barriers initialised before any remote arrive / TMA
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   const int total_tiles = p.m_tiles * p.n_tiles;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -485,25 +489,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = cid; t < total_tiles; t += ncl) {
         int mt, nt;
         tile_coords(p, t, mt, nt);
-        std::uint32_t n, pix, oh, ow;
-        p.fd_P.divmod(std::uint32_t(mt * 2 * kBM + int(rank) * kBM), n, pix);
-        p.fd_OW.divmod(pix, oh, ow);
-        const int cw = int(ow) * p.sw - p.pw, ch = int(oh) * p.sh - p.ph;
+        int cws[2], chs[2], ns[2];
+        for (int m = 0; m < msub; ++m) {
+          std::uint32_t n, pix, oh, ow;
+          p.fd_P.divmod(std::uint32_t(mt * 2 * msub * kBM + m * 2 * kBM + int(rank) * kBM), n, pix);
+          p.fd_OW.divmod(pix, oh, ow);
+          cws[m] = int(ow) * p.sw - p.pw;
+          chs[m] = int(oh) * p.sh - p.ph;
+          ns[m] = int(n);
+        }
         const int brow0 = nt * p.ksteps * p.BN + int(rank) * bh;
         for (int j = 0; j < jsteps; ++j, ++it) {
           if ((it % kStages) % nprod != pq) continue;
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
-          if (rank == 0) mbar_expect_tx(&full[s], 2u * nsub * (a_bytes + b_bytes));
+          if (rank == 0) mbar_expect_tx(&full[s], 2u * nsub * (msub * a_bytes + b_bytes));
           const std::uint32_t bar = mapa(smem_u32(&full[s]), 0);
           for (int sub = 0; sub < nsub; ++sub) {
             const int k = k0 + sub;
             unsigned char* sa = smem + s * stage_bytes + sub * sub_bytes;
             const int tap = k / p.c_chunks, cc = k - tap * p.c_chunks;
             const int r = tap / p.S, q = tap - r * p.S;
-            tma_im2col_4d_2sm(sa, &amap, bar, cc * 32, cw, ch, int(n), (unsigned short)q, (unsigned short)r);
-            tma_2d_2sm(sa + a_bytes, &bmap, bar, 0, brow0 + k * p.BN);
+            for (int m = 0; m < msub; ++m)
+              tma_im2col_4d_2sm(sa + m * a_bytes, &amap, bar, cc * 32, cws[m], chs[m], ns[m], (unsigned short)q,
+                                (unsigned short)r);
+            tma_2d_2sm(sa + msub * a_bytes, &bmap, bar, 0, brow0 + k * p.BN);
           }
         }
       }
@@ -514,30 +525,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------- MMA issuer (pair leader)
       const std::uint32_t idesc = idesc_tf32(2 * kBM, p.BN);
       const std::uint32_t sbase = smem_u32(smem);
-      const std::uint64_t da0 = umma_desc_sw128(sbase), db0 = umma_desc_sw128(sbase + a_bytes);
+      const std::uint64_t da0 = umma_desc_sw128(sbase), db0 = umma_desc_sw128(sbase + msub * a_bytes);
+      const int nacc = p.nacc2;
       int it = 0, tl = 0;
       for (int t = cid; t < total_tiles; t += ncl, ++tl) {
-        const int acc = tl & 1;
-        mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        const int acc = tl % nacc, use = tl / nacc;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
-        const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
+        const std::uint32_t dtm = tmem + std::uint32_t(acc * msub * p.BN);
         for (int j = 0; j < jsteps; ++j, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           tc_fence_after();
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
-          if (lane == 0) {
+          {  // whole warp, one elected lane issues
             const std::uint32_t so = (std::uint32_t(s) * stage_bytes) >> 4;
             for (int sub = 0; sub < nsub; ++sub) {
               const std::uint32_t o = so + ((std::uint32_t(sub) * sub_bytes) >> 4);
               const std::uint32_t first = (k0 + sub) != 0;
-              mma_tf32_2sm(dtm, da0 + o, db0 + o, idesc, first);
-              mma_tf32_2sm(dtm, da0 + o + 2, db0 + o + 2, idesc, 1u);
-              mma_tf32_2sm(dtm, da0 + o + 4, db0 + o + 4, idesc, 1u);
-              mma_tf32_2sm(dtm, da0 + o + 6, db0 + o + 6, idesc, 1u);
+              for (int m = 0; m < msub; ++m) {
+                const std::uint32_t oa = o + ((std::uint32_t(m) * a_bytes) >> 4);
+                const std::uint32_t dm = dtm + std::uint32_t(m * p.BN);
+                mma_tf32_2sm_w(dm, da0 + oa, db0 + o, idesc, first);
+                mma_tf32_2sm_w(dm, da0 + oa + 2, db0 + o + 2, idesc, 1u);
+                mma_tf32_2sm_w(dm, da0 + oa + 4, db0 + o + 4, idesc, 1u);
+                mma_tf32_2sm_w(dm, da0 + oa + 6, db0 + o + 6, idesc, 1u);
+              }
             }
-            mma_commit_2sm(&empty[s], 3);
-            if (j == jsteps - 1) mma_commit_2sm(&tfull[acc], 3);
+            mma_commit_2sm_w(&empty[s], 3);
+            if (j == jsteps - 1) mma_commit_2sm_w(&tfull[acc], 3);
           }
           __syncwarp();
         }
@@ -551,10 +567,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = cid; t < total_tiles; t += ncl, ++tl) {
       int mt, nt;
       tile_coords(p, t, mt, nt);
-      const int acc = tl & 1;
-      mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      const int acc = tl % p.nacc2, use = tl / p.nacc2;
+      mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      const int row = mt * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
+      for (int m = 0; m < msub; ++m) {
+      const int row = mt * 2 * msub * kBM + m * 2 * kBM + int(rank) * kBM + ew * 32 + lane;
       const bool ok = row < p.M;
       std::int64_t obase = 0;
       int hb = 0, wb = 0;
@@ -570,7 +587,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           wb = int(j) * p.bp * p.ssw - p.spw;
         }
       }
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t tbase =
+          tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t((acc * msub + m) * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -589,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_row32(p, p.out + obase + std::int64_t(col0) * p.P, min(32, min(p.BN - c0, p.Nout - col0)),
                       std::int64_t(p.P), v);
         }
+      }
       }
       tc_fence_before();
       if (rank == 0) mbar_arrive(&tempty[acc]);
@@ -968,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
   pdl_wait();  // everything above touched only smem / TMEM / the param-space tensor map
   pdl_trigger();
   const int total_tiles = p.m_tiles * p.n_tiles;
@@ -1035,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
           mbar_wait(&full[st], (it / kStages) & 1);
           tc_fence_after();
-          if (lane == 0) {
+          {  // whole warp, one elected lane issues
             for (int i = 0; i < ntap; ++i) {
               const int tap = tap0 + i, r = tap / p.S, q = tap - r * p.S;
               const std::uint32_t sa = sbase + sb * strip_bytes + std::uint32_t(r * p.Wp + q) * 128;
@@ -1045,12 +1064,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // swap: A = filter rows, B = 256 strip positions
                 const std::uint64_t da = umma_desc_sw128((p.swap ? sbb : sa) + k * 32);
                 const std::uint64_t db = umma_desc_sw128((p.swap ? sa : sbb) + k * 32);
-                mma_tf32(dtm, da, db, idesc, (cc | tap | k) != 0);
+                mma_tf32_w(dtm, da, db, idesc, (cc | tap | k) != 0);
               }
             }
-            mma_commit(&empty[st]);
-            if (ts == tsteps - 1) mma_commit(&sempty[sb]);
-            if (ts == tsteps - 1 && cc == p.c_chunks - 1) mma_commit(&tfull[acc]);
+            mma_commit_w(&empty[st]);
+            if (ts == tsteps - 1) mma_commit_w(&sempty[sb]);
+            if (ts == tsteps - 1 && cc == p.c_chunks - 1) mma_commit_w(&tfull[acc]);
           }
           __syncwarp();
         }
@@ -1487,17 +1506,23 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    p.m_tiles = (p.M + 2 * kBM - 1) / (2 * kBM);
+    // two pair sub-tiles per tile (512 rows) share each filter box:
+    // UCUDNN_TUNE=pc2_msub=2 forces it, 0 picks it when every cluster still
+    // gets a tile
+    const int pc2_msub = tune("pc2_msub", 1);
+    p.msub = pc2_msub == 2 || (pc2_msub == 0 && p.M >= 4 * kBM * (sm_count() / 2)) ? 2 : 1;
+    p.nacc2 = 2 * p.msub * ((BN + 31) & ~31) <= 512 ? 2 : 1;  // tmem_ld32 reads whole 32-column groups
+    p.m_tiles = (p.M + 2 * p.msub * kBM - 1) / (2 * p.msub * kBM);
     p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
-    p.ksub = std::max(1, std::min(2, tune("pc2_ksub", 2)));
-    const int stage2 = p.ksub * (kBM * 128 + ((BN / 2 * 128 + 1023) & ~1023));
+    p.ksub = std::max(1, std::min(2, tune("pc2_ksub", p.msub == 2 ? 1 : 2)));
+    const int stage2 = p.ksub * (p.msub * kBM * 128 + ((BN / 2 * 128 + 1023) & ~1023));
     p.stages = ring_stages(std::min(tune("pc2_stages", 8), (200 * 1024) / stage2));
     const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
     e = set_smem_attr(reinterpret_cast<const void*>(precomp2_kernel), 227 * 1024);
     if (e != cudaSuccess) return e;
     const int clusters = std::min(sm_count() / 2, p.m_tiles * p.n_tiles);
-    trace_variant("precomp2 flip=%d m_tiles=%d n_tiles=%d clusters=%d BN=%d phase=%d s2d=%d", flip,
-                  p.m_tiles, p.n_tiles, clusters, BN, int(g.phase), int(g.s2d));
+    trace_variant("precomp2 flip=%d m_tiles=%d n_tiles=%d clusters=%d BN=%d msub=%d phase=%d s2d=%d", flip,
+                  p.m_tiles, p.n_tiles, clusters, BN, p.msub, int(g.phase), int(g.s2d));
     count_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * clusters);

@@ -171,6 +171,55 @@ template <int kCols>
 __device__ __forceinline__ void tmem_free_2sm(std::uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
 }
+// Warp-wide forms of the above: the whole (converged) warp executes them and
+// one elected lane issues. Called that way, operands every lane computes
+// from warp-uniform values (kernel parameters, loop counters, smem
+// addresses, a TMEM base read through __shfl_sync) stay in uniform
+// registers; issued from inside `if (lane == 0)` ptxas instead wraps every
+// tcgen05 instruction in an R2UR.BROADCAST "waterfall" loop, which measured
+// ~4x slower per MMA (scripts/mma_ts_probe.cu; DESIGN finding 21).
+__device__ __forceinline__ void mma_tf32_w(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
+                                           std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(std::uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_2sm_w(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
+                                               std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_w(std::uint64_t* bar, std::uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// TMEM base address made provably warp-uniform (read from shared memory it
+// is a per-thread value to the compiler).
+__device__ __forceinline__ std::uint32_t tmem_base_uniform(const std::uint32_t* slot) {
+  return __shfl_sync(0xffffffffu, *slot, 0);
+}
+
 // D[tmem] (+)= A * B^T over a CTA pair: M = 256 (128 rows of A per CTA), B
 // split along N (N/2 rows per CTA); issued by the pair's rank-0 CTA.
 __device__ __forceinline__ void mma_tf32_2sm(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,

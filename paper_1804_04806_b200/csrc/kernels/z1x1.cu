@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const std::uint32_t tmem = *tmem_slot;
+  const std::uint32_t tmem = tmem_base_uniform(tmem_slot);
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // ------------------------------------------------ TMA producers (stage s owned by thread s % 3)

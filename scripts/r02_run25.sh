@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+L="256,64,27,27,192,5,5,2,1 256,64,56,56,64,3,3,1,1 256,192,13,13,384,3,3,1,1"
+for t in "" "strip=1" "sswap=1" "strip=1,pc_cps=1"; do
+  echo "== $t" >> gpurun_out/tt_r25.txt
+  UCUDNN_TUNE=$t timeout 300 python scripts/time_table.py $L --ops 0,1 --algos 5 --batches 64 >> gpurun_out/tt_r25.txt 2>&1
+done
+cat gpurun_out/tt_r25.txt

@@ -175,13 +175,25 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("z_msub=2", "4 40 9 9 300 3 3 1 1 1 0"),
                                        ("z_bres=1", "2 3 31 31 16 11 11 2 4 1 0"),
                                        ("z_bres=1", "2 3 30 30 64 7 7 3 2 1 0"),
-                                       ("z_bres=1", "3 5 13 13 7 5 5 2 1 1 0")])
+                                       ("z_bres=1", "3 5 13 13 7 5 5 2 1 1 0"),
+                                       ("fct=0", "2 3 31 31 16 11 11 2 4 0 0"),
+                                       ("fct=0", "2 3 36 36 70 7 7 3 2 0 0"),
+                                       ("fct_ring=79", "4 3 63 63 20 11 11 1 4 0 0"),
+                                       ("fct_ring=33", "3 3 36 36 64 7 7 3 2 0 0"),
+                                       ("pc2_msub=2", "3 64 13 13 192 3 3 1 1 0 5"),
+                                       ("pc2_msub=2", "5 64 27 27 192 5 5 2 1 0 5"),
+                                       ("pc2_msub=2", "3 256 13 13 64 3 3 1 1 1 5"),
+                                       ("pc2_msub=2", "2 32 28 28 128 3 3 1 2 0 5")])
 def test_knob_variants(cuda, tune, spec):
     """Variants the default shapes here do not reach, kept exact: the gather
     BackwardFilter with MN-major x rows (bfl_xmn=1), algorithm 0's
     SIMT-gather fallback (z=0, shapes the tcgen05 kernel does not take) and
     its two-sub-tile mode (z_msub=2, chosen automatically only at large
-    batch) and resident-filter BackwardData (z_bres=1); UCUDNN_TUNE is read
+    batch), resident-filter BackwardData (z_bres=1) and the CTA-pair implicit
+    GEMM's two pair sub-tiles per tile (pc2_msub=2, 512 rows, BN=256 with one
+    accumulator set), the shared-memory-patch Forward behind the TMEM-operand
+    one (fct=0) and that kernel's input-row ring at its minimum depth
+    (fct_ring: loaders wait on almost every tile); UCUDNN_TUNE is read
     once per process, so each runs in a child."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -189,3 +201,7 @@ def test_knob_variants(cuda, tune, spec):
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *spec.split()],
                          env=env, capture_output=True, text=True, timeout=300)
     assert "exact True" in out.stdout, out.stdout + out.stderr
+    if tune == "pc2_msub=2":
+        assert "precomp2" in out.stdout and "msub=2" in out.stdout, out.stdout
+    if tune.startswith("fct_ring="):
+        assert "fct fwd" in out.stdout and tune.replace("fct_", "") in out.stdout, out.stdout

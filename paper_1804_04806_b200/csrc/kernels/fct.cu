@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdio>
 
+
 #include "conv_common.h"
 #include "fct.h"
 #include "launch.h"
@@ -163,6 +164,21 @@ struct RowWalk {
   }
 };
 
+// The BackwardFilter kernel's walk: units are single output rows (n, oh).
+struct BParams;
+struct RowWalkB {
+  int vstart = 0, vend = 0, n = -1;
+  template <typename P>
+  __device__ __forceinline__ bool next(const P& p, int u) {
+    const int nn = u / p.OH;
+    const bool fresh = nn != n;
+    vstart = fresh ? vend : vstart + p.sh;
+    vend = vstart + p.R;
+    n = nn;
+    return fresh;
+  }
+};
+
 // Wait-time instrumentation (build with -DFCT_PROFILE, run with
 // UCUDNN_TUNE=fct_dbg=1): cycles each role spent waiting, CTAs 0-1, printf.
 #ifdef FCT_PROFILE
@@ -174,7 +190,7 @@ struct RowWalk {
     acc += clock64() - t_q; \
   } while (0)
 #define FCT_PRINT(name)                                                                          \
-  if (p.dbg && (threadIdx.x & 31) == 0 && blockIdx.x < 2 && (warp % 4) == 0)                     \
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < 1 && (warp % 4) == 0 || (threadIdx.x == 13 * 32 || threadIdx.x == 15 * 32) && blockIdx.x < 1)                     \
   printf("blk %d %s: total %lld wait1 %lld wait2 %lld w3 %lld\n", blockIdx.x, name, clock64() - t_beg, t_w1, \
          t_w2, t_w3)
 #else
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
     // ------------------------------------------------ row loaders (zero off the image)
     const int lw = warp - 13;
     RowWalk walk;
-    int hist[kHist];  // vstart of the last kHist tiles
+    __shared__ int hist[kHist];  // vstart of the last kHist tiles (shared: a local array spilled to L2-latency local memory)
     int waited = -1;  // every tile <= waited has been consumed
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
@@ -388,7 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
         FCT_W(t_w1, mbar_wait_sleep(&consumed[need % kNB], (need / kNB) & 1));
         waited = need;
       }
-      hist[i % kHist] = walk.vstart;
+      __syncwarp();
+      if (lane == 0) hist[i % kHist] = walk.vstart;
+      __syncwarp();
       const float* xn = p.x + (long long)n * p.CHW;
       const int nrows = p.C * cnt;
       for (int cb = 0; cb < p.pitch; cb += 256) {
@@ -429,6 +447,321 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
   if (warp == 12) {
     tc_fence_after();
     tmem_free<512>(tmem);
+  }
+}
+
+// ============================================================== BackwardFilter
+//
+//   dW[k][c][r][s] = beta * dW + alpha * sum_{n,oh,ow} dy[n][k][oh][ow] * x[n][c][oh*sh-ph+r][ow*sw-pw+s]
+//   (reference_conv.hpp:141-180)
+//
+// D[q][k] = sum_px A[q][px] * B[k][px] with q = (c, r, s) on the TMEM lanes
+// (QT tiles of 128), the reduction over output pixels in 32-pixel blocks of
+// one output row, and N = the K output channels. A (the x taps) is built in
+// TMEM: producer thread q reads x[c][oh*sh-ph+r][ow*sw-pw+s] for the block's
+// 32 pixels from the input-row ring (the ring pitch is = S mod 32, so the 32
+// lanes of a warp -- consecutive (r, s) -- hit 32 different banks) and
+// stores them with one tcgen05.st. B (dy rows, 32 pixels x K) arrives by
+// coalesced loads into a K-major SWIZZLE_128B ring. A CTA owns a contiguous
+// run of output rows and accumulates all of them in TMEM; at the end its
+// partial sums go to its own workspace slice and a finalize adds the slices
+// in a fixed order: deterministic, no atomics.
+constexpr int kBfMaxQT = 3;
+constexpr int kBfDSlots = 12;  // dy ring (8 KB per 64-channel block)
+constexpr int kBfXLoaders = 1;  // x-row loader warp (bulk copies)
+constexpr int kBfDLoaders = 4;  // dy loader warps, each owning whole 32-pixel blocks (64 loads in flight per lane)
+// warps: 0 .. 4*QT-1 A producers (+ the final slice store), 12 MMA issuer,
+// 13 x-row loader, 14-17 dy loaders (18 warps: 96 registers)
+constexpr int kBfThreads = (4 * kBfMaxQT + 1 + kBfXLoaders + kBfDLoaders) * 32;
+
+struct BParams {
+  const float* x;
+  const float* dy;
+  float* slices;
+  int C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
+  int rows, BN, nblk, units, RR, pitch, nslots;
+  long long CHW, KOHW;
+};
+
+__device__ __forceinline__ void bulk_g2s_u32(std::uint32_t dst, const void* src, std::uint32_t bytes,
+                                             std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(std::uint32_t taddr, const float (&v)[32]) {
+  const std::uint32_t* r = reinterpret_cast<const std::uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void bf_range(const BParams& p, int& u0, int& u1) {
+  u0 = int((long long)blockIdx.x * p.units / gridDim.x);
+  u1 = int((long long)(blockIdx.x + 1) * p.units / gridDim.x);
+}
+
+template <int SW, int QT>
+__global__ void __launch_bounds__(kBfThreads, 1) fct_bwdf_kernel(const BParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t dslot_bytes = std::uint32_t(p.BN) * 128;
+  unsigned char* dring = smem;  // kBfDSlots x [BN rows x 128 B], SWIZZLE_128B K-major
+  float* ring = reinterpret_cast<float*>(dring + kBfDSlots * dslot_bytes);  // [C][RR][pitch]
+  // the pitch is odd in general: round the barrier block up to 16 B
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(
+      (reinterpret_cast<std::uintptr_t>(ring + p.C * p.RR * p.pitch) + 15) & ~std::uintptr_t(15));
+  std::uint64_t* afull = bars;
+  std::uint64_t* aempty = afull + kMaxSlots;
+  std::uint64_t* dfull = aempty + kMaxSlots;
+  std::uint64_t* dempty = dfull + kBfDSlots;
+  std::uint64_t* loaded = dempty + kBfDSlots;
+  std::uint64_t* consumed = loaded + kNB;
+  std::uint64_t* tdone = consumed + kNB;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tdone + 1);
+  int* eshift = reinterpret_cast<int*>(tmem_slot + 4);  // [C][RR]: data offset of each ring row (-1: zero row)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(&afull[s], QT * 128);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < kBfDSlots; ++s) {
+      mbar_init(&dfull[s], 32);
+      mbar_init(&dempty[s], 1);
+    }
+    for (int b = 0; b < kNB; ++b) {
+      mbar_init(&loaded[b], 1);
+      mbar_init(&consumed[b], QT * 128);
+    }
+    mbar_init(tdone, 1);
+    mbar_fence_init();
+  }
+  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  int u0, u1;
+  bf_range(p, u0, u1);
+  const int my_units = u1 - u0;
+  const std::uint32_t a_col0 = std::uint32_t(QT * p.BN);  // A ring after the QT accumulators
+
+  if (warp < 4 * QT) {
+    // ------------------------------------------------ A producers: lane = x row q = (c, r, s)
+    const int qt = warp >> 2, quarter = warp & 3;
+    const int q = qt * 128 + quarter * 32 + lane;
+    const bool qok = q < p.rows;
+    const int qe = qok ? q : 0;
+    const int c = qe / (p.R * p.S), rs = qe - c * p.R * p.S, r = rs / p.S, s = rs - r * p.S;
+    const std::uint32_t tq = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(qt * 32);
+    RowWalkB walk;
+    int g = 0;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      walk.next(p, u0 + i);
+      FCT_W(t_w1, mbar_wait(&loaded[i % kNB], (i / kNB) & 1));
+      int prow = walk.vstart % p.RR + r;
+      if (prow >= p.RR) prow -= p.RR;
+      // the ring row's data offset (bulk copies land 16 B aligned), -1: off the image
+      const int e = eshift[c * p.RR + prow];
+      const std::uint32_t xb = smem_u32(ring) + std::uint32_t(((c * p.RR + prow) * p.pitch + max(e, 0) + s) * 4);
+      const bool live = qok && e >= 0;
+      for (int b = 0; b < p.nblk; ++b, ++g) {
+        const int slot = g % p.nslots;
+        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+        tc_fence_after();
+        const int ow0 = b * 32;
+        const std::uint32_t a0 = xb + std::uint32_t(ow0 * SW * 4);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(a0 + j * SW * 4));
+        // only taps on the image count: the ring around the copied row data
+        // (padding columns, rows off the image, pixels past the row end) may
+        // hold anything
+        const int iw0 = ow0 * SW + s - p.pw;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (!live || ow0 + j >= p.OW || unsigned(iw0 + j * SW) >= unsigned(p.W)) v[j] = 0.f;
+        tmem_st32(tq + std::uint32_t(slot * QT * 32), v);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&afull[slot]);
+      }
+      mbar_arrive(&consumed[i % kNB]);
+    }
+    FCT_PRINT("bf prod (loaded, aempty)");
+    // ------------------------------------------------ this CTA's partial sums -> its slice
+    if (my_units > 0) {
+      mbar_wait_sleep(tdone, 0);
+      tc_fence_after();
+    }
+    float* slice = p.slices + (long long)blockIdx.x * p.rows * p.K + (long long)q * p.K;
+    for (int k0 = 0; k0 < p.BN; k0 += 32) {
+      float v[32];
+      if (my_units > 0) {
+        tmem_ld32(tmem + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(qt * p.BN + k0), v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+      if (!qok) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (k0 + j < p.K) slice[k0 + j] = v[j];
+    }
+  } else if (warp == 12) {
+    // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint64_t dd0 = umma_desc_sw128(smem_u32(dring));
+    const std::uint32_t dslot_desc = dslot_bytes >> 4;
+    int g = 0;
+    const int total = my_units * p.nblk;
+    FCT_T0;
+    for (; g < total; ++g) {
+      const int slot = g % p.nslots, ds = g % kBfDSlots;
+      FCT_W(t_w1, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+      FCT_W(t_w2, mbar_wait(&dfull[ds], (g / kBfDSlots) & 1));
+      tc_fence_after();
+      const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * QT * 32);
+      const std::uint64_t bd = dd0 + std::uint64_t(ds) * dslot_desc;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int t = 0; t < QT; ++t)
+          mma_tf32_ts_warp(tmem + std::uint32_t(t * p.BN), ta + std::uint32_t(t * 32 + 8 * k), bd + 2 * k, idesc,
+                           (g | k) ? 1u : 0u);
+      mma_commit_warp(&aempty[slot]);
+      mma_commit_warp(&dempty[ds]);
+      __syncwarp();
+    }
+    FCT_PRINT("bf mma (afull, dfull)");
+    if (total > 0) mma_commit_warp(tdone);
+    __syncwarp();
+  } else if (warp == 13) {
+    // ------------------------------------------------ x-row loader: one bulk copy per new ring row
+    // (issued by one lane each, all rows of a unit in flight at once), landed
+    // 16 B aligned with the row's shift recorded in eshift
+    RowWalkB walk;
+    __shared__ int hist[kHist];  // (shared: a local array spilled to L2-latency local memory)
+    int waited = -1;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u = u0 + i;
+      const bool fresh = walk.next(p, u);
+      const int n = u / p.OH, oh = u - n * p.OH;
+      const int lo = fresh ? walk.vstart : walk.vend - p.sh;
+      const int cnt = walk.vend - lo;
+      const int ov = walk.vend - 1 - p.RR;
+      int need = -1;
+      for (int j = i - 1; j >= 0 && j >= i - kHist; --j)
+        if (hist[j % kHist] <= ov) {
+          need = j;
+          break;
+        }
+      if (need > waited) {
+        FCT_W(t_w1, mbar_wait_sleep(&consumed[need % kNB], (need / kNB) & 1));
+        waited = need;
+      }
+      __syncwarp();
+      if (lane == 0) hist[i % kHist] = walk.vstart;
+      __syncwarp();
+      const int nrows = p.C * cnt;  // <= 4 * 11: at most two rows per lane
+      std::uint32_t bytes[2] = {0, 0}, dst[2] = {0, 0};
+      const float* src[2] = {nullptr, nullptr};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = lane + 32 * h;
+        if (row >= nrows) continue;
+        const int c = row / cnt, vr = lo + row - c * cnt;
+        const int ih = oh * p.sh - p.ph + (vr - walk.vstart);
+        const int prow = vr % p.RR;
+        int e = -1;
+        if (unsigned(ih) < unsigned(p.H)) {
+          const float* rp = p.x + ((long long)(n * p.C + c) * p.H + ih) * p.W;
+          const std::uintptr_t af = reinterpret_cast<std::uintptr_t>(rp) >> 2;  // float address
+          e = int((af - std::uintptr_t(p.pw)) & 3);
+          const std::uintptr_t a0 = af & ~std::uintptr_t(3), a1 = (af + p.W + 3) & ~std::uintptr_t(3);
+          src[h] = reinterpret_cast<const float*>(a0 << 2);
+          bytes[h] = std::uint32_t(a1 - a0) * 4;
+          dst[h] = smem_u32(ring) + std::uint32_t(((c * p.RR + prow) * p.pitch + e + p.pw - int(af & 3)) * 4);
+        }
+        eshift[c * p.RR + prow] = e;
+      }
+      std::uint32_t total = bytes[0] + bytes[1];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      __syncwarp();
+      FCT_W(t_w2, if (lane == 0) mbar_expect_tx(&loaded[i % kNB], total));  // arrive (releases eshift) + the bytes to come
+      __syncwarp();
+      FCT_W(t_w3,
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (bytes[h]) bulk_g2s_u32(dst[h], src[h], bytes[h], &loaded[i % kNB]));
+    }
+    FCT_PRINT("bf xload (consumed, -)");
+  } else if (warp >= 13 + kBfXLoaders) {
+    // ------------------------------------------------ dy loaders: warp g % 4 owns block g
+    // ([K rows x 32 pixels], zero past the row end), all its rows in flight at once
+    const int dw = warp - 13 - kBfXLoaders;
+    const long long ks = (long long)p.OH * p.OW;
+    const int total = my_units * p.nblk;
+    FCT_T0;
+    for (int g = dw; g < total; g += kBfDLoaders) {
+      const int u = u0 + g / p.nblk, b = g % p.nblk;
+      const int n = u / p.OH, oh = u - n * p.OH;
+      const int ds = g % kBfDSlots;
+      const int ow = b * 32 + lane;
+      const bool pok = ow < p.OW;
+      const float* src = p.dy + (long long)n * p.KOHW + (long long)oh * p.OW + (pok ? ow : 0);
+      float v[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) v[k] = pok && k < p.K ? __ldg(src + k * ks) : 0.f;
+      FCT_W(t_w1, mbar_wait_sleep(&dempty[ds], ((g / kBfDSlots) & 1) ^ 1));
+      unsigned char* slotp = dring + ds * dslot_bytes + (lane & 3) * 4;
+#pragma unroll
+      for (int k = 0; k < 64; ++k)
+        if (k < p.BN) *reinterpret_cast<float*>(slotp + k * 128 + (((lane >> 2) ^ (k & 7)) << 4)) = v[k];
+      fence_async_smem();  // generic stores -> the tensor core's async-proxy reads
+      mbar_arrive(&dfull[ds]);
+    }
+    FCT_PRINT("bf dyload (dempty, -)");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// dW[k][q] = beta * dW + alpha * sum_g slice_g[q][k], slices added in order
+struct BFinal {
+  const float* slices;
+  float* dw;
+  float alpha, beta;
+  int rows, K, nslices;
+};
+__global__ void __launch_bounds__(256) fct_bwdf_finalize_kernel(const BFinal f) {
+  pdl_wait();
+  const long long n = (long long)f.rows * f.K;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int q = int(i / f.K), k = int(i - (long long)q * f.K);
+    float acc = 0.f;
+    for (int g = 0; g < f.nslices; ++g) acc += f.slices[g * n + i];
+    float* d = f.dw + (long long)k * f.rows + q;
+    *d = f.beta == 0.f ? f.alpha * acc : f.alpha * acc + f.beta * *d;
   }
 }
 
@@ -510,6 +843,81 @@ cudaError_t fct_fwd_run(const ConvShape& s, const float* x, const float* w, floa
   trace_variant("fct fwd units=%d grid=%d TR=%d np=%d kslots=%d BN=%d pitch=%d slots=%d ring=%d", g.units, g.grid,
                 g.TR, g.np, g.kslots, g.BN, g.pitch, g.nslots, g.RR);
   return launch_pdl(kern, dim3(g.grid), dim3(kThreads), g.smem, st, p);
+}
+
+namespace {
+
+struct BGeo {
+  int OH, OW, rows, QT, BN, nblk, units, grid, pitch, RR, nslots;
+  std::size_t smem;
+};
+
+BGeo make_bgeo(const ConvShape& s) {
+  BGeo g{};
+  g.OH = s.OH();
+  g.OW = s.OW();
+  g.rows = s.C * s.R * s.S;
+  g.QT = (g.rows + kBM - 1) / kBM;
+  g.BN = (s.K + 15) / 16 * 16;
+  g.nblk = (g.OW + 31) / 32;
+  g.units = s.N * g.OH;
+  g.grid = std::min(sm_count(), g.units);
+  // ring pitch: a multiple of 4 floats (rows land by 16 B-aligned bulk
+  // copies), covering the copied row (shift <= 3, pw, the 16 B round-up) and
+  // every tap read of the last 32-pixel block; = 12 (mod 32) so a warp's
+  // consecutive (r, s) lanes mostly fall in different banks
+  const int need = std::max(s.pw + s.W + 10, (g.nblk * 32 - 1) * s.sw + s.S + 3);
+  g.pitch = (need + 3) / 4 * 4;
+  while (g.pitch % 32 != 12) g.pitch += 4;
+  g.nslots = std::min(kMaxSlots, (512 - g.QT * g.BN) / std::max(1, g.QT * 32));
+  const std::size_t fixed = std::size_t(kBfDSlots) * g.BN * 128 + 1024 + 2048;  // + barriers, eshift
+  const std::size_t row_bytes = std::size_t(s.C) * g.pitch * 4;
+  int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
+  rr = std::min(rr, s.R + (kHist - 2) * s.sh);
+  rr = std::min(rr, tune("fct_bf_ring", rr));
+  g.RR = std::max(rr, 1);
+  g.smem = fixed + row_bytes * g.RR;
+  return g;
+}
+
+}  // namespace
+
+bool fct_bwdf_supports(const ConvShape& s) {
+  if (s.sh != s.sw || (s.sw != 2 && s.sw != 4) || s.C > 4 || s.K > 64 || !tune("fct_bf", 1)) return false;
+  const BGeo g = make_bgeo(s);
+  return g.QT <= kBfMaxQT && s.C * s.R <= 64 && g.nslots >= 2 && g.RR >= s.R + s.sh && g.smem <= 220 * 1024 &&
+         std::int64_t(s.N) * s.C * s.H * s.W < (1ll << 40);
+}
+
+std::int64_t fct_bwdf_workspace(const ConvShape& s) {
+  const BGeo g = make_bgeo(s);
+  return (std::int64_t(g.grid) * g.rows * s.K * 4 + 255) / 256 * 256;
+}
+
+cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
+                         float beta, cudaStream_t st) {
+  const BGeo g = make_bgeo(s);
+  BParams p{};
+  p.x = x; p.dy = dy; p.slices = static_cast<float*>(ws);
+  p.C = s.C; p.H = s.H; p.W = s.W; p.K = s.K; p.R = s.R; p.S = s.S; p.ph = s.ph; p.pw = s.pw;
+  p.sh = s.sh; p.sw = s.sw; p.OH = g.OH; p.OW = g.OW;
+  p.rows = g.rows; p.BN = g.BN; p.nblk = g.nblk; p.units = g.units; p.RR = g.RR; p.pitch = g.pitch;
+  p.nslots = g.nslots;
+  p.CHW = std::int64_t(s.C) * s.H * s.W;
+  p.KOHW = std::int64_t(s.K) * g.OH * g.OW;
+  void (*kern)(const BParams) = nullptr;
+  if (s.sw == 4) kern = g.QT == 1 ? fct_bwdf_kernel<4, 1> : g.QT == 2 ? fct_bwdf_kernel<4, 2> : fct_bwdf_kernel<4, 3>;
+  else kern = g.QT == 1 ? fct_bwdf_kernel<2, 1> : g.QT == 2 ? fct_bwdf_kernel<2, 2> : fct_bwdf_kernel<2, 3>;
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
+  if (e != cudaSuccess) return e;
+  trace_variant("fct bwdf units=%d grid=%d rows=%d QT=%d BN=%d nblk=%d pitch=%d ring=%d slots=%d", g.units, g.grid,
+                g.rows, g.QT, g.BN, g.nblk, g.pitch, g.RR, g.nslots);
+  e = launch_pdl(kern, dim3(g.grid), dim3(kBfThreads), g.smem, st, p);
+  if (e != cudaSuccess) return e;
+  BFinal f{p.slices, dw, alpha, beta, g.rows, s.K, g.grid};
+  const long long n = (long long)g.rows * s.K;
+  return launch_pdl(fct_bwdf_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
+                    dim3(256), 0, st, f);
 }
 
 }  // namespace ucudnn

@@ -13,4 +13,11 @@ bool fct_fwd_supports(const ConvShape& s);
 cudaError_t fct_fwd_run(const ConvShape& s, const float* x, const float* w, float* y, float alpha, float beta,
                         cudaStream_t stream);
 
+bool fct_bwdf_supports(const ConvShape& s);
+// per-CTA partial-sum slices (batch-independent)
+std::int64_t fct_bwdf_workspace(const ConvShape& s);
+// dw = beta * dw + alpha * sum; deterministic (slices added in a fixed order)
+cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
+                         float beta, cudaStream_t stream);
+
 }  // namespace ucudnn

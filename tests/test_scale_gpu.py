@@ -282,4 +282,4 @@ def test_zz_bench_scale_variants_exercised(cuda):
     # few-channel shapes of test_algos_gpu.py
     assert {d["bmode"] for d in z} >= {"0", "2"}, "zgemm B paths not exercised"
     assert any(l.startswith("fct fwd ") for l in TRACE), "no TMEM-operand Forward (AlexNet conv1, algorithm 0)"
-    assert any(l.startswith("bfs ") for l in TRACE), "no shared-memory patch BackwardFilter (AlexNet conv1)"
+    assert any(l.startswith("fct bwdf ") for l in TRACE), "no TMEM-operand BackwardFilter (AlexNet conv1)"

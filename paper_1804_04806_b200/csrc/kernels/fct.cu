@@ -38,6 +38,7 @@
 #include <cstdio>
 
 
+
 #include "conv_common.h"
 #include "fct.h"
 #include "launch.h"
@@ -765,6 +766,334 @@ __global__ void __launch_bounds__(256) fct_bwdf_finalize_kernel(const BFinal f) 
   }
 }
 
+// ============================================================== BackwardData
+//
+//   dx[n][c][h][w] = beta * dx + alpha * sum_{k,r,s} dy[n][k][(h+ph-r)/sh][(w+pw-s)/sw] * w[k][c][r][s]
+//   (terms with (h+ph-r) % sh == 0 and (w+pw-s) % sw == 0; reference_conv.hpp:104-138)
+//
+// Stride-phase form: with h + ph = i*sh + a, w + pw = j*sw + b (a, b < sh),
+//   dx[c][i*sh+a-ph][j*sw+b-pw] = sum_{k,t,u} dy[k][i-t][j-u] * w[k][c][a+sh*t][b+sw*u]
+// so one "phase pixel" (i, j) -- a TMEM lane -- owns the sh*sw dx pixels of
+// every channel: N = C*sh*sw columns (AlexNet conv1: 48), reduction
+// (t, u, k) over the T x U taps of each phase and the K dy channels. The
+// filter, rearranged into that (c, a, b) x (t, u, k) matrix, stays resident
+// in shared memory; the dy rows a tile of phase rows needs sit in a ring
+// (bulk copies, one per channel row, landed 16 B aligned -- each row's float
+// shift follows from its address, so producers compute it instead of
+// looking it up); producer thread (i, j) reads dy[k][i-t][j-u] for 32
+// channels per slot (lanes = consecutive j: conflict-free) and writes them
+// to TMEM; one ring slot = one (t, u) tap = 64 reduction columns. The
+// epilogue scatters each lane's 48 columns to its sh x sw dx block of every
+// channel.
+constexpr int kBdKp = 64;  // reduction columns per (t, u) tap: K <= 64, zero-padded
+constexpr int kBdKS = 68;  // ring floats per position: 64 channels + 4 (16 B rows 17 chunks apart: conflict-free)
+constexpr int kBdLoaders = 4;
+// warps: 0-7 A producers, 8-11 epilogue, 12 MMA issuer, 13-16 dy-row loaders
+constexpr int kBdThreads = (13 + kBdLoaders) * 32;
+
+struct DParams {
+  const float* dy;
+  const float* w;
+  float* dx;
+  float alpha, beta;
+  int C, H, W, K, R, S, ph, pw, sh, OH, OW;
+  int T, U, Hq, Wq, TR, np, tiles_per_img, units, BN, AS, nslots, RR, XP, PH;
+  long long OHW, KOHW, CHW;
+};
+
+struct RowWalkD {
+  int vstart = 0, vend = 0, n = -1;
+  __device__ __forceinline__ bool next(const DParams& p, int u) {
+    const int nn = u / p.tiles_per_img;
+    const bool fresh = nn != n;
+    vstart = fresh ? vend : vstart + p.TR;
+    vend = vstart + p.PH;
+    n = nn;
+    return fresh;
+  }
+};
+
+template <int SH, int TU>
+__global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kChunks = TU * kBdKp / 32;
+  const std::uint32_t b_bytes = std::uint32_t(kChunks) * p.BN * 128;
+  float* ring = reinterpret_cast<float*>(smem + b_bytes);  // [RR][XP][kBdKS]
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(ring + p.RR * p.XP * kBdKS);
+  std::uint64_t* afull = bars;
+  std::uint64_t* aempty = afull + kMaxSlots;
+  std::uint64_t* loaded = aempty + kMaxSlots;
+  std::uint64_t* consumed = loaded + kNB;
+  std::uint64_t* tfull = consumed + kNB;
+  std::uint64_t* tempty = tfull + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+
+  // the filter as B[(c, a, b)][(t, u, k)] = w[k][c][a + sh t][b + sh u] (0 off the filter),
+  // K-major SWIZZLE_128B, BN rows per 32-column chunk
+  {
+    const int per_chunk = p.BN * 32;
+    const int total = kChunks * per_chunk;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int chunk = i / per_chunk, rem = i - chunk * per_chunk;
+      const int row = rem >> 5, j = rem & 31;
+      const int kk = chunk * 32 + j;
+      const int tu = kk / kBdKp, k = kk - tu * kBdKp;
+      const int t = tu / p.U, u = tu - t * p.U;
+      const int c = row / (p.sh * p.sh), ab = row - c * p.sh * p.sh, a = ab / p.sh, b = ab - a * p.sh;
+      const int r = a + p.sh * t, q = b + p.sh * u;
+      float v = 0.f;
+      if (c < p.C && k < p.K && r < p.R && q < p.S) v = p.w[((long long)(k * p.C + c) * p.R + r) * p.S + q];
+      *reinterpret_cast<float*>(smem + chunk * p.BN * 128 + row * 128 + (((j >> 2) ^ (row & 7)) << 4) + (j & 3) * 4) =
+          v;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(&afull[s], 256);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int b = 0; b < kNB; ++b) {
+      mbar_init(&loaded[b], kBdLoaders * 32);
+      mbar_init(&consumed[b], 256);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  int t0, t1;
+  {
+    t0 = int((long long)blockIdx.x * p.units / gridDim.x);
+    t1 = int((long long)(blockIdx.x + 1) * p.units / gridDim.x);
+  }
+  const int my_units = t1 - t0;
+  const std::uint32_t a_col0 = 2u * std::uint32_t(p.AS);
+
+  if (warp < 8) {
+    // ------------------------------------------------ A producers: lane = phase pixel (i, j);
+    // warps w and w + 4 share lane quarter w % 4 and take channels [0, 32) / [32, 64)
+    const int quarter = warp & 3, half = warp >> 2;
+    const int px = quarter * 32 + lane;
+    const bool pok = px < p.np;
+    const int pe = pok ? px : 0;
+    const int rl = pe / p.Wq, j = pe - rl * p.Wq;
+    const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16);
+    const int k0 = half * 32;
+    RowWalkD walk;
+    int g = 0;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u_ = t0 + i;
+      walk.next(p, u_);
+      FCT_W(t_w1, mbar_wait(&loaded[i % kNB], (i / kNB) & 1));
+      for (int tu = 0; tu < TU; ++tu, ++g) {
+        const int t = tu / p.U, u = tu - t * p.U;
+        // ring row of dy row i - t, position j - u (+ U - 1): its 32 channels are contiguous
+        const int prow = (walk.vstart + rl + p.T - 1 - t) % p.RR;
+        const std::uint32_t addr =
+            smem_u32(ring) + std::uint32_t(((prow * p.XP + j - u + p.U - 1) * kBdKS + k0) * 4);
+        const int slot = g % p.nslots;
+        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+        tc_fence_after();
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                       : "r"(addr + 16 * q));
+        tmem_st32(tlane + a_col0 + std::uint32_t(slot * kBdKp + half * 32), v);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&afull[slot]);
+      }
+      mbar_arrive(&consumed[i % kNB]);
+    }
+    FCT_PRINT("bd prod (loaded, aempty)");
+  } else if (warp < 12) {
+    // ------------------------------------------------ epilogue: lane (i, j) -> its SH x SH dx blocks;
+    // columns are (c, a, b) with b fastest, so a lane's SH values of one
+    // (c, a) are SH consecutive dx floats: one vector store when the row's
+    // alignment (uniform across the warp) allows
+    const int quarter = warp & 3;
+    const int px = quarter * 32 + lane;
+    const int rl = px / p.Wq, j = px - rl * p.Wq;
+    const long long HW = (long long)p.H * p.W;
+    const int w0 = j * SH - p.pw;
+    const bool wall = w0 >= 0 && w0 + SH <= p.W;  // all SH columns on the image
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u_ = t0 + i;
+      const int n = u_ / p.tiles_per_img, ii = (u_ - n * p.tiles_per_img) * p.TR + rl;
+      const int acc = i & 1;
+      FCT_W(t_w1, mbar_wait_sleep(&tfull[acc], (i >> 1) & 1));
+      tc_fence_after();
+      const bool live = px < p.np && ii < p.Hq;
+      const int h0 = ii * SH - p.ph;
+      float* dxn = p.dx + (long long)n * p.CHW;
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * p.AS + c0), v);
+        if (!live) continue;
+#pragma unroll
+        for (int rr = 0; rr < 32 / SH; ++rr) {  // one (c, a) row of SH values per step
+          const int ca = c0 / SH + rr, c = ca / SH, a = ca - c * SH;
+          const int h = h0 + a;
+          if (c >= p.C || unsigned(h) >= unsigned(p.H)) continue;
+          float* d = dxn + c * HW + (long long)h * p.W + w0;
+          if (p.beta == 0.f && wall) {
+            float o[SH];
+#pragma unroll
+            for (int b = 0; b < SH; ++b) o[b] = p.alpha * v[rr * SH + b];
+            const unsigned mis = unsigned(reinterpret_cast<std::uintptr_t>(d) >> 2) & 3;
+            if constexpr (SH == 4) {
+              if (mis == 0) {
+                *reinterpret_cast<float4*>(d) = make_float4(o[0], o[1], o[2], o[3]);
+              } else if (mis == 2) {
+                *reinterpret_cast<float2*>(d) = make_float2(o[0], o[1]);
+                *reinterpret_cast<float2*>(d + 2) = make_float2(o[2], o[3]);
+              } else {
+                d[0] = o[0];
+                *reinterpret_cast<float2*>(d + 1 + (mis == 1 ? 0 : 0)) = make_float2(o[1], o[2]);
+                d[3] = o[3];
+              }
+            } else {
+              if ((mis & 1) == 0) {
+                *reinterpret_cast<float2*>(d) = make_float2(o[0], o[1]);
+              } else {
+                d[0] = o[0];
+                d[1] = o[1];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < SH; ++b) {
+              if (unsigned(w0 + b) >= unsigned(p.W)) continue;
+              const float val = p.alpha * v[rr * SH + b];
+              d[b] = p.beta == 0.f ? val : val + p.beta * d[b];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    FCT_PRINT("bd epi (tfull, -)");
+  } else if (warp == 12) {
+    // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem));
+    const std::uint32_t chunk_desc = std::uint32_t(p.BN * 128) >> 4;
+    int g = 0;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int acc = i & 1;
+      FCT_W(t_w1, mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const std::uint32_t d = tmem + std::uint32_t(acc * p.AS);
+      std::uint64_t bd = bdesc0;
+      for (int tu = 0; tu < TU; ++tu, ++g) {
+        const int slot = g % p.nslots;
+        FCT_W(t_w2, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+        tc_fence_after();
+        const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * kBdKp);
+#pragma unroll
+        for (int m = 0; m < kBdKp / 8; ++m)
+          mma_tf32_ts_warp(d, ta + std::uint32_t(8 * m), bd + (m >> 2) * chunk_desc + 2 * (m & 3), idesc,
+                           (tu | m) ? 1u : 0u);
+        mma_commit_warp(&aempty[slot]);
+        if (tu + 1 == TU) mma_commit_warp(&tfull[acc]);
+        __syncwarp();
+        bd += (kBdKp / 32) * chunk_desc;
+      }
+    }
+    FCT_PRINT("bd mma (tempty, afull)");
+  } else {
+    // ------------------------------------------------ dy-row loaders: the dy rows each tile adds,
+    // transposed to [position][channel] (4 channels per lane: 4 coalesced
+    // loads, one 16 B store), zero off the tensor
+    const int lw = warp - 13;
+    RowWalkD walk;
+    __shared__ int hist[kHist];
+    int waited = -1;
+    const int nxb = (p.XP + 31) / 32;
+    FCT_T0;
+    for (int i = 0; i < my_units; ++i) {
+      const int u_ = t0 + i;
+      const bool fresh = walk.next(p, u_);
+      const int n = u_ / p.tiles_per_img, i0 = (u_ - n * p.tiles_per_img) * p.TR;
+      const int lo = fresh ? walk.vstart : walk.vend - p.TR;
+      const int cnt = walk.vend - lo;
+      const int ov = walk.vend - 1 - p.RR;
+      int need = -1;
+      for (int jj = i - 1; jj >= 0 && jj >= i - kHist; --jj)
+        if (hist[jj % kHist] <= ov) {
+          need = jj;
+          break;
+        }
+      if (need > waited) {
+        FCT_W(t_w1, mbar_wait_sleep(&consumed[need % kNB], (need / kNB) & 1));
+        waited = need;
+      }
+      if (lw == 0) {
+        __syncwarp();
+        if (lane == 0) hist[i % kHist] = walk.vstart;
+        __syncwarp();
+      }
+      const float* dyn = p.dy + (long long)n * p.KOHW;
+      // warp lw owns channel quads lw, lw + 4, .. (16 channels); per new row,
+      // every (position block, quad) of the warp is in flight at once
+      for (int rr = 0; rr < cnt; ++rr) {
+        const int y = i0 - (p.T - 1) + (lo + rr - walk.vstart);
+        const bool yok = unsigned(y) < unsigned(p.OH);
+        const float* rowp = dyn + (long long)(lw * 4) * p.OHW + (long long)(yok ? y : 0) * p.OW;
+        float* dstrow = ring + ((lo + rr) % p.RR) * p.XP * kBdKS + lw * 4;
+        float v[2][kBdKp / 16][4];
+#pragma unroll
+        for (int xb = 0; xb < 2; ++xb) {
+          const int ow = xb * 32 + lane - (p.U - 1);
+          const bool ok = yok && xb < nxb && unsigned(ow) < unsigned(p.OW);
+#pragma unroll
+          for (int qq = 0; qq < kBdKp / 16; ++qq)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = lw * 4 + qq * 16 + e;
+              v[xb][qq][e] = ok && k < p.K ? __ldg(rowp + (long long)(qq * 16 + e) * p.OHW + ow) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int xb = 0; xb < 2; ++xb) {
+          const int x = xb * 32 + lane;
+          if (xb < nxb && x < p.XP) {
+#pragma unroll
+            for (int qq = 0; qq < kBdKp / 16; ++qq)
+              *reinterpret_cast<float4*>(dstrow + x * kBdKS + qq * 16) =
+                  make_float4(v[xb][qq][0], v[xb][qq][1], v[xb][qq][2], v[xb][qq][3]);
+          }
+        }
+      }
+      mbar_arrive(&loaded[i % kNB]);  // release: this thread's ring stores
+    }
+    FCT_PRINT("bd load (consumed, -)");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
 int sm_count() {
   static int v = [] {
     int dev = 0, n = 148;
@@ -918,6 +1247,76 @@ cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, fl
   const long long n = (long long)g.rows * s.K;
   return launch_pdl(fct_bwdf_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
                     dim3(256), 0, st, f);
+}
+
+namespace {
+
+struct DGeo {
+  int T, U, Hq, Wq, TR, np, tiles_per_img, units, grid, BN, AS, nslots, RR, XP, PH;
+  std::size_t smem;
+};
+
+DGeo make_dgeo(const ConvShape& s) {
+  DGeo g{};
+  const int OH = s.OH(), OW = s.OW();
+  g.T = (s.R + s.sh - 1) / s.sh;
+  g.U = (s.S + s.sw - 1) / s.sw;
+  g.Hq = (s.H - 1 + s.ph) / s.sh + 1;
+  g.Wq = (s.W - 1 + s.pw) / s.sw + 1;
+  g.TR = std::max(1, kBM / std::max(1, g.Wq));
+  g.np = g.TR * g.Wq;
+  g.tiles_per_img = (g.Hq + g.TR - 1) / g.TR;
+  g.units = s.N * g.tiles_per_img;
+  g.grid = std::min(sm_count(), g.units);
+  g.BN = (s.C * s.sh * s.sw + 15) / 16 * 16;
+  g.AS = (g.BN + 31) / 32 * 32;
+  g.nslots = std::min(kMaxSlots, (512 - 2 * g.AS) / kBdKp);
+  g.PH = g.TR + g.T - 1;
+  // ring row: positions x = ow + U - 1 for every tap column read
+  g.XP = g.Wq + g.U - 1;
+  const std::size_t b_bytes = std::size_t(g.T * g.U * kBdKp / 32) * g.BN * 128;
+  const std::size_t fixed = b_bytes + 1024 + 1024;
+  const std::size_t row_bytes = std::size_t(g.XP) * kBdKS * 4;
+  int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
+  rr = std::min(rr, g.PH + (kHist - 2) * g.TR);
+  rr = std::min(rr, tune("fct_bd_ring", rr));
+  g.RR = std::max(rr, 1);
+  g.smem = fixed + row_bytes * g.RR;
+  (void)OH;
+  return g;
+}
+
+}  // namespace
+
+bool fct_bwdd_supports(const ConvShape& s) {
+  if (s.sh != s.sw || (s.sh != 2 && s.sh != 4) || s.C > 4 || s.K > kBdKp || !tune("fct_bd", 1)) return false;
+  const DGeo g = make_dgeo(s);
+  const int tu = g.T * g.U;
+  return (tu == 9 || tu == 4 || tu == 16) && g.Wq <= kBM && g.BN <= 64 && g.nslots >= 2 &&
+         g.RR >= g.PH + g.TR && g.smem <= 220 * 1024 && std::int64_t(s.N) * s.C * s.H * s.W < (1ll << 40);
+}
+
+cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha, float beta,
+                         cudaStream_t st) {
+  const DGeo g = make_dgeo(s);
+  DParams p{};
+  p.dy = dy; p.w = w; p.dx = dx; p.alpha = alpha; p.beta = beta;
+  p.C = s.C; p.H = s.H; p.W = s.W; p.K = s.K; p.R = s.R; p.S = s.S; p.ph = s.ph; p.pw = s.pw; p.sh = s.sh;
+  p.OH = s.OH(); p.OW = s.OW();
+  p.T = g.T; p.U = g.U; p.Hq = g.Hq; p.Wq = g.Wq; p.TR = g.TR; p.np = g.np; p.tiles_per_img = g.tiles_per_img;
+  p.units = g.units; p.BN = g.BN; p.AS = g.AS; p.nslots = g.nslots; p.RR = g.RR; p.XP = g.XP; p.PH = g.PH;
+  p.OHW = std::int64_t(p.OH) * p.OW;
+  p.KOHW = std::int64_t(s.K) * p.OHW;
+  p.CHW = std::int64_t(s.C) * s.H * s.W;
+  const int tu = g.T * g.U;
+  void (*kern)(const DParams) = nullptr;
+  if (s.sh == 4) kern = tu == 9 ? fct_bwdd_kernel<4, 9> : tu == 4 ? fct_bwdd_kernel<4, 4> : fct_bwdd_kernel<4, 16>;
+  else kern = tu == 9 ? fct_bwdd_kernel<2, 9> : tu == 4 ? fct_bwdd_kernel<2, 4> : fct_bwdd_kernel<2, 16>;
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
+  if (e != cudaSuccess) return e;
+  trace_variant("fct bwdd units=%d grid=%d TR=%d np=%d TU=%d BN=%d XP=%d ring=%d slots=%d", g.units, g.grid, g.TR,
+                g.np, tu, g.BN, g.XP, g.RR, g.nslots);
+  return launch_pdl(kern, dim3(g.grid), dim3(kBdThreads), g.smem, st, p);
 }
 
 }  // namespace ucudnn

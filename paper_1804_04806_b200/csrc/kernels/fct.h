@@ -20,4 +20,9 @@ std::int64_t fct_bwdf_workspace(const ConvShape& s);
 cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
                          float beta, cudaStream_t stream);
 
+bool fct_bwdd_supports(const ConvShape& s);
+// dx = alpha * conv_bwd_data(dy, w) + beta * dx; no workspace
+cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha, float beta,
+                         cudaStream_t stream);
+
 }  // namespace ucudnn

@@ -432,6 +432,7 @@ cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, fl
 cudaError_t igemm_backward_data(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha,
                                 float beta, cudaStream_t stream) {
   if (tune("z", 1) && z1x1_supports(kBwdData, s)) return z1x1_run(kBwdData, s, dy, w, dx, alpha, beta, stream);
+  if (tune("z", 1) && fct_bwdd_supports(s)) return fct_bwdd_run(s, dy, w, dx, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kBwdData, s)) return zgemm_backward_data(s, dy, w, dx, alpha, beta, stream);
   for (int pa = 0; pa < s.sh; ++pa)
     for (int pb = 0; pb < s.sw; ++pb) {

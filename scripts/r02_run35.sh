@@ -1,0 +1,5 @@
+#!/bin/bash
+for sp in "2 3 31 31 16 11 11 2 4" "3 3 227 227 64 11 11 0 4" "1 2 40 40 8 11 11 0 4" "3 4 30 30 24 5 5 2 2" "5 3 63 63 20 11 11 1 4" "2 1 20 20 5 3 3 1 2" "2 3 36 36 64 7 7 3 2" "3 3 47 51 64 11 11 2 4" "2 3 227 227 40 11 11 0 4"; do
+  timeout 60 python scripts/one_small.py $sp 1 0 2>&1 | grep -E "exact|rror|trace"
+done
+timeout 60 python scripts/one_conv.py --shape 256,3,227,227,64,11,11,0,4 --op 1 --algo 0 --batch 256 --reps 1 2>&1 | grep "blk 0"

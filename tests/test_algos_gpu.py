@@ -176,6 +176,10 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("z_bres=1", "2 3 31 31 16 11 11 2 4 1 0"),
                                        ("z_bres=1", "2 3 30 30 64 7 7 3 2 1 0"),
                                        ("z_bres=1", "3 5 13 13 7 5 5 2 1 1 0"),
+                                       ("fct_bd=0", "2 3 31 31 16 11 11 2 4 1 0"),
+                                       ("fct_bd=0", "2 3 36 36 70 7 7 3 2 1 0"),
+                                       ("fct_bd_ring=18", "3 3 63 63 20 11 11 1 4 1 0"),
+                                       ("fct_bd_ring=15", "2 3 36 36 64 7 7 3 2 1 0"),
                                        ("fct_bf=0", "2 3 31 31 16 11 11 2 4 2 6"),
                                        ("fct_bf=0", "2 3 36 36 70 7 7 3 2 2 6"),
                                        ("fct_bf_ring=15", "3 3 63 63 20 11 11 1 4 2 6"),
@@ -197,8 +201,10 @@ def test_knob_variants(cuda, tune, spec):
     GEMM's two pair sub-tiles per tile (pc2_msub=2, 512 rows, BN=256 with one
     accumulator set), the shared-memory-patch Forward behind the TMEM-operand
     one (fct=0), the shared-memory-patch BackwardFilter behind the TMEM-operand
-    one (fct_bf=0), and both TMEM-operand kernels' input-row rings at their
-    minimum depth (fct_ring / fct_bf_ring: loaders wait on almost every tile); UCUDNN_TUNE is read
+    one (fct_bf=0), the zero-workspace gather BackwardData behind the
+    TMEM-operand one (fct_bd=0), and the TMEM-operand kernels' row rings at
+    their minimum depth (fct_ring / fct_bf_ring / fct_bd_ring: loaders wait
+    on almost every tile); UCUDNN_TUNE is read
     once per process, so each runs in a child."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -210,5 +216,7 @@ def test_knob_variants(cuda, tune, spec):
         assert "precomp2" in out.stdout and "msub=2" in out.stdout, out.stdout
     if tune.startswith("fct_ring="):
         assert "fct fwd" in out.stdout and tune.replace("fct_", "") in out.stdout, out.stdout
+    if tune.startswith("fct_bd_ring="):
+        assert "fct bwdd" in out.stdout and tune.replace("fct_bd_", "") in out.stdout, out.stdout
     if tune.startswith("fct_bf_ring="):
         assert "fct bwdf" in out.stdout and tune.replace("fct_bf_", "") in out.stdout, out.stdout

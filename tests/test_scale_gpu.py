@@ -283,3 +283,4 @@ def test_zz_bench_scale_variants_exercised(cuda):
     assert {d["bmode"] for d in z} >= {"0", "2"}, "zgemm B paths not exercised"
     assert any(l.startswith("fct fwd ") for l in TRACE), "no TMEM-operand Forward (AlexNet conv1, algorithm 0)"
     assert any(l.startswith("fct bwdf ") for l in TRACE), "no TMEM-operand BackwardFilter (AlexNet conv1)"
+    assert any(l.startswith("fct bwdd ") for l in TRACE), "no TMEM-operand BackwardData (AlexNet conv1, algorithm 0)"

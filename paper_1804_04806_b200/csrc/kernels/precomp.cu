@@ -946,6 +946,7 @@ struct StripParams {
   FastDiv fd_blk;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
+  int msub;  // swap == 0: 128-position MMA sub-tiles per tile sharing each filter stage (1 or 2)
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -956,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t strip_bytes = std::uint32_t(p.nboxes * p.box_rows) * 128;
   const std::uint32_t tap_bytes = std::uint32_t(p.BN) * 128;  // swap: BN = 128 filter rows
-  const int tile_pos = p.swap ? 2 * kBM : kBM;
+  const int tile_pos = p.swap ? 2 * kBM : p.msub * kBM;
   const std::uint32_t stage_bytes = kTapsPerStage * tap_bytes;
   const int kStages = p.stages;
   unsigned char* strips = smem;
@@ -969,6 +970,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tempty = tfull + 2;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
   float* xpose = reinterpret_cast<float*>(ring + kStages * stage_bytes + 256);  // swap epilogue: 4 x 32 x 33
+  __shared__ std::uint32_t toff[64];  // tap -> strip row offset (r * Wp + s) in descriptor units (16 B)
+  for (int tap = threadIdx.x; tap < p.taps && tap < 64; tap += blockDim.x) {
+    const int r = tap / p.S, q = tap - r * p.S;
+    toff[tap] = std::uint32_t(r * p.Wp + q) * 8;
+  }
   if (threadIdx.x == 0) {
     prefetch_tmap(&xmap);
     for (int s = 0; s < kStages; ++s) {
@@ -1054,19 +1060,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
           mbar_wait(&full[st], (it / kStages) & 1);
           tc_fence_after();
-          {  // whole warp, one elected lane issues
+          if (p.swap) {  // whole warp, one elected lane issues
             for (int i = 0; i < ntap; ++i) {
-              const int tap = tap0 + i, r = tap / p.S, q = tap - r * p.S;
-              const std::uint32_t sa = sbase + sb * strip_bytes + std::uint32_t(r * p.Wp + q) * 128;
+              const int tap = tap0 + i;
+              const std::uint32_t sa = sbase + sb * strip_bytes + toff[tap] * 16;
               const std::uint32_t sbb = rbase + st * stage_bytes + i * tap_bytes;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                // swap: A = filter rows, B = 256 strip positions
-                const std::uint64_t da = umma_desc_sw128((p.swap ? sbb : sa) + k * 32);
-                const std::uint64_t db = umma_desc_sw128((p.swap ? sa : sbb) + k * 32);
-                mma_tf32_w(dtm, da, db, idesc, (cc | tap | k) != 0);
+              for (int k = 0; k < 4; ++k)  // A = filter rows, B = 256 strip positions
+                mma_tf32_w(dtm, umma_desc_sw128(sbb + k * 32), umma_desc_sw128(sa + k * 32), idesc, (cc | tap | k) != 0);
+            }
+          } else {
+            // descriptors are the strip / stage bases plus offsets: straight-line issue
+            const std::uint64_t ad0 = umma_desc_sw128(sbase + sb * strip_bytes);
+            const std::uint64_t bd0 = umma_desc_sw128(rbase + st * stage_bytes);
+#pragma unroll
+            for (int i = 0; i < kTapsPerStage; ++i) {
+              if (i >= ntap) break;
+              const int tap = tap0 + i;
+              const std::uint64_t ad = ad0 + toff[tap];
+              const std::uint64_t bd = bd0 + std::uint32_t(i) * (tap_bytes >> 4);
+              for (int m = 0; m < p.msub; ++m) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_tf32_w(dtm + std::uint32_t(m * p.BN), ad + std::uint32_t(m * kBM * 8 + 2 * k), bd + 2 * k, idesc,
+                             (cc | tap | k) != 0);
               }
             }
+          }
+          {
             mma_commit_w(&empty[st]);
             if (ts == tsteps - 1) mma_commit_w(&sempty[sb]);
             if (ts == tsteps - 1 && cc == p.c_chunks - 1) mma_commit_w(&tfull[acc]);
@@ -1126,7 +1147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&tempty[acc]);
         continue;
       }
-      const int pos = int(local) * kBM + ew * 32 + lane;  // flat position inside image n
+      for (int m = 0; m < p.msub; ++m) {
+      const int pos = int(local) * tile_pos + m * kBM + ew * 32 + lane;  // flat position inside image n
       std::uint32_t oh, ow;
       p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
       const bool ok = int(oh) < p.OH && int(ow) < p.OW;
@@ -1141,7 +1163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           obase = std::int64_t(n) * p.Nout * p.P + int(oh) * p.OW + int(ow);
         }
       }
-      const std::uint32_t tbase = tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN);
+      const std::uint32_t tbase =
+          tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN + m * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
@@ -1160,6 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_row32(p, p.out + obase + std::int64_t(col0) * p.P, min(32, min(p.BN - c0, p.Nout - col0)),
                       std::int64_t(p.P), v);
         }
+      }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -1258,6 +1282,7 @@ int phase_pair(const Geo& g) {
 // geometry of the padded input and of the per-chunk strip.
 struct StripGeo {
   bool ok = false, swap = false;
+  int msub = 1;
   int Hp = 0, Wp = 0, rows = 0, box_rows = 0, nboxes = 0, stages = 0;
   std::size_t strip_bytes = 0;
 };
@@ -1281,7 +1306,8 @@ StripGeo strip_geo(const Geo& g, int BN) {
   sg.Hp = g.Hin + g.ph + (g.ph_hi < 0 ? g.ph : g.ph_hi);
   sg.Wp = g.Win + g.pw + (g.pw_hi < 0 ? g.pw : g.pw_hi);
   if (sg.Hp - g.R + 1 != g.Hout || sg.Wp - g.S + 1 != g.Wout) return sg;
-  sg.rows = (sg.swap ? 2 * kBM : kBM) + (g.R - 1) * sg.Wp + (g.S - 1);
+  sg.msub = !sg.swap && BN <= 128 && tune("strip_msub", 2) == 2 ? 2 : 1;
+  sg.rows = (sg.swap ? 2 * kBM : sg.msub * kBM) + (g.R - 1) * sg.Wp + (g.S - 1);
   sg.box_rows = std::min(256, (sg.rows + 7) / 8 * 8);
   sg.nboxes = (sg.rows + sg.box_rows - 1) / sg.box_rows;
   sg.strip_bytes = std::size_t(sg.nboxes) * sg.box_rows * 128;
@@ -1353,7 +1379,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   p.OH = g.Hout;
   p.OW = g.Wout;
   p.swap = sg.swap ? 1 : 0;
-  const int tile_pos = sg.swap ? 2 * kBM : kBM;
+  p.msub = sg.msub;
+  const int tile_pos = sg.swap ? 2 * kBM : sg.msub * kBM;
   p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + tile_pos - 1) / tile_pos;
   p.m_tiles = g.N * p.tpi;
   p.taps = taps;
@@ -1386,8 +1413,11 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   }
   const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
-  e = set_smem_attr(reinterpret_cast<const void*>(strip_kernel), 227 * 1024);
+  // the launch's own size (the kernel also has a small static tap table)
+  e = set_smem_attr(reinterpret_cast<const void*>(strip_kernel), std::max(smem, 116 * 1024));
   if (e != cudaSuccess) return e;
+  trace_variant("strip swap=%d msub=%d m_tiles=%d n_tiles=%d BN=%d stages=%d boxes=%d", p.swap, p.msub, p.m_tiles,
+                p.n_tiles, BN, sg.stages, sg.nboxes);
   return launch_pdl(strip_kernel, dim3(std::min(sm_count(), p.m_tiles * p.n_tiles)), dim3(kThreads),
                     std::size_t(std::max(smem, 116 * 1024)), st, xmap, p);
 }

@@ -946,7 +946,9 @@ struct StripParams {
   FastDiv fd_blk;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
-  int msub;  // swap == 0: 128-position MMA sub-tiles per tile sharing each filter stage (1 or 2)
+  int msub;  // swap == 0: 128-position MMA sub-tiles per tile sharing each filter stage (1 .. 4)
+  int prof;  // UCUDNN_TUNE=prof=1: MMA-warp cycle split into g_prof (strip wait, stage wait, acc wait, total)
+  int nsb;   // strip buffers (2; 1 when a wide tile's strip would leave too few filter stages)
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -961,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t stage_bytes = kTapsPerStage * tap_bytes;
   const int kStages = p.stages;
   unsigned char* strips = smem;
-  unsigned char* ring = smem + 2 * strip_bytes;
+  unsigned char* ring = smem + p.nsb * strip_bytes;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + kStages * stage_bytes);
   std::uint64_t* empty = full + kMaxStages;
   std::uint64_t* sfull = empty + kMaxStages;
@@ -1009,8 +1011,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.fd_tpi.divmod(mt, n, local);
         const int p0 = int(n) * p.HWp + int(local) * tile_pos;
         for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
-          const int sb = sc & 1;
-          mbar_wait(&sempty[sb], ((sc >> 1) & 1) ^ 1);
+          const int sb = sc % p.nsb;
+          mbar_wait(&sempty[sb], ((sc / p.nsb) & 1) ^ 1);
           mbar_expect_tx(&sfull[sb], strip_bytes);
           for (int bx = 0; bx < p.nboxes; ++bx)
             tma_2d(strips + sb * strip_bytes + bx * p.box_rows * 128, &xmap, &sfull[sb], cc * 32,
@@ -1046,19 +1048,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t idesc = idesc_tf32(kBM, p.swap ? 2 * kBM : p.BN);
     const std::uint32_t sbase = smem_u32(strips), rbase = smem_u32(ring);
     int it = 0, sc = 0, tl = 0;
+    long long c_strip = 0, c_stage = 0, c_acc = 0, t_start = clock64(), cq = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       const int acc = tl & 1;
+      if (p.prof) cq = clock64();
       mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+      if (p.prof) c_acc += clock64() - cq;
       tc_fence_after();
       const std::uint32_t dtm = tmem + std::uint32_t(acc * kMaxBN);
       for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
-        const int sb = sc & 1;
-        mbar_wait(&sfull[sb], (sc >> 1) & 1);
+        const int sb = sc % p.nsb;
+        if (p.prof) cq = clock64();
+        mbar_wait(&sfull[sb], (sc / p.nsb) & 1);
+        if (p.prof) c_strip += clock64() - cq;
         tc_fence_after();
         for (int ts = 0; ts < tsteps; ++ts, ++it) {
           const int st = it % kStages;
           const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
+          if (p.prof) cq = clock64();
           mbar_wait(&full[st], (it / kStages) & 1);
+          if (p.prof) c_stage += clock64() - cq;
           tc_fence_after();
           if (p.swap) {  // whole warp, one elected lane issues
             for (int i = 0; i < ntap; ++i) {
@@ -1095,6 +1104,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       }
+    }
+    if (p.prof && lane == 0 && blockIdx.x < 1024) {
+      g_prof[blockIdx.x * 4 + 0] = c_strip + c_stage;
+      g_prof[blockIdx.x * 4 + 1] = c_stage;
+      g_prof[blockIdx.x * 4 + 2] = c_acc;
+      g_prof[blockIdx.x * 4 + 3] = clock64() - t_start;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
@@ -1282,7 +1297,7 @@ int phase_pair(const Geo& g) {
 // geometry of the padded input and of the per-chunk strip.
 struct StripGeo {
   bool ok = false, swap = false;
-  int msub = 1;
+  int msub = 1, nsb = 2;
   int Hp = 0, Wp = 0, rows = 0, box_rows = 0, nboxes = 0, stages = 0;
   std::size_t strip_bytes = 0;
 };
@@ -1306,15 +1321,20 @@ StripGeo strip_geo(const Geo& g, int BN) {
   sg.Hp = g.Hin + g.ph + (g.ph_hi < 0 ? g.ph : g.ph_hi);
   sg.Wp = g.Win + g.pw + (g.pw_hi < 0 ? g.pw : g.pw_hi);
   if (sg.Hp - g.R + 1 != g.Hout || sg.Wp - g.S + 1 != g.Wout) return sg;
-  sg.msub = !sg.swap && BN <= 128 && tune("strip_msub", 2) == 2 ? 2 : 1;
+  sg.msub = sg.swap ? 1 : std::max(1, std::min(std::min(4, tune("strip_msub", 2)), 256 / std::max(BN, 1)));
   sg.rows = (sg.swap ? 2 * kBM : sg.msub * kBM) + (g.R - 1) * sg.Wp + (g.S - 1);
   sg.box_rows = std::min(256, (sg.rows + 7) / 8 * 8);
   sg.nboxes = (sg.rows + sg.box_rows - 1) / sg.box_rows;
   sg.strip_bytes = std::size_t(sg.nboxes) * sg.box_rows * 128;
   const std::size_t stage = std::size_t(kTapsPerStage) * BN * 128;
   const std::size_t budget = 210 * 1024 - (sg.swap ? 4 * 32 * 33 * 4 : 0);
-  if (2 * sg.strip_bytes + 2 * stage > budget) return sg;
-  sg.stages = int(std::min<std::size_t>(kMaxStages, (budget - 2 * sg.strip_bytes) / stage));
+  // two strip buffers unless that leaves fewer than 6 filter stages (a
+  // filter stage refill takes ~1-2 us: with 3 stages the 4-sub-tile tile
+  // waited on filters 54 % of the time); one buffer stalls each chunk change
+  sg.nsb = 2;
+  if ((budget - std::min(budget, 2 * sg.strip_bytes)) / stage < 6 && tune("strip_nsb", 0) != 2) sg.nsb = 1;
+  if (sg.nsb * sg.strip_bytes + 2 * stage > budget) return sg;
+  sg.stages = int(std::min<std::size_t>(kMaxStages, (budget - sg.nsb * sg.strip_bytes) / stage));
   sg.ok = true;
   return sg;
 }
@@ -1380,6 +1400,8 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   p.OW = g.Wout;
   p.swap = sg.swap ? 1 : 0;
   p.msub = sg.msub;
+  p.nsb = sg.nsb;
+  p.prof = tune("prof", 0);
   const int tile_pos = sg.swap ? 2 * kBM : sg.msub * kBM;
   p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + tile_pos - 1) / tile_pos;
   p.m_tiles = g.N * p.tpi;
@@ -1411,13 +1433,13 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.bp = g.pf.P;
     p.fd_blk = FastDiv(std::uint32_t(p.sAh * g.pf.bw * g.pf.C));
   }
-  const int smem = int(2 * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
+  const int smem = int(sg.nsb * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
   // the launch's own size (the kernel also has a small static tap table)
   e = set_smem_attr(reinterpret_cast<const void*>(strip_kernel), std::max(smem, 116 * 1024));
   if (e != cudaSuccess) return e;
-  trace_variant("strip swap=%d msub=%d m_tiles=%d n_tiles=%d BN=%d stages=%d boxes=%d", p.swap, p.msub, p.m_tiles,
-                p.n_tiles, BN, sg.stages, sg.nboxes);
+  trace_variant("strip swap=%d msub=%d nsb=%d m_tiles=%d n_tiles=%d BN=%d stages=%d boxes=%d", p.swap, p.msub, p.nsb,
+                p.m_tiles, p.n_tiles, BN, sg.stages, sg.nboxes);
   return launch_pdl(strip_kernel, dim3(std::min(sm_count(), p.m_tiles * p.n_tiles)), dim3(kThreads),
                     std::size_t(std::max(smem, 116 * 1024)), st, xmap, p);
 }

@@ -53,11 +53,12 @@ constexpr int kBM = 128;
 constexpr int kMaxSlots = 8;
 constexpr int kNB = 8;        // tile barriers (ring of tiles in flight between loaders and producers)
 constexpr int kHist = 8;      // loader's history of tile row origins (>= the lookahead)
-constexpr int kLoaders = 7;   // loader warps (20 warps in all: 5 per SM sub-partition, 96 registers)
+// Forward: 20 warps (5 per SM sub-partition: 96 registers; 21 would get 80)
+constexpr int kFwdWarps = 20;
 constexpr int kRB = 4;        // ring rows per loader batch (8 x 32 columns each)
 constexpr int kMaxGroups = 64;
-// warps: 0-7 A producers, 8-11 epilogue, 12 MMA issuer, 13-19 row loaders
-constexpr int kThreads = (13 + kLoaders) * 32;
+// warps: 0-7 A producers, 8 MMA issuer, 9 .. 8+nepi epilogue, the rest row loaders
+constexpr int kThreads = kFwdWarps * 32;
 
 struct TGeo {
   int OH, OW, TR, np, tiles_per_img, units, grid;
@@ -74,6 +75,7 @@ struct TParams {
   int C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
   int TR, np, tiles_per_img, units;
   int groups, kslots, nchunk, BN, PH, pitch, nslots, RR;
+  int nepi;  // epilogue warps (4 or 8); the loaders get the other 11 - nepi
   int dbg;  // UCUDNN_TUNE=fct_dbg=1: per-role wait cycles of CTAs 0-1 (printf)
   long long CHW, KOHW;
 };
@@ -248,16 +250,16 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       mbar_init(&aempty[s], 1);
     }
     for (int b = 0; b < kNB; ++b) {
-      mbar_init(&loaded[b], kLoaders * 32);
+      mbar_init(&loaded[b], (11 - p.nepi) * 32);
       mbar_init(&consumed[b], 256);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], p.nepi * 32);
     }
     mbar_fence_init();
   }
-  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
   fence_async_smem();  // the filter stores are read by the tensor core
   tc_fence_before();
   __syncthreads();
@@ -316,9 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       mbar_arrive(&consumed[i % kNB]);  // this thread's ring reads are done (their values went to TMEM)
     }
     FCT_PRINT("prod (loaded, slot)");
-  } else if (warp < 12) {
-    // ------------------------------------------------ epilogue (NCHW stores, lane = pixel)
-    const int quarter = warp & 3, half = 0;
+  } else if (warp >= 9 && warp < 9 + p.nepi) {
+    // ------------------------------------------------ epilogue (NCHW stores, lane = pixel); with 8
+    // warps (store-heavy layers: few input rows per tile) two take each lane quarter
+    const int quarter = warp & 3, half = (warp - 9) >> 2, nh = p.nepi >> 2;
     const int px = quarter * 32 + lane;
     const int rl = px / p.OW, ow = px - rl * p.OW;
     const long long ks = (long long)p.OH * p.OW;
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       tc_fence_after();
       const bool live = px < p.np && oh0 + rl < p.OH;
       float* yb = p.y + (long long)n * p.KOHW + (long long)(oh0 + rl) * p.OW + ow;
-      for (int c0 = half * 32; c0 < p.BN; c0 += 32) {
+      for (int c0 = half * 32; c0 < p.BN; c0 += 32 * nh) {
         float v[32];
         tmem_ld32(tmem + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * p.BN + c0), v);
         if (!live) continue;
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       mbar_arrive(&tempty[acc]);
     }
     FCT_PRINT("epi (tfull, -)");
-  } else if (warp == 12) {
+  } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
     // A slot spans KG * SP / 32 whole filter chunks, so every descriptor is
     // the slot's base plus a compile-time step: straight-line issue code
@@ -379,9 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       }
     }
     FCT_PRINT("mma (tempty, afull)");
-  } else {
+  } else if (warp >= 9 + p.nepi) {
     // ------------------------------------------------ row loaders (zero off the image)
-    const int lw = warp - 13;
+    const int lw = warp - 9 - p.nepi, nl = 11 - p.nepi;
     RowWalk walk;
     __shared__ int hist[kHist];  // vstart of the last kHist tiles (shared: a local array spilled to L2-latency local memory)
     int waited = -1;  // every tile <= waited has been consumed
@@ -411,11 +414,11 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       const float* xn = p.x + (long long)n * p.CHW;
       const int nrows = p.C * cnt;
       for (int cb = 0; cb < p.pitch; cb += 256) {
-        for (int q0 = lw; q0 < nrows; q0 += kLoaders * kRB) {
+        for (int q0 = lw; q0 < nrows; q0 += nl * kRB) {
           float v[kRB][8];
 #pragma unroll
           for (int rb = 0; rb < kRB; ++rb) {
-            const int q = q0 + rb * kLoaders;
+            const int q = q0 + rb * nl;
             const int c = q / cnt, vr = lo + q - c * cnt;
             const int ih = oh0 * p.sh - p.ph + (vr - walk.vstart);
             const bool rok = q < nrows && unsigned(ih) < unsigned(p.H);
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
           }
 #pragma unroll
           for (int rb = 0; rb < kRB; ++rb) {
-            const int q = q0 + rb * kLoaders;
+            const int q = q0 + rb * nl;
             if (q >= nrows) break;
             const int c = q / cnt, vr = lo + q - c * cnt;
             float* dst = ring + (c * p.RR + vr % p.RR) * p.pitch + cb + lane;
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_free<512>(tmem);
   }
@@ -1163,6 +1166,8 @@ cudaError_t fct_fwd_run(const ConvShape& s, const float* x, const float* w, floa
   p.TR = g.TR; p.np = g.np; p.tiles_per_img = g.tiles_per_img; p.units = g.units;
   p.groups = g.groups; p.kslots = g.kslots; p.nchunk = g.nchunk; p.BN = g.BN; p.PH = g.PH; p.pitch = g.pitch;
   p.nslots = g.nslots; p.RR = g.RR;
+  // few new input rows per tile (ResNet conv1: 2 x 3) -> store-bound: 8 epilogue warps
+  p.nepi = tune("fct_epi", s.C * g.TR * s.sh <= 8 ? 8 : 4) == 8 ? 8 : 4;
   p.dbg = tune("fct_dbg", 0);
   p.CHW = std::int64_t(s.C) * s.H * s.W;
   p.KOHW = std::int64_t(s.K) * g.OH * g.OW;

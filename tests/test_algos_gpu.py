@@ -184,6 +184,9 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct_bf=0", "2 3 36 36 70 7 7 3 2 2 6"),
                                        ("fct_bf_ring=15", "3 3 63 63 20 11 11 1 4 2 6"),
                                        ("fct_bf_ring=9", "3 3 36 36 64 7 7 3 2 2 6"),
+                                       ("fct_epi=8", "2 3 31 31 16 11 11 2 4 0 0"),
+                                       ("fct_epi=8", "2 3 36 36 70 7 7 3 2 0 0"),
+                                       ("fct_epi=4", "2 3 224 224 64 7 7 3 2 0 0"),
                                        ("fct=0", "2 3 31 31 16 11 11 2 4 0 0"),
                                        ("fct=0", "2 3 36 36 70 7 7 3 2 0 0"),
                                        ("fct_ring=79", "4 3 63 63 20 11 11 1 4 0 0"),

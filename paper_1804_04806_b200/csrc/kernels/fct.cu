@@ -800,14 +800,14 @@ struct DParams {
   float* dx;
   float alpha, beta;
   int C, H, W, K, R, S, ph, pw, sh, OH, OW;
-  int T, U, Hq, Wq, TR, np, tiles_per_img, units, BN, AS, nslots, RR, XP, PH;
+  int T, U, Hq, Wq, TR, np, tps, SW, nstrip, units, BN, AS, nslots, RR, XP, PH;
   long long OHW, KOHW, CHW;
 };
 
 struct RowWalkD {
   int vstart = 0, vend = 0, n = -1;
   __device__ __forceinline__ bool next(const DParams& p, int u) {
-    const int nn = u / p.tiles_per_img;
+    const int nn = u / p.tps;  // (image, column strip)
     const bool fresh = nn != n;
     vstart = fresh ? vend : vstart + p.TR;
     vend = vstart + p.PH;
@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     const int px = quarter * 32 + lane;
     const bool pok = px < p.np;
     const int pe = pok ? px : 0;
-    const int rl = pe / p.Wq, j = pe - rl * p.Wq;
+    const int rl = pe / p.SW, jl = pe - rl * p.SW;  // strip-local phase column
     const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16);
     const int k0 = half * 32;
     RowWalkD walk;
@@ -905,7 +905,7 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         // ring row of dy row i - t, position j - u (+ U - 1): its 32 channels are contiguous
         const int prow = (walk.vstart + rl + p.T - 1 - t) % p.RR;
         const std::uint32_t addr =
-            smem_u32(ring) + std::uint32_t(((prow * p.XP + j - u + p.U - 1) * kBdKS + k0) * 4);
+            smem_u32(ring) + std::uint32_t(((prow * p.XP + jl - u + p.U - 1) * kBdKS + k0) * 4);
         const int slot = g % p.nslots;
         FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
         tc_fence_after();
@@ -930,18 +930,19 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     // alignment (uniform across the warp) allows
     const int quarter = warp & 3;
     const int px = quarter * 32 + lane;
-    const int rl = px / p.Wq, j = px - rl * p.Wq;
+    const int rl = px / p.SW, jl = px - rl * p.SW;
     const long long HW = (long long)p.H * p.W;
-    const int w0 = j * SH - p.pw;
-    const bool wall = w0 >= 0 && w0 + SH <= p.W;  // all SH columns on the image
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       const int u_ = t0 + i;
-      const int n = u_ / p.tiles_per_img, ii = (u_ - n * p.tiles_per_img) * p.TR + rl;
+      const int key = u_ / p.tps, n = key / p.nstrip;
+      const int j = (key - n * p.nstrip) * p.SW + jl, ii = (u_ - key * p.tps) * p.TR + rl;
+      const int w0 = j * SH - p.pw;
+      const bool wall = w0 >= 0 && w0 + SH <= p.W;  // all SH columns on the image
       const int acc = i & 1;
       FCT_W(t_w1, mbar_wait_sleep(&tfull[acc], (i >> 1) & 1));
       tc_fence_after();
-      const bool live = px < p.np && ii < p.Hq;
+      const bool live = px < p.np && ii < p.Hq && j < p.Wq;
       const int h0 = ii * SH - p.ph;
       float* dxn = p.dx + (long long)n * p.CHW;
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
@@ -1034,7 +1035,8 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     for (int i = 0; i < my_units; ++i) {
       const int u_ = t0 + i;
       const bool fresh = walk.next(p, u_);
-      const int n = u_ / p.tiles_per_img, i0 = (u_ - n * p.tiles_per_img) * p.TR;
+      const int key = u_ / p.tps, n = key / p.nstrip, j0 = (key - n * p.nstrip) * p.SW;
+      const int i0 = (u_ - key * p.tps) * p.TR;
       const int lo = fresh ? walk.vstart : walk.vend - p.TR;
       const int cnt = walk.vend - lo;
       const int ov = walk.vend - 1 - p.RR;
@@ -1064,8 +1066,8 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         float v[2][kBdKp / 16][4];
 #pragma unroll
         for (int xb = 0; xb < 2; ++xb) {
-          const int ow = xb * 32 + lane - (p.U - 1);
-          const bool ok = yok && xb < nxb && unsigned(ow) < unsigned(p.OW);
+          const int ow = j0 + xb * 32 + lane - (p.U - 1);
+          const bool ok = yok && xb < nxb && xb * 32 + lane < p.XP && unsigned(ow) < unsigned(p.OW);
 #pragma unroll
           for (int qq = 0; qq < kBdKp / 16; ++qq)
 #pragma unroll
@@ -1257,7 +1259,7 @@ cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, fl
 namespace {
 
 struct DGeo {
-  int T, U, Hq, Wq, TR, np, tiles_per_img, units, grid, BN, AS, nslots, RR, XP, PH;
+  int T, U, Hq, Wq, TR, np, tps, SW, nstrip, units, grid, BN, AS, nslots, RR, XP, PH;
   std::size_t smem;
 };
 
@@ -1268,25 +1270,31 @@ DGeo make_dgeo(const ConvShape& s) {
   g.U = (s.S + s.sw - 1) / s.sw;
   g.Hq = (s.H - 1 + s.ph) / s.sh + 1;
   g.Wq = (s.W - 1 + s.pw) / s.sw + 1;
-  g.TR = std::max(1, kBM / std::max(1, g.Wq));
-  g.np = g.TR * g.Wq;
-  g.tiles_per_img = (g.Hq + g.TR - 1) / g.TR;
-  g.units = s.N * g.tiles_per_img;
-  g.grid = std::min(sm_count(), g.units);
   g.BN = (s.C * s.sh * s.sw + 15) / 16 * 16;
   g.AS = (g.BN + 31) / 32 * 32;
   g.nslots = std::min(kMaxSlots, (512 - 2 * g.AS) / kBdKp);
-  g.PH = g.TR + g.T - 1;
-  // ring row: positions x = ow + U - 1 for every tap column read
-  g.XP = g.Wq + g.U - 1;
   const std::size_t b_bytes = std::size_t(g.T * g.U * kBdKp / 32) * g.BN * 128;
   const std::size_t fixed = b_bytes + 1024 + 1024;
-  const std::size_t row_bytes = std::size_t(g.XP) * kBdKS * 4;
-  int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
-  rr = std::min(rr, g.PH + (kHist - 2) * g.TR);
-  rr = std::min(rr, tune("fct_bd_ring", rr));
-  g.RR = std::max(rr, 1);
-  g.smem = fixed + row_bytes * g.RR;
+  // column strips (each a separate pass down the image) until the dy-row
+  // ring holds two tiles' rows and a strip's positions fit two 32-blocks
+  const int force = tune("fct_bd_strips", 0);
+  for (g.nstrip = force > 0 ? force : 1; g.nstrip <= 8; ++g.nstrip) {
+    g.SW = (g.Wq + g.nstrip - 1) / g.nstrip;
+    g.XP = g.SW + g.U - 1;  // ring positions x = ow - strip origin + U - 1
+    g.TR = std::max(1, kBM / g.SW);
+    g.PH = g.TR + g.T - 1;
+    const std::size_t row_bytes = std::size_t(g.XP) * kBdKS * 4;
+    int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
+    rr = std::min(rr, g.PH + (kHist - 2) * g.TR);
+    rr = std::min(rr, tune("fct_bd_ring", rr));
+    g.RR = std::max(rr, 1);
+    g.smem = fixed + row_bytes * g.RR;
+    if (force > 0 || (g.XP <= 64 && g.RR >= g.PH + g.TR)) break;
+  }
+  g.np = g.TR * g.SW;
+  g.tps = (g.Hq + g.TR - 1) / g.TR;
+  g.units = s.N * g.nstrip * g.tps;
+  g.grid = std::min(sm_count(), g.units);
   (void)OH;
   return g;
 }
@@ -1297,7 +1305,7 @@ bool fct_bwdd_supports(const ConvShape& s) {
   if (s.sh != s.sw || (s.sh != 2 && s.sh != 4) || s.C > 4 || s.K > kBdKp || !tune("fct_bd", 1)) return false;
   const DGeo g = make_dgeo(s);
   const int tu = g.T * g.U;
-  return (tu == 9 || tu == 4 || tu == 16) && g.Wq <= kBM && g.BN <= 64 && g.nslots >= 2 &&
+  return (tu == 9 || tu == 4 || tu == 16) && g.nstrip <= 8 && g.XP <= 64 && g.BN <= 64 && g.nslots >= 2 &&
          g.RR >= g.PH + g.TR && g.smem <= 220 * 1024 && std::int64_t(s.N) * s.C * s.H * s.W < (1ll << 40);
 }
 
@@ -1308,7 +1316,7 @@ cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, fl
   p.dy = dy; p.w = w; p.dx = dx; p.alpha = alpha; p.beta = beta;
   p.C = s.C; p.H = s.H; p.W = s.W; p.K = s.K; p.R = s.R; p.S = s.S; p.ph = s.ph; p.pw = s.pw; p.sh = s.sh;
   p.OH = s.OH(); p.OW = s.OW();
-  p.T = g.T; p.U = g.U; p.Hq = g.Hq; p.Wq = g.Wq; p.TR = g.TR; p.np = g.np; p.tiles_per_img = g.tiles_per_img;
+  p.T = g.T; p.U = g.U; p.Hq = g.Hq; p.Wq = g.Wq; p.TR = g.TR; p.np = g.np; p.tps = g.tps; p.SW = g.SW; p.nstrip = g.nstrip;
   p.units = g.units; p.BN = g.BN; p.AS = g.AS; p.nslots = g.nslots; p.RR = g.RR; p.XP = g.XP; p.PH = g.PH;
   p.OHW = std::int64_t(p.OH) * p.OW;
   p.KOHW = std::int64_t(s.K) * p.OHW;
@@ -1319,8 +1327,8 @@ cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, fl
   else kern = tu == 9 ? fct_bwdd_kernel<2, 9> : tu == 4 ? fct_bwdd_kernel<2, 4> : fct_bwdd_kernel<2, 16>;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
   if (e != cudaSuccess) return e;
-  trace_variant("fct bwdd units=%d grid=%d TR=%d np=%d TU=%d BN=%d XP=%d ring=%d slots=%d", g.units, g.grid, g.TR,
-                g.np, tu, g.BN, g.XP, g.RR, g.nslots);
+  trace_variant("fct bwdd units=%d grid=%d TR=%d np=%d strips=%d TU=%d BN=%d XP=%d ring=%d slots=%d", g.units,
+                g.grid, g.TR, g.np, g.nstrip, tu, g.BN, g.XP, g.RR, g.nslots);
   return launch_pdl(kern, dim3(g.grid), dim3(kBdThreads), g.smem, st, p);
 }
 

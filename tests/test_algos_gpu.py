@@ -180,6 +180,9 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct_bd=0", "2 3 36 36 70 7 7 3 2 1 0"),
                                        ("fct_bd_ring=18", "3 3 63 63 20 11 11 1 4 1 0"),
                                        ("fct_bd_ring=15", "2 3 36 36 64 7 7 3 2 1 0"),
+                                       ("fct_bd_strips=2", "2 3 36 36 64 7 7 3 2 1 0"),
+                                       ("fct_bd_strips=3", "3 3 47 51 64 11 11 2 4 1 0"),
+                                       ("", "2 3 100 140 32 7 7 3 2 1 0"),
                                        ("fct_bf=0", "2 3 31 31 16 11 11 2 4 2 6"),
                                        ("fct_bf=0", "2 3 36 36 70 7 7 3 2 2 6"),
                                        ("fct_bf_ring=15", "3 3 63 63 20 11 11 1 4 2 6"),
@@ -219,6 +222,8 @@ def test_knob_variants(cuda, tune, spec):
         assert "precomp2" in out.stdout and "msub=2" in out.stdout, out.stdout
     if tune.startswith("fct_ring="):
         assert "fct fwd" in out.stdout and tune.replace("fct_", "") in out.stdout, out.stdout
+    if tune.startswith("fct_bd_strips="):
+        assert "fct bwdd" in out.stdout and "strips=" + tune.split("=")[1] in out.stdout, out.stdout
     if tune.startswith("fct_bd_ring="):
         assert "fct bwdd" in out.stdout and tune.replace("fct_bd_", "") in out.stdout, out.stdout
     if tune.startswith("fct_bf_ring="):

@@ -122,6 +122,16 @@ __device__ __forceinline__ void mma_tf32_ts_warp(std::uint32_t d_tmem, std::uint
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_tf32_ts_2sm_warp(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t bdesc,
+                                                     std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_warp(std::uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -816,7 +826,7 @@ struct RowWalkD {
   }
 };
 
-template <int SH, int TU>
+template <int SH, int TU, bool PAIR>
 __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -824,7 +834,11 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kChunks = TU * kBdKp / 32;
-  const std::uint32_t b_bytes = std::uint32_t(kChunks) * p.BN * 128;
+  // CTA pair: each CTA holds half of the filter's N rows and its own 128
+  // lanes of A and D; rank 0 issues M = 256 MMAs for both
+  const std::uint32_t rank = PAIR ? cluster_rank() : 0;
+  const int BH = PAIR ? p.BN / 2 : p.BN;  // filter rows held here
+  const std::uint32_t b_bytes = std::uint32_t(kChunks) * BH * 128;
   float* ring = reinterpret_cast<float*>(smem + b_bytes);  // [RR][XP][kBdKS]
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(ring + p.RR * p.XP * kBdKS);
   std::uint64_t* afull = bars;
@@ -838,11 +852,11 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
   // the filter as B[(c, a, b)][(t, u, k)] = w[k][c][a + sh t][b + sh u] (0 off the filter),
   // K-major SWIZZLE_128B, BN rows per 32-column chunk
   {
-    const int per_chunk = p.BN * 32;
+    const int per_chunk = BH * 32;
     const int total = kChunks * per_chunk;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
       const int chunk = i / per_chunk, rem = i - chunk * per_chunk;
-      const int row = rem >> 5, j = rem & 31;
+      const int lrow = rem >> 5, j = rem & 31, row = int(rank) * BH + lrow;
       const int kk = chunk * 32 + j;
       const int tu = kk / kBdKp, k = kk - tu * kBdKp;
       const int t = tu / p.U, u = tu - t * p.U;
@@ -850,13 +864,13 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
       const int r = a + p.sh * t, q = b + p.sh * u;
       float v = 0.f;
       if (c < p.C && k < p.K && r < p.R && q < p.S) v = p.w[((long long)(k * p.C + c) * p.R + r) * p.S + q];
-      *reinterpret_cast<float*>(smem + chunk * p.BN * 128 + row * 128 + (((j >> 2) ^ (row & 7)) << 4) + (j & 3) * 4) =
+      *reinterpret_cast<float*>(smem + chunk * BH * 128 + lrow * 128 + (((j >> 2) ^ (lrow & 7)) << 4) + (j & 3) * 4) =
           v;
     }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxSlots; ++s) {
-      mbar_init(&afull[s], 256);
+      mbar_init(&afull[s], PAIR ? 512 : 256);  // PAIR: both CTAs' producers, on rank 0's barrier
       mbar_init(&aempty[s], 1);
     }
     for (int b = 0; b < kNB; ++b) {
@@ -865,22 +879,37 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], PAIR ? 256 : 128);
     }
     mbar_fence_init();
   }
-  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  if (warp == 12) {
+    if constexpr (PAIR) tmem_alloc_2sm<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs' barriers initialised before any remote arrive
   tc_fence_after();
   const std::uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  int t0, t1;
-  {
+  // units: contiguous runs; a pair splits its run in two halves, the second
+  // CTA padding its half with a dummy tile when the run is odd (both CTAs
+  // must feed every pair MMA)
+  int t0, my_units, real_units;
+  if constexpr (PAIR) {
+    const int pairs = gridDim.x >> 1, pid = blockIdx.x >> 1;
+    const int pa0 = int((long long)pid * p.units / pairs), pa1 = int((long long)(pid + 1) * p.units / pairs);
+    const int h = (pa1 - pa0 + 1) >> 1;
+    t0 = rank == 0 ? pa0 : pa0 + h;
+    my_units = h;
+    real_units = rank == 0 ? h : pa1 - pa0 - h;
+  } else {
     t0 = int((long long)blockIdx.x * p.units / gridDim.x);
-    t1 = int((long long)(blockIdx.x + 1) * p.units / gridDim.x);
+    my_units = real_units = int((long long)(blockIdx.x + 1) * p.units / gridDim.x) - t0;
   }
-  const int my_units = t1 - t0;
+  const std::uint32_t afull0 = PAIR ? mapa(smem_u32(&afull[0]), 0) : 0;
+  const std::uint32_t tempty0 = PAIR ? mapa(smem_u32(&tempty[0]), 0) : 0;
   const std::uint32_t a_col0 = 2u * std::uint32_t(p.AS);
 
   if (warp < 8) {
@@ -918,7 +947,8 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         tmem_st32(tlane + a_col0 + std::uint32_t(slot * kBdKp + half * 32), v);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&afull[slot]);
+        if constexpr (PAIR) mbar_arrive_remote(afull0 + std::uint32_t(slot) * 8);
+        else mbar_arrive(&afull[slot]);
       }
       mbar_arrive(&consumed[i % kNB]);
     }
@@ -942,7 +972,7 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
       const int acc = i & 1;
       FCT_W(t_w1, mbar_wait_sleep(&tfull[acc], (i >> 1) & 1));
       tc_fence_after();
-      const bool live = px < p.np && ii < p.Hq && j < p.Wq;
+      const bool live = px < p.np && ii < p.Hq && j < p.Wq && i < real_units;
       const int h0 = ii * SH - p.ph;
       float* dxn = p.dx + (long long)n * p.CHW;
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
@@ -990,14 +1020,18 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) mbar_arrive_remote(tempty0 + std::uint32_t(acc) * 8);
+      else mbar_arrive(&tempty[acc]);
     }
     FCT_PRINT("bd epi (tfull, -)");
   } else if (warp == 12) {
-    // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
-    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    // ------------------------------------------------ MMA issuer (whole warp, one elected lane;
+    // PAIR: rank 0 only, M = 256 over both CTAs' lanes, commits multicast to both)
+    if (PAIR && rank != 0) goto mma_done;
+    {
+    const std::uint32_t idesc = idesc_tf32(PAIR ? 2 * kBM : kBM, p.BN);
     const std::uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem));
-    const std::uint32_t chunk_desc = std::uint32_t(p.BN * 128) >> 4;
+    const std::uint32_t chunk_desc = std::uint32_t(BH * 128) >> 4;
     int g = 0;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
@@ -1012,16 +1046,28 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         tc_fence_after();
         const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * kBdKp);
 #pragma unroll
-        for (int m = 0; m < kBdKp / 8; ++m)
-          mma_tf32_ts_warp(d, ta + std::uint32_t(8 * m), bd + (m >> 2) * chunk_desc + 2 * (m & 3), idesc,
-                           (tu | m) ? 1u : 0u);
-        mma_commit_warp(&aempty[slot]);
-        if (tu + 1 == TU) mma_commit_warp(&tfull[acc]);
+        for (int m = 0; m < kBdKp / 8; ++m) {
+          if constexpr (PAIR)
+            mma_tf32_ts_2sm_warp(d, ta + std::uint32_t(8 * m), bd + (m >> 2) * chunk_desc + 2 * (m & 3), idesc,
+                                 (tu | m) ? 1u : 0u);
+          else
+            mma_tf32_ts_warp(d, ta + std::uint32_t(8 * m), bd + (m >> 2) * chunk_desc + 2 * (m & 3), idesc,
+                             (tu | m) ? 1u : 0u);
+        }
+        if constexpr (PAIR) {
+          mma_commit_2sm_w(&aempty[slot], 3);
+          if (tu + 1 == TU) mma_commit_2sm_w(&tfull[acc], 3);
+        } else {
+          mma_commit_warp(&aempty[slot]);
+          if (tu + 1 == TU) mma_commit_warp(&tfull[acc]);
+        }
         __syncwarp();
         bd += (kBdKp / 32) * chunk_desc;
       }
     }
     FCT_PRINT("bd mma (tempty, afull)");
+    }
+  mma_done:;
   } else {
     // ------------------------------------------------ dy-row loaders: the dy rows each tile adds,
     // transposed to [position][channel] (4 channels per lane: 4 coalesced
@@ -1055,10 +1101,11 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         if (lane == 0) hist[i % kHist] = walk.vstart;
         __syncwarp();
       }
-      const float* dyn = p.dy + (long long)n * p.KOHW;
+      const float* dyn = p.dy + (long long)(i < real_units ? n : 0) * p.KOHW;
       // warp lw owns channel quads lw, lw + 4, .. (16 channels); per new row,
-      // every (position block, quad) of the warp is in flight at once
-      for (int rr = 0; rr < cnt; ++rr) {
+      // every (position block, quad) of the warp is in flight at once (a
+      // pair's dummy tile loads nothing: its rows are never stored)
+      for (int rr = 0; rr < (i < real_units ? cnt : 0); ++rr) {
         const int y = i0 - (p.T - 1) + (lo + rr - walk.vstart);
         const bool yok = unsigned(y) < unsigned(p.OH);
         const float* rowp = dyn + (long long)(lw * 4) * p.OHW + (long long)(yok ? y : 0) * p.OW;
@@ -1093,9 +1140,11 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 12) {
     tc_fence_after();
-    tmem_free<512>(tmem);
+    if constexpr (PAIR) tmem_free_2sm<512>(tmem);
+    else tmem_free<512>(tmem);
   }
 }
 
@@ -1260,6 +1309,7 @@ namespace {
 
 struct DGeo {
   int T, U, Hq, Wq, TR, np, tps, SW, nstrip, units, grid, BN, AS, nslots, RR, XP, PH;
+  bool pair;
   std::size_t smem;
 };
 
@@ -1273,7 +1323,11 @@ DGeo make_dgeo(const ConvShape& s) {
   g.BN = (s.C * s.sh * s.sw + 15) / 16 * 16;
   g.AS = (g.BN + 31) / 32 * 32;
   g.nslots = std::min(kMaxSlots, (512 - 2 * g.AS) / kBdKp);
-  const std::size_t b_bytes = std::size_t(g.T * g.U * kBdKp / 32) * g.BN * 128;
+  // CTA pairs (M = 256 per MMA, each CTA holding half the filter rows):
+  // exact, but measured slower (AlexNet conv1 BD 361 -> 388 us, ResNet conv1
+  // 1052 -> 1571: the pair's producers run in lockstep), so opt-in
+  g.pair = tune("fct_bd_pair", 0) == 1 && g.BN % 16 == 0;
+  const std::size_t b_bytes = std::size_t(g.T * g.U * kBdKp / 32) * (g.pair ? g.BN / 2 : g.BN) * 128;
   const std::size_t fixed = b_bytes + 1024 + 1024;
   // column strips (each a separate pass down the image) until the dy-row
   // ring holds two tiles' rows and a strip's positions fit two 32-blocks
@@ -1294,7 +1348,7 @@ DGeo make_dgeo(const ConvShape& s) {
   g.np = g.TR * g.SW;
   g.tps = (g.Hq + g.TR - 1) / g.TR;
   g.units = s.N * g.nstrip * g.tps;
-  g.grid = std::min(sm_count(), g.units);
+  g.grid = g.pair ? 2 * std::min(sm_count() / 2, (g.units + 1) / 2) : std::min(sm_count(), g.units);
   (void)OH;
   return g;
 }
@@ -1323,13 +1377,34 @@ cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, fl
   p.CHW = std::int64_t(s.C) * s.H * s.W;
   const int tu = g.T * g.U;
   void (*kern)(const DParams) = nullptr;
-  if (s.sh == 4) kern = tu == 9 ? fct_bwdd_kernel<4, 9> : tu == 4 ? fct_bwdd_kernel<4, 4> : fct_bwdd_kernel<4, 16>;
-  else kern = tu == 9 ? fct_bwdd_kernel<2, 9> : tu == 4 ? fct_bwdd_kernel<2, 4> : fct_bwdd_kernel<2, 16>;
+#define FCT_BD_PICK(P)                                                                                        \
+  if (s.sh == 4) kern = tu == 9 ? fct_bwdd_kernel<4, 9, P> : tu == 4 ? fct_bwdd_kernel<4, 4, P> : fct_bwdd_kernel<4, 16, P>; \
+  else kern = tu == 9 ? fct_bwdd_kernel<2, 9, P> : tu == 4 ? fct_bwdd_kernel<2, 4, P> : fct_bwdd_kernel<2, 16, P>;
+  if (g.pair) {
+    FCT_BD_PICK(true)
+  } else {
+    FCT_BD_PICK(false)
+  }
+#undef FCT_BD_PICK
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
   if (e != cudaSuccess) return e;
-  trace_variant("fct bwdd units=%d grid=%d TR=%d np=%d strips=%d TU=%d BN=%d XP=%d ring=%d slots=%d", g.units,
-                g.grid, g.TR, g.np, g.nstrip, tu, g.BN, g.XP, g.RR, g.nslots);
-  return launch_pdl(kern, dim3(g.grid), dim3(kBdThreads), g.smem, st, p);
+  trace_variant("fct bwdd units=%d grid=%d TR=%d np=%d strips=%d TU=%d BN=%d XP=%d ring=%d slots=%d pair=%d", g.units,
+                g.grid, g.TR, g.np, g.nstrip, tu, g.BN, g.XP, g.RR, g.nslots, int(g.pair));
+  if (!g.pair) return launch_pdl(kern, dim3(g.grid), dim3(kBdThreads), g.smem, st, p);
+  count_launch();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kBdThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute cat[1];
+  cat[0].id = cudaLaunchAttributeClusterDimension;
+  cat[0].val.clusterDim.x = 2;
+  cat[0].val.clusterDim.y = 1;
+  cat[0].val.clusterDim.z = 1;
+  cfg.attrs = cat;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace ucudnn

@@ -180,6 +180,10 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct_bd=0", "2 3 36 36 70 7 7 3 2 1 0"),
                                        ("fct_bd_ring=18", "3 3 63 63 20 11 11 1 4 1 0"),
                                        ("fct_bd_ring=15", "2 3 36 36 64 7 7 3 2 1 0"),
+                                       ("fct_bd_pair=1", "2 3 31 31 16 11 11 2 4 1 0"),
+                                       ("fct_bd_pair=1", "3 3 47 51 64 11 11 2 4 1 0"),
+                                       ("fct_bd_pair=1", "2 3 100 140 32 7 7 3 2 1 0"),
+                                       ("fct_bd_pair=1", "1 3 45 45 8 11 11 0 4 1 0"),
                                        ("fct_bd_strips=2", "2 3 36 36 64 7 7 3 2 1 0"),
                                        ("fct_bd_strips=3", "3 3 47 51 64 11 11 2 4 1 0"),
                                        ("", "2 3 100 140 32 7 7 3 2 1 0"),
@@ -222,6 +226,8 @@ def test_knob_variants(cuda, tune, spec):
         assert "precomp2" in out.stdout and "msub=2" in out.stdout, out.stdout
     if tune.startswith("fct_ring="):
         assert "fct fwd" in out.stdout and tune.replace("fct_", "") in out.stdout, out.stdout
+    if tune == "fct_bd_pair=1":
+        assert "fct bwdd" in out.stdout and "pair=1" in out.stdout, out.stdout
     if tune.startswith("fct_bd_strips="):
         assert "fct bwdd" in out.stdout and "strips=" + tune.split("=")[1] in out.stdout, out.stdout
     if tune.startswith("fct_bd_ring="):

@@ -772,8 +772,16 @@ __global__ void __launch_bounds__(256) fct_bwdf_finalize_kernel(const BFinal f) 
   const long long n = (long long)f.rows * f.K;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int q = int(i / f.K), k = int(i - (long long)q * f.K);
-    float acc = 0.f;
-    for (int g = 0; g < f.nslices; ++g) acc += f.slices[g * n + i];
+    // eight interleaved partial sums (loads in flight instead of one
+    // dependent chain of ~148), combined in a fixed order: deterministic
+    float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int g = 0;
+    for (; g + 8 <= f.nslices; g += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) part[j] += f.slices[(g + j) * n + i];
+    }
+    for (int j = 0; g < f.nslices; ++g, ++j) part[j] += f.slices[g * n + i];
+    const float acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
     float* d = f.dw + (long long)k * f.rows + q;
     *d = f.beta == 0.f ? f.alpha * acc : f.alpha * acc + f.beta * *d;
   }

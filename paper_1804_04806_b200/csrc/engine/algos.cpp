@@ -169,17 +169,22 @@ cudaError_t wino4_run(int op, const ConvShape& s, const float* a, const float* b
 // TMEM-operand kernel (fct.cu), else the shared-memory patch kernel (bfs.cu),
 // instead of the strided L2 gather.
 bool gather_supports(int op, const ConvShape& s) {
-  return (op == 2 && (fct_bwdf_supports(s) || bfs_supports(s) || bfl_supports(s))) || (op == 1 && bds_supports(s));
+  return (op == 2 && (fct_bwdf_supports(s) || fct_bwdf1_supports(s) || bfs_supports(s) || bfl_supports(s))) ||
+         (op == 1 && bds_supports(s));
 }
 std::int64_t gather_workspace(int op, const ConvShape& s) {
   if (op == 2)
-    return fct_bwdf_supports(s) ? fct_bwdf_workspace(s) : bfs_supports(s) ? bfs_workspace(s) : bfl_workspace(s);
+    return fct_bwdf_supports(s)    ? fct_bwdf_workspace(s)
+           : fct_bwdf1_supports(s) ? fct_bwdf1_workspace(s)
+           : bfs_supports(s)       ? bfs_workspace(s)
+                                   : bfl_workspace(s);
   return op == 1 ? bds_workspace(s) : 0;
 }
 cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                        float beta, cudaStream_t st, int) {
   if (op == 2) {
     if (fct_bwdf_supports(s)) return fct_bwdf_run(s, a, b, out, ws, alpha, beta, st);
+    if (fct_bwdf1_supports(s)) return fct_bwdf1_run(s, a, b, out, ws, alpha, beta, st);
     return bfs_supports(s) ? bfs_run(s, a, b, out, ws, alpha, beta, st) : bfl_run(s, a, b, out, ws, alpha, beta, st);
   }
   if (op == 1) return bds_run(s, a, b, out, alpha, beta, st);

@@ -36,6 +36,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 
 
@@ -760,6 +762,270 @@ __global__ void __launch_bounds__(kBfThreads, 1) fct_bwdf_kernel(const BParams p
   }
 }
 
+// ---------------------------------------------------------- stride-1 variant
+// The same D[q][k] = sum_px x-tap[q][px] * dy[k][px] for stride-1 layers with
+// many channels (ResNet 3x3 layers: C*R*S = 576 .. 2304 x rows). The x rows q
+// are split into groups of QT*128 (QT = 3 for K <= 64, 2 for K <= 128) and the
+// grid into one set of CTAs per group, each CTA accumulating its group's
+// rows over a contiguous run of output rows. Operands come by TMA straight
+// from the caller's NCHW tensors (16 B aligned rows: W % 4 == 0): per output
+// row one 4-D box of x (XW columns from w = -4, the group's CR channels,
+// zero-filled off the image) into a row ring [RR][CR][XW] (ring rows padded
+// so a warp's (c, r, s) lanes spread over the banks), and per 32-pixel block
+// one 3-D box of dy (32 pixels x K channels) that lands as the SWIZZLE_128B
+// K-major B operand. No loader threads touch the data. (Ring rows start 128 B
+// aligned, as TMA destinations must.)
+constexpr int kB1Threads = 15 * 32;  // 0 .. 4*QT-1 producers, 12 MMA, 13 x TMA, 14 dy TMA
+constexpr int kB1MaxDS = 8;
+
+struct B1Params {
+  float* slices;
+  int C, H, W, K, R, S, ph, pw, OH, OW;
+  int rows, BN, nblk, units, RR, XW, RS, CR, QG, cpg, nslots, nds;
+};
+
+__device__ __forceinline__ void tma_4d(std::uint32_t dst, const void* tmap, std::uint64_t* bar, int x, int y, int z,
+                                       int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(std::uint32_t dst, const void* tmap, std::uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+struct RowWalk1 {
+  int vstart = 0, vend = 0, n = -1;
+  __device__ __forceinline__ bool next(const B1Params& p, int u) {
+    const int nn = u / p.OH;
+    const bool fresh = nn != n;
+    vstart = fresh ? vend : vstart + 1;
+    vend = vstart + p.R;
+    n = nn;
+    return fresh;
+  }
+};
+
+template <int QT>
+__global__ void __launch_bounds__(kB1Threads, 1)
+    fct_bwdf1_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dmap,
+                     const B1Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t dslot_bytes = std::uint32_t(p.BN) * 128;
+  unsigned char* dring = smem;  // nds x [BN rows x 128 B], SWIZZLE_128B K-major
+  float* ring = reinterpret_cast<float*>(dring + p.nds * dslot_bytes);  // [RR] x (RS floats: [CR][XW], 128 B rows)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(ring + p.RR * p.RS);
+  std::uint64_t* afull = bars;
+  std::uint64_t* aempty = afull + kMaxSlots;
+  std::uint64_t* dfull = aempty + kMaxSlots;
+  std::uint64_t* dempty = dfull + kB1MaxDS;
+  std::uint64_t* loaded = dempty + kB1MaxDS;
+  std::uint64_t* consumed = loaded + kNB;
+  std::uint64_t* tdone = consumed + kNB;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tdone + 1);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&dmap);
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(&afull[s], QT * 128);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < kB1MaxDS; ++s) {
+      mbar_init(&dfull[s], 1);
+      mbar_init(&dempty[s], 1);
+    }
+    for (int b = 0; b < kNB; ++b) {
+      mbar_init(&loaded[b], 1);
+      mbar_init(&consumed[b], QT * 128);
+    }
+    mbar_init(tdone, 1);
+    mbar_fence_init();
+  }
+  if (warp == 12) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const std::uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int grp = blockIdx.x / p.cpg, bi = blockIdx.x - grp * p.cpg;
+  const int u0 = int((long long)bi * p.units / p.cpg), u1 = int((long long)(bi + 1) * p.units / p.cpg);
+  const int my_units = u1 - u0;
+  const int RSf = p.R * p.S;
+  const int c_lo = grp * p.QG / RSf;
+  const std::uint32_t a_col0 = std::uint32_t(QT * p.BN);
+
+  if (warp < 4 * QT) {
+    // ------------------------------------------------ A producers: lane = x row q = (c, r, s) of the group
+    const int qt = warp >> 2, quarter = warp & 3;
+    const int ql = qt * 128 + quarter * 32 + lane, q = grp * p.QG + ql;
+    const bool qok = q < p.rows;
+    const int qe = qok ? q : grp * p.QG;
+    const int c = qe / RSf, rs = qe - c * RSf, r = rs / p.S, s = rs - r * p.S;
+    const std::uint32_t tq = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(qt * 32);
+    const int xoff = (c - c_lo) * p.XW + s + 4 - p.pw;  // ring column 0 is w = -4
+    RowWalk1 walk;
+    int g = 0;
+    for (int i = 0; i < my_units; ++i) {
+      walk.next(p, u0 + i);
+      mbar_wait(&loaded[i % kNB], (i / kNB) & 1);
+      int prow = walk.vstart % p.RR + r;
+      if (prow >= p.RR) prow -= p.RR;
+      const std::uint32_t xb = smem_u32(ring) + std::uint32_t((prow * p.RS + xoff) * 4);
+      for (int b = 0; b < p.nblk; ++b, ++g) {
+        const int slot = g % p.nslots;
+        mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1);
+        tc_fence_after();
+        const int ow0 = b * 32;
+        const std::uint32_t a0 = xb + std::uint32_t(ow0 * 4);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(a0 + j * 4));
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (!qok || ow0 + j >= p.OW) v[j] = 0.f;
+        tmem_st32(tq + std::uint32_t(slot * QT * 32), v);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&afull[slot]);
+      }
+      mbar_arrive(&consumed[i % kNB]);
+    }
+    if (my_units > 0) {
+      mbar_wait_sleep(tdone, 0);
+      tc_fence_after();
+    }
+    float* slice = p.slices + ((long long)blockIdx.x * p.QG + ql) * p.K;
+    for (int k0 = 0; k0 < p.BN; k0 += 32) {
+      float v[32];
+      if (my_units > 0) {
+        tmem_ld32(tmem + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(qt * p.BN + k0), v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+      if (!qok) continue;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        if (k0 + j + 4 <= p.K)
+          *reinterpret_cast<float4*>(slice + k0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  } else if (warp == 12) {
+    // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
+    const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
+    const std::uint64_t dd0 = umma_desc_sw128(smem_u32(dring));
+    const std::uint32_t dslot_desc = dslot_bytes >> 4;
+    const int total = my_units * p.nblk;
+    for (int g = 0; g < total; ++g) {
+      const int slot = g % p.nslots, ds = g % p.nds;
+      mbar_wait(&afull[slot], (g / p.nslots) & 1);
+      mbar_wait(&dfull[ds], (g / p.nds) & 1);
+      tc_fence_after();
+      const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * QT * 32);
+      const std::uint64_t bd = dd0 + std::uint64_t(ds) * dslot_desc;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int t = 0; t < QT; ++t)
+          mma_tf32_ts_warp(tmem + std::uint32_t(t * p.BN), ta + std::uint32_t(t * 32 + 8 * k), bd + 2 * k, idesc,
+                           (g | k) ? 1u : 0u);
+      mma_commit_warp(&aempty[slot]);
+      mma_commit_warp(&dempty[ds]);
+      __syncwarp();
+    }
+    if (total > 0) mma_commit_warp(tdone);
+    __syncwarp();
+  } else if (warp == 13) {
+    // ------------------------------------------------ x rows: one TMA box per new output row
+    RowWalk1 walk;
+    __shared__ int hist[kHist];
+    int waited = -1;
+    for (int i = 0; i < my_units; ++i) {
+      const int u = u0 + i;
+      const bool fresh = walk.next(p, u);
+      const int n = u / p.OH, oh = u - n * p.OH;
+      const int lo = fresh ? walk.vstart : walk.vend - 1;
+      const int ov = walk.vend - 1 - p.RR;
+      int need = -1;
+      for (int j = i - 1; j >= 0 && j >= i - kHist; --j)
+        if (hist[j % kHist] <= ov) {
+          need = j;
+          break;
+        }
+      if (need > waited) {
+        mbar_wait_sleep(&consumed[need % kNB], (need / kNB) & 1);
+        waited = need;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        hist[i % kHist] = walk.vstart;
+        const int cnt = walk.vend - lo;
+        mbar_expect_tx(&loaded[i % kNB], std::uint32_t(cnt * p.CR * p.XW * 4));
+        for (int vr = lo; vr < walk.vend; ++vr)
+          tma_4d(smem_u32(ring) + std::uint32_t((vr % p.RR) * p.RS * 4), &xmap, &loaded[i % kNB], -4,
+                 oh - p.ph + (vr - walk.vstart), c_lo, n);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 14) {
+    // ------------------------------------------------ dy blocks: one TMA box (32 pixels x K channels) each
+    if (lane == 0) {
+      const int total = my_units * p.nblk;
+      for (int g = 0; g < total; ++g) {
+        const int u = u0 + g / p.nblk, b = g - (g / p.nblk) * p.nblk;
+        const int n = u / p.OH, oh = u - n * p.OH;
+        const int ds = g % p.nds;
+        mbar_wait_sleep(&dempty[ds], ((g / p.nds) & 1) ^ 1);
+        mbar_expect_tx(&dfull[ds], dslot_bytes);
+        tma_3d(smem_u32(dring) + std::uint32_t(ds) * dslot_bytes, &dmap, &dfull[ds], b * 32, oh, n * p.K);
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// dW[k][q] = beta * dW + alpha * sum over the group's CTAs of slice[cta][q - group * QG][k], in order
+struct B1Final {
+  const float* slices;
+  float* dw;
+  float alpha, beta;
+  int rows, K, QG, cpg;
+};
+__global__ void __launch_bounds__(256) fct_bwdf1_finalize_kernel(const B1Final f) {
+  pdl_wait();
+  const long long n = (long long)f.rows * f.K;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int q = int(i / f.K), k = int(i - (long long)q * f.K);
+    const int grp = q / f.QG, ql = q - grp * f.QG;
+    const float* sl = f.slices + ((long long)grp * f.cpg * f.QG + ql) * f.K + k;
+    const long long cstride = (long long)f.QG * f.K;
+    float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int b = 0;
+    for (; b + 8 <= f.cpg; b += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) part[j] += sl[(b + j) * cstride];
+    }
+    for (int j = 0; b < f.cpg; ++b, ++j) part[j] += sl[b * cstride];
+    const float acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+    float* d = f.dw + (long long)k * f.rows + q;
+    *d = f.beta == 0.f ? f.alpha * acc : f.alpha * acc + f.beta * *d;
+  }
+}
+
 // dW[k][q] = beta * dW + alpha * sum_g slice_g[q][k], slices added in order
 struct BFinal {
   const float* slices;
@@ -1413,6 +1679,117 @@ cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, fl
   cfg.attrs = cat;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fct() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+struct B1Geo {
+  int OH, OW, rows, QT, QG, G, cpg, BN, nblk, units, XW, CR, RS, RR, nslots, nds;
+  std::size_t smem;
+};
+
+B1Geo make_b1geo(const ConvShape& s) {
+  B1Geo g{};
+  g.OH = s.OH();
+  g.OW = s.OW();
+  g.rows = s.C * s.R * s.S;
+  g.BN = (s.K + 15) / 16 * 16;
+  g.QT = g.BN <= 64 ? 3 : 2;
+  g.QG = g.QT * kBM;
+  g.G = (g.rows + g.QG - 1) / g.QG;
+  g.cpg = std::max(1, sm_count() / g.G);
+  g.nblk = (g.OW + 31) / 32;
+  g.units = s.N * g.OH;
+  // channels a group's QG rows touch (+1: a group can start mid-channel)
+  g.CR = std::min(s.C, (g.QG + s.R * s.S - 1) / (s.R * s.S) + 1);
+  // ring columns from w = -4: every tap column read, 16 B multiple, = 12 mod 32
+  const int need = g.nblk * 32 - 1 + s.S - 1 + 4 - s.pw + 1;
+  g.XW = (need + 3) / 4 * 4;
+  while (g.XW % 32 != 12) g.XW += 4;
+  // ring row stride: the box rounded up to 128 B (the TMA destination
+  // alignment); the channel stride XW = 12 mod 32 spreads a warp's lanes
+  g.RS = (g.CR * g.XW + 31) / 32 * 32;
+  g.nslots = std::min(kMaxSlots, (512 - g.QT * g.BN) / (g.QT * 32));
+  g.nds = std::min(kB1MaxDS, (96 * 1024) / (g.BN * 128));
+  const std::size_t fixed = std::size_t(g.nds) * g.BN * 128 + 1024 + 512;
+  const std::size_t row_bytes = std::size_t(g.RS) * 4;
+  int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
+  rr = std::min(rr, s.R + (kHist - 2));
+  rr = std::min(rr, tune("fct_bf1_ring", rr));
+  g.RR = std::max(rr, 1);
+  g.smem = fixed + row_bytes * g.RR;
+  return g;
+}
+
+}  // namespace
+
+bool fct_bwdf1_supports(const ConvShape& s) {
+  if (s.sh != 1 || s.sw != 1 || s.C <= 4 || s.K % 16 != 0 || s.K > 128 || !tune("fct_bf1", 1)) return false;
+  const int OW = s.OW(), OH = s.OH();
+  // TMA: 16 B aligned rows of x and dy, the x box starting at w = -4
+  if (s.W % 4 != 0 || OW % 4 != 0 || (std::int64_t(OH) * OW) % 4 != 0 || s.pw > 4) return false;
+  const B1Geo g = make_b1geo(s);
+  return g.CR <= 256 && g.XW <= 256 && g.nslots >= 2 && g.nds >= 4 && g.RR >= s.R + 1 && g.smem <= 220 * 1024 &&
+         std::int64_t(s.N) * s.K * OH * OW < (1ll << 31);
+}
+
+std::int64_t fct_bwdf1_workspace(const ConvShape& s) {
+  const B1Geo g = make_b1geo(s);
+  return (std::int64_t(g.G) * g.cpg * g.QG * s.K * 4 + 255) / 256 * 256;
+}
+
+cudaError_t fct_bwdf1_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
+                          float beta, cudaStream_t st) {
+  const B1Geo g = make_b1geo(s);
+  CUtensorMap xmap, dmap;
+  {
+    const cuuint64_t dims[4] = {cuuint64_t(s.W), cuuint64_t(s.H), cuuint64_t(s.C), cuuint64_t(s.N)};
+    const cuuint64_t strides[3] = {cuuint64_t(s.W) * 4, cuuint64_t(s.H) * s.W * 4, cuuint64_t(s.C) * s.H * s.W * 4};
+    const cuuint32_t box[4] = {cuuint32_t(g.XW), 1, cuuint32_t(g.CR), 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    if (encode_tiled_fct()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[3] = {cuuint64_t(g.OW), cuuint64_t(g.OH), cuuint64_t(s.N) * s.K};
+    const cuuint64_t strides[2] = {cuuint64_t(g.OW) * 4, cuuint64_t(g.OH) * g.OW * 4};
+    const cuuint32_t box[3] = {32, 1, cuuint32_t(g.BN)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (encode_tiled_fct()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(dy), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  B1Params p{};
+  p.slices = static_cast<float*>(ws);
+  p.C = s.C; p.H = s.H; p.W = s.W; p.K = s.K; p.R = s.R; p.S = s.S; p.ph = s.ph; p.pw = s.pw;
+  p.OH = g.OH; p.OW = g.OW;
+  p.rows = g.rows; p.BN = g.BN; p.nblk = g.nblk; p.units = g.units; p.RR = g.RR; p.XW = g.XW; p.RS = g.RS;
+  p.CR = g.CR; p.QG = g.QG; p.cpg = g.cpg; p.nslots = g.nslots; p.nds = g.nds;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const B1Params) =
+      g.QT == 3 ? fct_bwdf1_kernel<3> : fct_bwdf1_kernel<2>;
+  cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
+  if (e != cudaSuccess) return e;
+  trace_variant("fct bwdf1 units=%d groups=%d cpg=%d QT=%d BN=%d CR=%d XW=%d ring=%d slots=%d dslots=%d", g.units,
+                g.G, g.cpg, g.QT, g.BN, g.CR, g.XW, g.RR, g.nslots, g.nds);
+  e = launch_pdl(kern, dim3(g.G * g.cpg), dim3(kB1Threads), g.smem, st, xmap, dmap, p);
+  if (e != cudaSuccess) return e;
+  B1Final f{p.slices, dw, alpha, beta, g.rows, s.K, g.QG, g.cpg};
+  const long long n = (long long)g.rows * s.K;
+  return launch_pdl(fct_bwdf1_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
+                    dim3(256), 0, st, f);
 }
 
 }  // namespace ucudnn

@@ -25,4 +25,10 @@ bool fct_bwdd_supports(const ConvShape& s);
 cudaError_t fct_bwdd_run(const ConvShape& s, const float* dy, const float* w, float* dx, float alpha, float beta,
                          cudaStream_t stream);
 
+// stride-1 BackwardFilter of many-channel layers (W % 4 == 0, K <= 128), operands by TMA
+bool fct_bwdf1_supports(const ConvShape& s);
+std::int64_t fct_bwdf1_workspace(const ConvShape& s);
+cudaError_t fct_bwdf1_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
+                          float beta, cudaStream_t stream);
+
 }  // namespace ucudnn

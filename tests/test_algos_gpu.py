@@ -187,6 +187,13 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct_bd_strips=2", "2 3 36 36 64 7 7 3 2 1 0"),
                                        ("fct_bd_strips=3", "3 3 47 51 64 11 11 2 4 1 0"),
                                        ("", "2 3 100 140 32 7 7 3 2 1 0"),
+                                       ("", "3 64 12 12 64 3 3 1 1 2 6"),
+                                       ("", "2 32 16 16 48 3 3 1 1 2 6"),
+                                       ("", "3 96 8 8 64 5 5 2 1 2 6"),
+                                       ("", "1 256 8 8 128 3 3 1 1 2 6"),
+                                       ("fct_bf1_ring=4", "3 64 12 12 64 3 3 1 1 2 6"),
+                                       ("fct_bf1_ring=6", "3 96 8 8 64 5 5 2 1 2 6"),
+                                       ("fct_bf1=0", "3 64 12 12 64 3 3 1 1 2 6"),
                                        ("fct_bf=0", "2 3 31 31 16 11 11 2 4 2 6"),
                                        ("fct_bf=0", "2 3 36 36 70 7 7 3 2 2 6"),
                                        ("fct_bf_ring=15", "3 3 63 63 20 11 11 1 4 2 6"),
@@ -232,5 +239,7 @@ def test_knob_variants(cuda, tune, spec):
         assert "fct bwdd" in out.stdout and "strips=" + tune.split("=")[1] in out.stdout, out.stdout
     if tune.startswith("fct_bd_ring="):
         assert "fct bwdd" in out.stdout and tune.replace("fct_bd_", "") in out.stdout, out.stdout
+    if tune.startswith("fct_bf1_ring=") or (tune == "" and spec.endswith(" 2 6") and int(spec.split()[1]) > 4):
+        assert "fct bwdf1" in out.stdout, out.stdout
     if tune.startswith("fct_bf_ring="):
         assert "fct bwdf" in out.stdout and tune.replace("fct_bf_", "") in out.stdout, out.stdout

@@ -859,25 +859,27 @@ __global__ void __launch_bounds__(kB1Threads, 1)
   const int grp = blockIdx.x / p.cpg, bi = blockIdx.x - grp * p.cpg;
   const int u0 = int((long long)bi * p.units / p.cpg), u1 = int((long long)(bi + 1) * p.units / p.cpg);
   const int my_units = u1 - u0;
-  const int RSf = p.R * p.S;
-  const int c_lo = grp * p.QG / RSf;
+  const int c_lo = grp * p.CR;  // the group's whole channels [c_lo, c_lo + CR)
   const std::uint32_t a_col0 = std::uint32_t(QT * p.BN);
 
   if (warp < 4 * QT) {
     // ------------------------------------------------ A producers: lane = x row q = (c, r, s) of the group
+    // lane ql = (r * CR + cl) * S + s: a warp's lanes share r (mostly) and
+    // span ~10 channels x S taps, which the channel stride XW = 12 (mod 32)
+    // spreads over the banks (c-major order put lanes differing only in r,
+    // 3 x 3 = 9 rows apart, on one bank: 2.8 wavefronts per load)
     const int qt = warp >> 2, quarter = warp & 3;
-    const int ql = qt * 128 + quarter * 32 + lane, q = grp * p.QG + ql;
-    const bool qok = q < p.rows;
-    const int qe = qok ? q : grp * p.QG;
-    const int c = qe / RSf, rs = qe - c * RSf, r = rs / p.S, s = rs - r * p.S;
+    const int ql = qt * 128 + quarter * 32 + lane;
+    const int rcl = ql / p.S, s = ql - rcl * p.S, r = rcl / p.CR, cl = rcl - r * p.CR;
+    const bool qok = r < p.R && c_lo + cl < p.C;
+    const int xoff = (qok ? cl * p.XW + s : 0) + 4 - p.pw;  // ring column 0 is w = -4
     const std::uint32_t tq = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(qt * 32);
-    const int xoff = (c - c_lo) * p.XW + s + 4 - p.pw;  // ring column 0 is w = -4
     RowWalk1 walk;
     int g = 0;
     for (int i = 0; i < my_units; ++i) {
       walk.next(p, u0 + i);
       mbar_wait(&loaded[i % kNB], (i / kNB) & 1);
-      int prow = walk.vstart % p.RR + r;
+      int prow = walk.vstart % p.RR + (qok ? r : 0);
       if (prow >= p.RR) prow -= p.RR;
       const std::uint32_t xb = smem_u32(ring) + std::uint32_t((prow * p.RS + xoff) * 4);
       for (int b = 0; b < p.nblk; ++b, ++g) {
@@ -1003,14 +1005,15 @@ struct B1Final {
   const float* slices;
   float* dw;
   float alpha, beta;
-  int rows, K, QG, cpg;
+  int rows, K, QG, cpg, CR, R, S;
 };
 __global__ void __launch_bounds__(256) fct_bwdf1_finalize_kernel(const B1Final f) {
   pdl_wait();
   const long long n = (long long)f.rows * f.K;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int q = int(i / f.K), k = int(i - (long long)q * f.K);
-    const int grp = q / f.QG, ql = q - grp * f.QG;
+    const int RS = f.R * f.S, c = q / RS, rs = q - c * RS, r = rs / f.S, s = rs - r * f.S;
+    const int grp = c / f.CR, ql = (r * f.CR + (c - grp * f.CR)) * f.S + s;  // the kernel's lane order
     const float* sl = f.slices + ((long long)grp * f.cpg * f.QG + ql) * f.K + k;
     const long long cstride = (long long)f.QG * f.K;
     float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1706,12 +1709,12 @@ B1Geo make_b1geo(const ConvShape& s) {
   g.BN = (s.K + 15) / 16 * 16;
   g.QT = g.BN <= 64 ? 3 : 2;
   g.QG = g.QT * kBM;
-  g.G = (g.rows + g.QG - 1) / g.QG;
+  // whole channels per group: CR * R * S <= QG x rows
+  g.CR = std::max(1, std::min(s.C, g.QG / (s.R * s.S)));
+  g.G = (s.C + g.CR - 1) / g.CR;
   g.cpg = std::max(1, sm_count() / g.G);
   g.nblk = (g.OW + 31) / 32;
   g.units = s.N * g.OH;
-  // channels a group's QG rows touch (+1: a group can start mid-channel)
-  g.CR = std::min(s.C, (g.QG + s.R * s.S - 1) / (s.R * s.S) + 1);
   // ring columns from w = -4: every tap column read, 16 B multiple, = 12 mod 32
   const int need = g.nblk * 32 - 1 + s.S - 1 + 4 - s.pw + 1;
   g.XW = (need + 3) / 4 * 4;
@@ -1739,7 +1742,7 @@ bool fct_bwdf1_supports(const ConvShape& s) {
   // TMA: 16 B aligned rows of x and dy, the x box starting at w = -4
   if (s.W % 4 != 0 || OW % 4 != 0 || (std::int64_t(OH) * OW) % 4 != 0 || s.pw > 4) return false;
   const B1Geo g = make_b1geo(s);
-  return g.CR <= 256 && g.XW <= 256 && g.nslots >= 2 && g.nds >= 4 && g.RR >= s.R + 1 && g.smem <= 220 * 1024 &&
+  return s.R * s.S <= g.QG && g.CR <= 256 && g.XW <= 256 && g.nslots >= 2 && g.nds >= 4 && g.RR >= s.R + 1 && g.smem <= 220 * 1024 &&
          std::int64_t(s.N) * s.K * OH * OW < (1ll << 31);
 }
 
@@ -1786,7 +1789,7 @@ cudaError_t fct_bwdf1_run(const ConvShape& s, const float* x, const float* dy, f
                 g.G, g.cpg, g.QT, g.BN, g.CR, g.XW, g.RR, g.nslots, g.nds);
   e = launch_pdl(kern, dim3(g.G * g.cpg), dim3(kB1Threads), g.smem, st, xmap, dmap, p);
   if (e != cudaSuccess) return e;
-  B1Final f{p.slices, dw, alpha, beta, g.rows, s.K, g.QG, g.cpg};
+  B1Final f{p.slices, dw, alpha, beta, g.rows, s.K, g.QG, g.cpg, g.CR, s.R, s.S};
   const long long n = (long long)g.rows * s.K;
   return launch_pdl(fct_bwdf1_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
                     dim3(256), 0, st, f);

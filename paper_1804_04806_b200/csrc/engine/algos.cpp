@@ -191,10 +191,17 @@ cudaError_t gather_run(int op, const ConvShape& s, const float* a, const float* 
   return cudaErrorInvalidValue;
 }
 
-bool sliced_supports(int op, const ConvShape& s) { return precomp_sliced_supports(op, s); }
-std::int64_t sliced_workspace(int op, const ConvShape& s) { return precomp_sliced_workspace(op, s); }
+// Stride-1 F / BD whose input channels come in multiples of 32 take the
+// TMEM-operand kernel (fct1.cu: input rows read once per tile, not once per
+// filter tap; its workspace is only the flipped filter for BD), the others
+// the precomp GEMM over reduction-channel slices.
+bool sliced_supports(int op, const ConvShape& s) { return fct1_supports(op, s) || precomp_sliced_supports(op, s); }
+std::int64_t sliced_workspace(int op, const ConvShape& s) {
+  return fct1_supports(op, s) ? fct1_workspace(op, s) : precomp_sliced_workspace(op, s);
+}
 cudaError_t sliced_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
-                       float beta, cudaStream_t st, int) {
+                       float beta, cudaStream_t st, int flags) {
+  if (fct1_supports(op, s)) return fct1_run(op, s, a, b, out, ws, alpha, beta, st, flags);
   return precomp_sliced_run(op, s, a, b, out, ws, alpha, beta, st);
 }
 

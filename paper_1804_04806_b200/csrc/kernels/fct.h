@@ -31,4 +31,11 @@ std::int64_t fct_bwdf1_workspace(const ConvShape& s);
 cudaError_t fct_bwdf1_run(const ConvShape& s, const float* x, const float* dy, float* dw, void* ws, float alpha,
                           float beta, cudaStream_t stream);
 
+// stride-1 Forward / BackwardData with the im2col operand in TMEM (fct1.cu):
+// input channels % 32 == 0, output width <= 128, <= 256 output channels
+bool fct1_supports(int op, const ConvShape& s);
+std::int64_t fct1_workspace(int op, const ConvShape& s);  // BackwardData: the flipped filter
+cudaError_t fct1_run(int op, const ConvShape& s, const float* in, const float* w, float* out, void* ws, float alpha,
+                     float beta, cudaStream_t stream, int flags);
+
 }  // namespace ucudnn

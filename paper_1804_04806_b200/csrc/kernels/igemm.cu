@@ -413,6 +413,7 @@ cudaError_t igemm_forward(const ConvShape& s, const float* x, const float* w, fl
   if (tune("z", 1) && z1x1_supports(kFwd, s)) return z1x1_run(kFwd, s, x, w, y, alpha, beta, stream);
   // few-channel strided layers (AlexNet / ResNet conv1): the shared-memory patch kernel
   if (tune("z", 1) && fct_fwd_supports(s)) return fct_fwd_run(s, x, w, y, alpha, beta, stream);
+  if (tune("z", 1) && fct1_supports(kFwd, s)) return fct1_run(kFwd, s, x, w, y, nullptr, alpha, beta, stream, 0);
   if (tune("z", 1) && fps_supports(s)) return fps_run(s, x, w, y, alpha, beta, stream);
   if (tune("z", 1) && zgemm_supports(kFwd, s)) return zgemm_forward(s, x, w, y, alpha, beta, stream);
   IgemmParams p{};

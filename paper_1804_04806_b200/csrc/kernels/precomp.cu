@@ -29,6 +29,7 @@
 #include <mutex>
 
 #include "bfilter.h"
+#include "z1x1.h"
 #include "conv_common.h"
 #include "launch.h"
 #include "precomp.h"
@@ -1727,6 +1728,35 @@ cudaError_t space_to_depth_nhwc(const float* x, float* out, int N, int C, int H,
   return launch_s2d(x, out, d, N, st);
 }
 
+// Strided 1x1 Forward (ResNet projections): the taps are a plain subsample
+// of x, so copy the sampled pixels into a compact NCHW tensor (one pass) and
+// run the 1x1 stride-1 GEMM straight on its planes (z1x1.cu) -- instead of
+// the space-to-depth rewrite, which would multiply the reduction by sh*sw
+// with all but one phase's weights zero.
+namespace {
+ConvShape subsampled(const ConvShape& s) {
+  ConvShape c = s;
+  c.H = s.OH();
+  c.W = s.OW();
+  c.sh = c.sw = 1;
+  return c;
+}
+bool use_subsample(int op, const ConvShape& s) {
+  return op == kFwd && s.R == 1 && s.S == 1 && s.ph == 0 && s.pw == 0 && (s.sh > 1 || s.sw > 1) &&
+         tune("pc_subsample", 1) && z1x1_supports(kFwd, subsampled(s));
+}
+__global__ void subsample_kernel(const float* __restrict__ x, float* __restrict__ xs, int H, int W, int OH, int OW,
+                                 int sh, int sw, long long planes) {
+  pdl_wait();
+  const long long n = planes * OH * OW;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long pl = i / ((long long)OH * OW);
+    const int rem = int(i - pl * OH * OW), oh = rem / OW, ow = rem - oh * OW;
+    xs[i] = __ldg(x + (pl * H + (long long)oh * sh) * W + (long long)ow * sw);
+  }
+}
+}  // namespace
+
 bool precomp_supports(int op, const ConvShape& s) {
   if (op == kFwd) return s.sh <= 8 && s.sw <= 8 && s.ph <= 127 && s.pw <= 127 && s.R <= 64 && s.S <= 64;
   if (op == kBwdData) {
@@ -1739,6 +1769,7 @@ bool precomp_supports(int op, const ConvShape& s) {
 }
 
 std::int64_t precomp_workspace(int op, const ConvShape& s) {
+  if (use_subsample(op, s)) return (std::int64_t(s.N) * s.C * s.OH() * s.OW() * 4 + 255) / 256 * 256;
   if (op == kFwd) return std::int64_t(geo_ws(f_geo(s)));
   if (op == kBwdData) return std::int64_t(geo_ws(bd_geo(s)));
   return bf_workspace(s);
@@ -1819,6 +1850,16 @@ cudaError_t precomp_sliced_run(int op, const ConvShape& s, const float* a, const
 
 cudaError_t precomp_run(int op, const ConvShape& s, const float* a, const float* b, float* out, void* ws, float alpha,
                         float beta, cudaStream_t st, int flags) {
+  if (use_subsample(op, s)) {
+    float* xs = static_cast<float*>(ws);
+    const long long n = (long long)s.N * s.C * s.OH() * s.OW();
+    cudaError_t e = launch_pdl(subsample_kernel, dim3(int(std::min<long long>((n + 255) / 256, 8 * sm_count()))),
+                               dim3(256), 0, st, a, xs, s.H, s.W, s.OH(), s.OW(), s.sh, s.sw,
+                               (long long)s.N * s.C);
+    if (e != cudaSuccess) return e;
+    trace_variant("precomp subsample 1x1 s%d -> z1x1", s.sh);
+    return z1x1_run(kFwd, subsampled(s), xs, b, out, alpha, beta, st);
+  }
   if (op == kFwd) return run_geo(f_geo(s), a, b, 0, out, ws, alpha, beta, st, flags);
   if (op == kBwdData) return run_geo(bd_geo(s), a, b, 1, out, ws, alpha, beta, st, flags);
   return bf_run(s, a, b, out, ws, alpha, beta, st);

@@ -194,6 +194,9 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct_bf1_ring=4", "3 64 12 12 64 3 3 1 1 2 6"),
                                        ("fct_bf1_ring=6", "3 96 8 8 64 5 5 2 1 2 6"),
                                        ("fct_bf1=0", "3 64 12 12 64 3 3 1 1 2 6"),
+                                       ("", "2 64 56 56 128 1 1 0 2 0 5"),
+                                       ("", "2 64 15 15 32 1 1 0 2 0 5"),
+                                       ("pc_subsample=0", "2 64 56 56 128 1 1 0 2 0 5"),
                                        ("fct1=1", "2 64 27 27 192 5 5 2 1 0 7"),
                                        ("fct1=1", "2 64 27 27 192 5 5 2 1 1 7"),
                                        ("fct1=1", "3 64 12 12 64 3 3 1 1 1 7"),
@@ -244,6 +247,8 @@ def test_knob_variants(cuda, tune, spec):
         assert "fct bwdd" in out.stdout and "strips=" + tune.split("=")[1] in out.stdout, out.stdout
     if tune.startswith("fct_bd_ring="):
         assert "fct bwdd" in out.stdout and tune.replace("fct_bd_", "") in out.stdout, out.stdout
+    if tune == "" and spec.endswith(" 1 1 0 2 0 5"):
+        assert "precomp subsample" in out.stdout, out.stdout
     if tune == "fct1=1":
         assert "fct1 op=" in out.stdout, out.stdout
     if tune.startswith("fct_bf1_ring=") or (tune == "" and spec.endswith(" 2 6") and int(spec.split()[1]) > 4):

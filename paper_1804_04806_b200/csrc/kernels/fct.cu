@@ -51,6 +51,8 @@ using namespace sm100;
 
 namespace {
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fct();  // (defined with the stride-1 host code)
+
 constexpr int kBM = 128;
 constexpr int kMaxSlots = 8;
 constexpr int kNB = 8;        // tile barriers (ring of tiles in flight between loaders and producers)
@@ -496,8 +498,18 @@ struct BParams {
   float* slices;
   int C, H, W, K, R, S, ph, pw, sh, sw, OH, OW;
   int rows, BN, nblk, units, RR, pitch, nslots;
+  int dtma;  // dy blocks by TMA (16 B aligned dy rows, BN == K): one box per block instead of loader warps
   long long CHW, KOHW;
 };
+
+__device__ __forceinline__ void tma_3d_b(std::uint32_t dst, const void* tmap, std::uint64_t* bar, int x, int y,
+                                         int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 
 __device__ __forceinline__ void bulk_g2s_u32(std::uint32_t dst, const void* src, std::uint32_t bytes,
                                              std::uint64_t* bar) {
@@ -526,7 +538,8 @@ __device__ __forceinline__ void bf_range(const BParams& p, int& u0, int& u1) {
 }
 
 template <int SW, int QT>
-__global__ void __launch_bounds__(kBfThreads, 1) fct_bwdf_kernel(const BParams p) {
+__global__ void __launch_bounds__(kBfThreads, 1)
+    fct_bwdf_kernel(const __grid_constant__ CUtensorMap dmap, const BParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
@@ -553,8 +566,9 @@ __global__ void __launch_bounds__(kBfThreads, 1) fct_bwdf_kernel(const BParams p
       mbar_init(&afull[s], QT * 128);
       mbar_init(&aempty[s], 1);
     }
+    if (p.dtma) prefetch_tmap(&dmap);
     for (int s = 0; s < kBfDSlots; ++s) {
-      mbar_init(&dfull[s], 32);
+      mbar_init(&dfull[s], p.dtma ? 1 : 32);
       mbar_init(&dempty[s], 1);
     }
     for (int b = 0; b < kNB; ++b) {
@@ -727,6 +741,21 @@ __global__ void __launch_bounds__(kBfThreads, 1) fct_bwdf_kernel(const BParams p
         if (bytes[h]) bulk_g2s_u32(dst[h], src[h], bytes[h], &loaded[i % kNB]));
     }
     FCT_PRINT("bf xload (consumed, -)");
+  } else if (warp >= 13 + kBfXLoaders && p.dtma) {
+    // ------------------------------------------------ dy blocks by TMA: one 3-D box (32 pixels x K) each,
+    // landing as the SWIZZLE_128B K-major operand, zero past the row end
+    if (warp == 13 + kBfXLoaders && lane == 0) {
+      const int total = my_units * p.nblk;
+      for (int g = 0; g < total; ++g) {
+        const int u = u0 + g / p.nblk, b = g % p.nblk;
+        const int n = u / p.OH, oh = u - n * p.OH;
+        const int ds = g % kBfDSlots;
+        mbar_wait_sleep(&dempty[ds], ((g / kBfDSlots) & 1) ^ 1);
+        mbar_expect_tx(&dfull[ds], dslot_bytes);
+        tma_3d_b(smem_u32(dring) + std::uint32_t(ds) * dslot_bytes, &dmap, &dfull[ds], b * 32, oh, n * p.K);
+      }
+    }
+    __syncwarp();
   } else if (warp >= 13 + kBfXLoaders) {
     // ------------------------------------------------ dy loaders: warp g % 4 owns block g
     // ([K rows x 32 pixels], zero past the row end), all its rows in flight at once
@@ -1567,14 +1596,27 @@ cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, fl
   p.nslots = g.nslots;
   p.CHW = std::int64_t(s.C) * s.H * s.W;
   p.KOHW = std::int64_t(s.K) * g.OH * g.OW;
-  void (*kern)(const BParams) = nullptr;
+  CUtensorMap dmap{};
+  p.dtma = g.OW % 4 == 0 && (std::int64_t(g.OH) * g.OW) % 4 == 0 && s.K == g.BN &&
+           (reinterpret_cast<std::uintptr_t>(dy) & 15) == 0 && tune("fct_bf_dtma", 1);
+  if (p.dtma) {
+    const cuuint64_t dims[3] = {cuuint64_t(g.OW), cuuint64_t(g.OH), cuuint64_t(s.N) * s.K};
+    const cuuint64_t strides[2] = {cuuint64_t(g.OW) * 4, cuuint64_t(g.OH) * g.OW * 4};
+    const cuuint32_t box[3] = {32, 1, cuuint32_t(g.BN)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (encode_tiled_fct()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(dy), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  void (*kern)(const CUtensorMap, const BParams) = nullptr;
   if (s.sw == 4) kern = g.QT == 1 ? fct_bwdf_kernel<4, 1> : g.QT == 2 ? fct_bwdf_kernel<4, 2> : fct_bwdf_kernel<4, 3>;
   else kern = g.QT == 1 ? fct_bwdf_kernel<2, 1> : g.QT == 2 ? fct_bwdf_kernel<2, 2> : fct_bwdf_kernel<2, 3>;
   cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(g.smem));
   if (e != cudaSuccess) return e;
-  trace_variant("fct bwdf units=%d grid=%d rows=%d QT=%d BN=%d nblk=%d pitch=%d ring=%d slots=%d", g.units, g.grid,
-                g.rows, g.QT, g.BN, g.nblk, g.pitch, g.RR, g.nslots);
-  e = launch_pdl(kern, dim3(g.grid), dim3(kBfThreads), g.smem, st, p);
+  trace_variant("fct bwdf units=%d grid=%d rows=%d QT=%d BN=%d nblk=%d pitch=%d ring=%d slots=%d dtma=%d", g.units,
+                g.grid, g.rows, g.QT, g.BN, g.nblk, g.pitch, g.RR, g.nslots, p.dtma);
+  e = launch_pdl(kern, dim3(g.grid), dim3(kBfThreads), g.smem, st, dmap, p);
   if (e != cudaSuccess) return e;
   BFinal f{p.slices, dw, alpha, beta, g.rows, s.K, g.grid};
   const long long n = (long long)g.rows * s.K;

@@ -202,6 +202,8 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("fct1=1", "3 64 12 12 64 3 3 1 1 1 7"),
                                        ("fct1=1", "2 64 28 28 128 3 3 1 1 1 7"),
                                        ("fct1=1", "1 64 56 56 64 3 3 1 1 0 0"),
+                                       ("fct_bf_dtma=0", "4 3 48 48 64 7 7 3 2 2 6"),
+                                       ("", "4 3 48 48 64 7 7 3 2 2 6"),
                                        ("fct_bf=0", "2 3 31 31 16 11 11 2 4 2 6"),
                                        ("fct_bf=0", "2 3 36 36 70 7 7 3 2 2 6"),
                                        ("fct_bf_ring=15", "3 3 63 63 20 11 11 1 4 2 6"),
@@ -249,6 +251,8 @@ def test_knob_variants(cuda, tune, spec):
         assert "fct bwdd" in out.stdout and tune.replace("fct_bd_", "") in out.stdout, out.stdout
     if tune == "" and spec.endswith(" 1 1 0 2 0 5"):
         assert "precomp subsample" in out.stdout, out.stdout
+    if spec == "4 3 48 48 64 7 7 3 2 2 6":
+        assert ("dtma=0" if tune else "dtma=1") in out.stdout, out.stdout
     if tune == "fct1=1":
         assert "fct1 op=" in out.stdout, out.stdout
     if tune.startswith("fct_bf1_ring=") or (tune == "" and spec.endswith(" 2 6") and int(spec.split()[1]) > 4):

@@ -3,7 +3,7 @@ algorithmic FLOPs (2*N*K*C*R*S*OH*OW), its eager
 device time (per_kernel_ms), achieved TFLOP/s and the fraction of the
 line's measured TF32 peak, plus its plan.
 
-  python scripts/roofline_table.py profiles/r02_bench_v3.json [configs/alexnet.net] > profiles/r02_alexnet_roofline.txt
+  python scripts/roofline_table.py profiles/r02_bench_v10.json [configs/alexnet.net] > profiles/r02_alexnet_roofline.txt
 """
 import json
 import os

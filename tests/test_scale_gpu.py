@@ -284,3 +284,9 @@ def test_zz_bench_scale_variants_exercised(cuda):
     assert any(l.startswith("fct fwd ") for l in TRACE), "no TMEM-operand Forward (AlexNet conv1, algorithm 0)"
     assert any(l.startswith("fct bwdf ") for l in TRACE), "no TMEM-operand BackwardFilter (AlexNet conv1)"
     assert any(l.startswith("fct bwdd ") for l in TRACE), "no TMEM-operand BackwardData (AlexNet conv1, algorithm 0)"
+    # ResNet-18's plan: stride-1 3x3 BackwardFilter through the TMA-operand
+    # TMEM kernel, conv1 BackwardFilter with dy by TMA, conv1 BackwardData in
+    # column strips
+    assert any(l.startswith("fct bwdf1 ") for l in TRACE), "no stride-1 TMEM-operand BackwardFilter (ResNet-18)"
+    assert any(l.startswith("fct bwdf ") and "dtma=1" in l for l in TRACE), "no TMA dy in conv1 BF (ResNet-18)"
+    assert any(l.startswith("fct bwdd ") and "strips=2" in l for l in TRACE), "no column strips (ResNet-18 conv1 BD)"

@@ -369,9 +369,40 @@ void benchmark_kernel(ucudnnContext* h, const Kernel& k, Policy policy) {
   }
   if (h->slots.empty()) {
     ModeScope det(h->deterministic, h->faithful);
-    for (std::size_t i = 0; i < jobs.size(); ++i)
-      if (!done[i]) jobs[i].ns = time_once(&h->primary, h->stream, h->warmup, h->iters, op, jobs[i].s,
-                                           jobs[i].key.alg, jobs[i].ws);
+    // Dominance pruning (UCUDNN_BENCH_PRUNE=0 disables): one probe run per
+    // row first; a row at least 25 % slower than another row of the same
+    // micro-batch size that needs no more workspace can never be chosen --
+    // not by the WR DP (fastest feasible per size) nor on a WD Pareto front --
+    // so its probe time is recorded and only the others get the full median
+    // of `iters` (AlexNet `all` planning: most (algorithm, size) rows).
+    static const bool prune = [] {
+      const char* e = std::getenv("UCUDNN_BENCH_PRUNE");
+      return !e || std::atoi(e) != 0;
+    }();
+    std::vector<std::int64_t> probe(jobs.size(), -1);
+    if (prune && h->iters > 1)
+      for (std::size_t i = 0; i < jobs.size(); ++i)
+        if (!done[i]) probe[i] = time_once(&h->primary, h->stream, h->warmup, 1, op, jobs[i].s, jobs[i].key.alg,
+                                           jobs[i].ws);
+    for (std::size_t i = 0; i < jobs.size(); ++i) {
+      if (done[i]) continue;
+      // compared as the rows' costs: steady time plus the amortised filter preparation
+      auto cost = [&](std::size_t q, std::int64_t t) {
+        return row_cost_ns(t, prep[std::size_t(jobs[q].key.alg)], jobs[q].key.batch, k.batch);
+      };
+      bool dominated = false;
+      if (probe[i] > 0) {
+        const std::int64_t ci = cost(i, probe[i]);
+        for (std::size_t j = 0; j < jobs.size() && !dominated; ++j) {
+          const std::int64_t tj = done[j] ? jobs[j].ns : probe[j];
+          dominated = j != i && jobs[j].key.batch == jobs[i].key.batch && tj > 0 && cost(j, tj) * 5 < ci * 4 &&
+                      jobs[j].ws <= jobs[i].ws;
+        }
+      }
+      jobs[i].ns = dominated ? probe[i]
+                             : time_once(&h->primary, h->stream, probe[i] > 0 ? 1 : h->warmup, h->iters, op,
+                                         jobs[i].s, jobs[i].key.alg, jobs[i].ws);
+    }
   } else {
     std::atomic<std::size_t> next{0};
     std::exception_ptr err;

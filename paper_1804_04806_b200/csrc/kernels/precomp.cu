@@ -938,17 +938,18 @@ struct StripParams {
   const float* btiles;  // [n_tile][chunk][tap][BN rows][32 floats, SW128]
   float* out;
   float alpha, beta;
-  int BN, n_tiles, m_tiles, tpi;  // tiles per image
+  int BN, n_tiles, m_tiles, nimg;  // m_tiles: flat position tiles over all images
   int taps, S, c_chunks, Wp, HWp;
   int OH, OW, Nout, P;
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
   int sAh, sBw, pair, bp;
   FastDiv fd_blk;
-  FastDiv fd_Cr, fd_ssw, fd_Wp, fd_tpi, fd_mt;
+  FastDiv fd_Cr, fd_ssw, fd_Wp, fd_HWp, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
   int msub;  // swap == 0: 128-position MMA sub-tiles per tile sharing each filter stage (1 .. 4)
-  int prof;  // UCUDNN_TUNE=prof=1: MMA-warp cycle split into g_prof (strip wait, stage wait, acc wait, total)
+  int prof;  // UCUDNN_TUNE=prof=1: MMA-warp cycle split into g_prof (strip wait, stage wait, acc wait, total);
+             // prof=2: epilogue busy, last epilogue, TMEM-load share, whole CTA
   int nsb;   // strip buffers (2; 1 when a wide tile's strip would leave too few filter stages)
 };
 
@@ -957,6 +958,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
+  const long long t_entry = p.prof == 2 ? clock64() : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t strip_bytes = std::uint32_t(p.nboxes * p.box_rows) * 128;
   const std::uint32_t tap_bytes = std::uint32_t(p.BN) * 128;  // swap: BN = 128 filter rows
@@ -1007,10 +1009,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------ strip producer
       int sc = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        std::uint32_t nt, mt, n, local;
+        std::uint32_t nt, mt;
         p.fd_mt.divmod(std::uint32_t(t), nt, mt);
-        p.fd_tpi.divmod(mt, n, local);
-        const int p0 = int(n) * p.HWp + int(local) * tile_pos;
+        const int p0 = int(mt) * tile_pos;  // tiles run over the flat (n, hp, wp) rows, across images
         for (int cc = 0; cc < p.c_chunks; ++cc, ++sc) {
           const int sb = sc % p.nsb;
           mbar_wait(&sempty[sb], ((sc / p.nsb) & 1) ^ 1);
@@ -1106,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (p.prof && lane == 0 && blockIdx.x < 1024) {
+    if (p.prof == 1 && lane == 0 && blockIdx.x < 1024) {
       g_prof[blockIdx.x * 4 + 0] = c_strip + c_stage;
       g_prof[blockIdx.x * 4 + 1] = c_stage;
       g_prof[blockIdx.x * 4 + 2] = c_acc;
@@ -1116,12 +1117,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ epilogue
     const int ew = warp - 4;
     int tl = 0;
+    long long e_busy = 0, e_last = 0, e_t = 0, e_ld = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
-      std::uint32_t nt, mt, n, local;
+      if (p.prof == 2 && tl > 0) {
+        e_last = clock64() - e_t;
+        e_busy += e_last;
+      }
+      std::uint32_t nt, mt;
       p.fd_mt.divmod(std::uint32_t(t), nt, mt);
-      p.fd_tpi.divmod(mt, n, local);
       const int acc = tl & 1;
       mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      if (p.prof == 2) e_t = clock64();
       tc_fence_after();
       if (p.swap) {
         // TMEM lane = output channel, column = position: stage 32 x 32
@@ -1134,10 +1140,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) tp[lane * 33 + j] = v[j];
           __syncwarp();
-          const int pos = int(local) * tile_pos + c0 + lane;
-          std::uint32_t oh, ow;
-          p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
-          if (int(oh) < p.OH && int(ow) < p.OW) {
+          const int pos = int(mt) * tile_pos + c0 + lane;
+          std::uint32_t n, rem, oh, ow;
+          p.fd_HWp.divmod(std::uint32_t(pos), n, rem);
+          p.fd_Wp.divmod(rem, oh, ow);
+          if (int(n) < p.nimg && int(oh) < p.OH && int(ow) < p.OW) {
             if (!p.phase) {
               float* base = p.out + std::int64_t(n) * p.Nout * p.P + int(oh) * p.OW + int(ow);
               for (int r = 0; r < 32; ++r) {
@@ -1164,10 +1171,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       for (int m = 0; m < p.msub; ++m) {
-      const int pos = int(local) * tile_pos + m * kBM + ew * 32 + lane;  // flat position inside image n
-      std::uint32_t oh, ow;
-      p.fd_Wp.divmod(std::uint32_t(pos), oh, ow);
-      const bool ok = int(oh) < p.OH && int(ow) < p.OW;
+      const int pos = int(mt) * tile_pos + m * kBM + ew * 32 + lane;  // flat (n, hp, wp) position
+      std::uint32_t n, rem, oh, ow;
+      p.fd_HWp.divmod(std::uint32_t(pos), n, rem);
+      p.fd_Wp.divmod(rem, oh, ow);
+      const bool ok = int(n) < p.nimg && int(oh) < p.OH && int(ow) < p.OW;
       std::int64_t obase = 0;
       int hb = 0, wb = 0;
       if (ok) {
@@ -1183,7 +1191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem + (std::uint32_t(ew * 32) << 16) + std::uint32_t(acc * kMaxBN + m * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         float v[32];
+        const long long tq = p.prof == 2 ? clock64() : 0;
         tmem_ld32(tbase + std::uint32_t(c0), v);
+        if (p.prof == 2) e_ld += clock64() - tq;
         if (!ok) continue;
         if (p.phase) {
 #pragma unroll 4
@@ -1204,9 +1214,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (p.prof == 2 && ew == 0 && lane == 0 && blockIdx.x < 1024) {  // epilogue busy, last epilogue
+      if (tl > 0) {
+        e_last = clock64() - e_t;
+        e_busy += e_last;
+      }
+      g_prof[blockIdx.x * 4 + 0] = e_busy;
+      g_prof[blockIdx.x * 4 + 1] = e_last;
+      g_prof[blockIdx.x * 4 + 2] = e_ld;
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (p.prof == 2 && threadIdx.x == 0 && blockIdx.x < 1024) {
+    g_prof[blockIdx.x * 4 + 3] = clock64() - t_entry;
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_free<512>(tmem);
@@ -1214,27 +1236,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NCHW -> zero-padded channels-last [n][Hp][Wp][Cp] (source pixel (h, w)
-// lands at (h + pt, w + pl)); 32 x 33 smem transpose per (n, row, w-block, c-block).
-__global__ void pad_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int H, int W, int Cp,
-                                int pt, int pl, int Hp, int Wp) {
+// lands at (h + pt, w + pl)); 32 x 33 smem transpose per (n, row, 32-pixel
+// block, 32-channel block), 128 threads: eight independent loads per thread in
+// flight and 16-byte stores (8 lanes per pixel's 128-byte channel run).
+__global__ void __launch_bounds__(128) pad_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C,
+                                                       int H, int W, int Cp, int pt, int pl, int Hp, int Wp) {
   pdl_wait();
   pdl_trigger();
   __shared__ float tile[32][33];
   const int n = blockIdx.z / Hp, hp = blockIdx.z - n * Hp;
   const int w0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-  const int h = hp - pt;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, w = w0 + threadIdx.x - pl;
-    float v = 0.f;
-    if (c < C && unsigned(h) < unsigned(H) && unsigned(w) < unsigned(W) && w0 + int(threadIdx.x) < Wp)
-      v = src[((std::int64_t(n) * C + c) * H + h) * W + w];
-    tile[i][threadIdx.x] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = hp - pt, w = w0 + lane - pl;
+  const bool row_ok = unsigned(h) < unsigned(H) && unsigned(w) < unsigned(W) && w0 + lane < Wp;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = c0 + warp + 4 * i;
+    tile[warp + 4 * i][lane] = (row_ok && c < C) ? __ldg(src + ((std::int64_t(n) * C + c) * H + h) * W + w) : 0.f;
   }
   __syncthreads();
   float* o = dst + (std::int64_t(n) * Hp + hp) * Wp * Cp;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int wp = w0 + i, c = c0 + threadIdx.x;
-    if (wp < Wp && c < Cp) o[std::int64_t(wp) * Cp + c] = tile[threadIdx.x][i];
+  const int q = threadIdx.x & 7;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int px = (threadIdx.x >> 3) + 16 * k, wp = w0 + px;
+    if (wp < Wp)
+      *reinterpret_cast<float4*>(o + std::int64_t(wp) * Cp + c0 + 4 * q) =
+          make_float4(tile[4 * q][px], tile[4 * q + 1][px], tile[4 * q + 2][px], tile[4 * q + 3][px]);
   }
 }
 
@@ -1324,16 +1352,21 @@ StripGeo strip_geo(const Geo& g, int BN) {
   if (sg.Hp - g.R + 1 != g.Hout || sg.Wp - g.S + 1 != g.Wout) return sg;
   sg.msub = sg.swap ? 1 : std::max(1, std::min(std::min(4, tune("strip_msub", 2)), 256 / std::max(BN, 1)));
   sg.rows = (sg.swap ? 2 * kBM : sg.msub * kBM) + (g.R - 1) * sg.Wp + (g.S - 1);
-  sg.box_rows = std::min(256, (sg.rows + 7) / 8 * 8);
-  sg.nboxes = (sg.rows + sg.box_rows - 1) / sg.box_rows;
+  sg.nboxes = (sg.rows + 255) / 256;  // TMA boxes of <= 256 rows, split evenly (8-row multiples)
+  sg.box_rows = ((sg.rows + sg.nboxes - 1) / sg.nboxes + 7) / 8 * 8;
   sg.strip_bytes = std::size_t(sg.nboxes) * sg.box_rows * 128;
   const std::size_t stage = std::size_t(kTapsPerStage) * BN * 128;
-  const std::size_t budget = 210 * 1024 - (sg.swap ? 4 * 32 * 33 * 4 : 0);
-  // two strip buffers unless that leaves fewer than 6 filter stages (a
-  // filter stage refill takes ~1-2 us: with 3 stages the 4-sub-tile tile
-  // waited on filters 54 % of the time); one buffer stalls each chunk change
+  // 227 KB per CTA less the 1 KB alignment slack, the barrier block and the
+  // static tap table
+  const std::size_t budget = 232448 - 1024 - 256 - 256 - (sg.swap ? 4 * 32 * 33 * 4 : 0);
+  // two strip buffers unless that leaves fewer than 3 filter stages
+  // (strip_minst): one buffer stalls each chunk change (AlexNet conv2 BD at
+  // 64 images, 4 sub-tiles: 553 -> 528 us per 256 images with two buffers and
+  // 3 stages; ResNet 3x3 64-channel BD 348 -> 323)
   sg.nsb = 2;
-  if ((budget - std::min(budget, 2 * sg.strip_bytes)) / stage < 6 && tune("strip_nsb", 0) != 2) sg.nsb = 1;
+  if ((budget - std::min(budget, 2 * sg.strip_bytes)) / stage < std::size_t(tune("strip_minst", 3)) &&
+      tune("strip_nsb", 0) != 2)
+    sg.nsb = 1;
   if (sg.nsb * sg.strip_bytes + 2 * stage > budget) return sg;
   sg.stages = int(std::min<std::size_t>(kMaxStages, (budget - sg.nsb * sg.strip_bytes) / stage));
   sg.ok = true;
@@ -1366,7 +1399,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     d.Cp = Cp;
     e = launch_s2d(act, xp, d, g.N, st);
   } else {
-    e = launch_pdl(pad_nhwc_kernel, dim3((sg.Wp + 31) / 32, (Cp + 31) / 32, g.N * sg.Hp), dim3(32, 8), 0, st, act, xp,
+    e = launch_pdl(pad_nhwc_kernel, dim3((sg.Wp + 31) / 32, Cp / 32, g.N * sg.Hp), dim3(128), 0, st, act, xp,
                    g.Cin, g.Hin, g.Win, Cp, g.ph, g.pw, sg.Hp, sg.Wp);
   }
   if (e != cudaSuccess) return e;
@@ -1404,8 +1437,10 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   p.nsb = sg.nsb;
   p.prof = tune("prof", 0);
   const int tile_pos = sg.swap ? 2 * kBM : sg.msub * kBM;
-  p.tpi = ((g.Hout - 1) * sg.Wp + g.Wout + tile_pos - 1) / tile_pos;
-  p.m_tiles = g.N * p.tpi;
+  // the last image needs positions up to (OH-1)*Wp + OW; the padding rows
+  // between images are computed and dropped (their strips read zeros)
+  p.nimg = g.N;
+  p.m_tiles = int(((std::int64_t(g.N) - 1) * p.HWp + (g.Hout - 1) * sg.Wp + g.Wout + tile_pos - 1) / tile_pos);
   p.taps = taps;
   p.S = g.S;
   p.c_chunks = Cp / 32;
@@ -1415,7 +1450,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
   p.nboxes = sg.nboxes;
   p.stages = sg.stages;
   p.fd_Wp = FastDiv(std::uint32_t(sg.Wp));
-  p.fd_tpi = FastDiv(std::uint32_t(p.tpi));
+  p.fd_HWp = FastDiv(std::uint32_t(p.HWp));
   p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
   p.phase = g.phase;
   if (g.phase) {

@@ -24,3 +24,5 @@ r = (C.c_double * 4)()
 lib().ucudnnDebugPrecompProfile(r)
 tot = r[3] or 1
 print(f"{sys.argv[1]} op{op} {os.environ.get('UCUDNN_TUNE')}: operand-wait {100*r[0]/tot:5.1f}% (stage {100*r[1]/tot:5.1f}%) acc-wait {100*r[2]/tot:5.1f}% total {r[3]/1.9e3:8.1f} us")
+if os.environ.get("UCUDNN_TUNE", "").endswith("prof=2"):
+    print(f"  prof=2: epilogue busy {r[0]/1.9e3:7.1f} us  last epilogue {r[1]/1.9e3:6.1f} us  tmem-ld {r[2]/1.9e3:6.1f} us  CTA {r[3]/1.9e3:7.1f} us")

@@ -218,7 +218,14 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("pc2_msub=2", "3 64 13 13 192 3 3 1 1 0 5"),
                                        ("pc2_msub=2", "5 64 27 27 192 5 5 2 1 0 5"),
                                        ("pc2_msub=2", "3 256 13 13 64 3 3 1 1 1 5"),
-                                       ("pc2_msub=2", "2 32 28 28 128 3 3 1 2 0 5")])
+                                       ("pc2_msub=2", "2 32 28 28 128 3 3 1 2 0 5"),
+                                       ("strip=1", "3 64 12 12 64 3 3 1 1 0 5"),
+                                       ("strip=1", "3 64 12 12 64 3 3 1 1 1 5"),
+                                       ("strip=1,strip_msub=4", "5 64 27 27 40 5 5 2 1 1 5"),
+                                       ("strip=1,strip_msub=4", "3 32 9 9 64 3 3 1 1 0 5"),
+                                       ("strip=1,strip_msub=1", "3 40 9 9 70 3 3 1 1 0 5"),
+                                       ("strip=1", "2 16 15 15 32 3 3 1 2 1 5"),
+                                       ("sswap=1", "3 64 12 12 64 3 3 1 1 1 5")])
 def test_knob_variants(cuda, tune, spec):
     """Variants the default shapes here do not reach, kept exact: the gather
     BackwardFilter with MN-major x rows (bfl_xmn=1), algorithm 0's
@@ -239,6 +246,8 @@ def test_knob_variants(cuda, tune, spec):
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "one_small.py"), *spec.split()],
                          env=env, capture_output=True, text=True, timeout=300)
     assert "exact True" in out.stdout, out.stdout + out.stderr
+    if tune.startswith("strip=1") or tune == "sswap=1":
+        assert "strip swap=" in out.stdout, out.stdout
     if tune == "pc2_msub=2":
         assert "precomp2" in out.stdout and "msub=2" in out.stdout, out.stdout
     if tune.startswith("fct_ring="):

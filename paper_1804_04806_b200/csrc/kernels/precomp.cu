@@ -69,6 +69,7 @@ struct PrecompParams {
   int bp;        // blocked phase BD: phase-grid columns per GEMM row (column = (pb, a, b, c))
   FastDiv fd_blk;  // Ah * Bw * C
   int sAh, sBw;  // phases with taps (< ssh, ssw when the filter is narrower than the stride)
+  int ph32;      // phase chunks of 32 columns are one (a, b): phase_store32
   int stages, ksub, prof, cps;
   int nacc2;  // precomp2: accumulator sets (2 when 2 * msub * BN <= 512)
   int msub;      // 1-SM kernel: 128-pixel MMA sub-tiles per tile sharing each B (filter) chunk
@@ -151,6 +152,24 @@ __device__ __forceinline__ void store_row32(const P& p, float* base, int n, std:
         if (j0 + j < n) base[(j0 + j) * pitch] = p.alpha * v[j0 + j] + p.beta * o[j];
     }
   }
+}
+
+// Stride-phase scatter of one pixel's 32-column chunk when every chunk is a
+// single phase (a, b): the phase-channel count is a multiple of 32 and there
+// are no blocked columns, pair stores or tapless phases (p.ph32, set on the
+// host). The chunk's (a, b, c) is decoded once and its channels are strided
+// stores (store_row32) -- instead of a divmod pair, a tapless test and a
+// bounds test per value, which made the epilogue the bound of the strided
+// BackwardData (30 M warp instructions for ResNet-18 l2b1c1 at 64 images).
+template <typename P>
+__device__ __forceinline__ void phase_store32(const P& p, std::int64_t obase, int col0, int n, int hb, int wb,
+                                              const float (&v)[32]) {
+  std::uint32_t ab, c, a, b;
+  p.fd_Cr.divmod(std::uint32_t(col0), ab, c);
+  p.fd_ssw.divmod(ab, a, b);
+  const int h = hb + int(a), w = wb + int(b);
+  if (unsigned(h) >= unsigned(p.Hr) || unsigned(w) >= unsigned(p.Wr)) return;
+  store_row32(p, p.out + obase + (std::int64_t(c) * p.Hr + h) * p.Wr + w, n, std::int64_t(p.Hr) * p.Wr, v);
 }
 
 __device__ __forceinline__ void tile_coords(const PrecompParams& p, int t, int& mt, int& nt) {
@@ -383,6 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
         if (!ok) continue;
+        if (p.ph32) {
+          const int col0 = nt * p.BN + c0;
+          phase_store32(p, obase, col0, min(32, min(p.BN - c0, p.Nout - col0)), hb, wb, v);
+          continue;
+        }
         if (ptab) {
           const int nv = min(32, min(p.BN - c0, p.Nout - nt * p.BN - c0));
 #pragma unroll 4
@@ -594,6 +618,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tbase + std::uint32_t(c0), v);
         if (!ok) continue;
+        if (p.ph32) {
+          const int col0 = nt * p.BN + c0;
+          phase_store32(p, obase, col0, min(32, min(p.BN - c0, p.Nout - col0)), hb, wb, v);
+          continue;
+        }
         if (p.phase) {
 #pragma unroll 4
           for (int j = 0; j < 32; ++j) {
@@ -943,7 +972,7 @@ struct StripParams {
   int OH, OW, Nout, P;
   int box_rows, nboxes, stages;
   int phase, Cr, Hr, Wr, ssh, ssw, sph, spw;
-  int sAh, sBw, pair, bp;
+  int sAh, sBw, pair, bp, ph32;
   FastDiv fd_blk;
   FastDiv fd_Cr, fd_ssw, fd_Wp, fd_HWp, fd_mt;
   int swap;  // 1: MMA rows = output channels (<= 128), N = 256 strip positions
@@ -1195,6 +1224,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tbase + std::uint32_t(c0), v);
         if (p.prof == 2) e_ld += clock64() - tq;
         if (!ok) continue;
+        if (p.ph32) {
+          const int col0 = int(nt) * p.BN + c0;
+          phase_store32(p, obase, col0, min(32, min(p.BN - c0, p.Nout - col0)), hb, wb, v);
+          continue;
+        }
         if (p.phase) {
 #pragma unroll 4
           for (int j = 0; j < 32; ++j) {
@@ -1468,6 +1502,7 @@ cudaError_t run_strip(const Geo& g, const StripGeo& sg, const float* act, const 
     p.pair = phase_pair(g);
     p.bp = g.pf.P;
     p.fd_blk = FastDiv(std::uint32_t(p.sAh * g.pf.bw * g.pf.C));
+    p.ph32 = g.pf.C % 32 == 0 && !p.pair && p.bp == 1 && p.sAh >= p.ssh && p.sBw >= p.ssw && tune("ph32", 1);
   }
   const int smem = int(sg.nsb * sg.strip_bytes + std::size_t(sg.stages) * kTapsPerStage * BN * 128) + 1024 + 256 +
                    (sg.swap ? 4 * 32 * 33 * 4 : 0);
@@ -1583,6 +1618,7 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.pair = phase_pair(g);
     p.bp = g.pf.P;
     p.fd_blk = FastDiv(std::uint32_t(p.sAh * g.pf.bw * g.pf.C));
+    p.ph32 = g.pf.C % 32 == 0 && !p.pair && p.bp == 1 && p.sAh >= p.ssh && p.sBw >= p.ssw && tune("ph32", 1);
   }
   if (two_sm) {
     CUtensorMap bmap;

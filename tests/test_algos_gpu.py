@@ -225,7 +225,12 @@ def test_bf_nhwc_variants(cuda, spec, tune):
                                        ("strip=1,strip_msub=4", "3 32 9 9 64 3 3 1 1 0 5"),
                                        ("strip=1,strip_msub=1", "3 40 9 9 70 3 3 1 1 0 5"),
                                        ("strip=1", "2 16 15 15 32 3 3 1 2 1 5"),
-                                       ("sswap=1", "3 64 12 12 64 3 3 1 1 1 5")])
+                                       ("sswap=1", "3 64 12 12 64 3 3 1 1 1 5"),
+                                       ("", "2 64 16 16 128 3 3 1 2 1 5"),
+                                       ("", "3 32 9 9 64 3 3 1 2 1 5"),
+                                       ("", "3 64 15 17 64 3 3 1 2 1 5"),
+                                       ("ph32=0", "2 64 16 16 128 3 3 1 2 1 5"),
+                                       ("strip=1", "2 64 16 16 128 3 3 1 2 1 5")])
 def test_knob_variants(cuda, tune, spec):
     """Variants the default shapes here do not reach, kept exact: the gather
     BackwardFilter with MN-major x rows (bfl_xmn=1), algorithm 0's

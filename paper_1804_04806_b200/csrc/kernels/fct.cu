@@ -298,15 +298,15 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
     const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16);
     constexpr int KH = KG / 2;
     RowWalk walk;
-    int g = 0;  // A ring slot counter over the whole kernel
+    RingPos rs;  // A ring slot over the whole kernel
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       walk.next(p, t0 + i);
       FCT_W(t_w1, mbar_wait_sleep(&loaded[i % kNB], (i / kNB) & 1));
       const int row0 = (walk.vstart + rl * p.sh) % p.RR;  // ring row of tap row 0 at this pixel
-      for (int ks = 0; ks < p.kslots; ++ks, ++g) {
-        const int slot = g % p.nslots;
-        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+      for (int ks = 0; ks < p.kslots; ++ks, rs.step(p.nslots)) {
+        const int slot = rs.slot;
+        FCT_W(t_w2, mbar_wait(&aempty[slot], rs.ph ^ 1));
         tc_fence_after();
         const int g0 = ks * KG + half * KH;
         float v[KH * SP];
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
     const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
     const std::uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem));
     const std::uint32_t chunk_desc = std::uint32_t(p.BN * 128) >> 4;
-    int g = 0;
+    RingPos rs;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       const int acc = i & 1;
@@ -380,9 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1) fct_fwd_kernel(const TParams p) {
       tc_fence_after();
       const std::uint32_t d = tmem + std::uint32_t(acc * p.BN);
       std::uint64_t bd = bdesc0;
-      for (int ks = 0; ks < p.kslots; ++ks, ++g) {
-        const int slot = g % p.nslots;
-        FCT_W(t_w2, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+      for (int ks = 0; ks < p.kslots; ++ks, rs.step(p.nslots)) {
+        const int slot = rs.slot;
+        FCT_W(t_w2, mbar_wait(&afull[slot], rs.ph));
         tc_fence_after();
         const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * KG * SP);
 #pragma unroll
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kBfThreads, 1)
     const int c = qe / (p.R * p.S), rs = qe - c * p.R * p.S, r = rs / p.S, s = rs - r * p.S;
     const std::uint32_t tq = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(qt * 32);
     RowWalkB walk;
-    int g = 0;
+    RingPos ra;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       walk.next(p, u0 + i);
@@ -608,9 +608,9 @@ __global__ void __launch_bounds__(kBfThreads, 1)
       const int e = eshift[c * p.RR + prow];
       const std::uint32_t xb = smem_u32(ring) + std::uint32_t(((c * p.RR + prow) * p.pitch + max(e, 0) + s) * 4);
       const bool live = qok && e >= 0;
-      for (int b = 0; b < p.nblk; ++b, ++g) {
-        const int slot = g % p.nslots;
-        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+      for (int b = 0; b < p.nblk; ++b, ra.step(p.nslots)) {
+        const int slot = ra.slot;
+        FCT_W(t_w2, mbar_wait(&aempty[slot], ra.ph ^ 1));
         tc_fence_after();
         const int ow0 = b * 32;
         const std::uint32_t a0 = xb + std::uint32_t(ow0 * SW * 4);
@@ -659,9 +659,10 @@ __global__ void __launch_bounds__(kBfThreads, 1)
     int g = 0;
     const int total = my_units * p.nblk;
     FCT_T0;
-    for (; g < total; ++g) {
-      const int slot = g % p.nslots, ds = g % kBfDSlots;
-      FCT_W(t_w1, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+    RingPos rs;
+    for (; g < total; ++g, rs.step(p.nslots)) {
+      const int slot = rs.slot, ds = g % kBfDSlots;
+      FCT_W(t_w1, mbar_wait(&afull[slot], rs.ph));
       FCT_W(t_w2, mbar_wait(&dfull[ds], (g / kBfDSlots) & 1));
       tc_fence_after();
       const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * QT * 32);
@@ -904,16 +905,16 @@ __global__ void __launch_bounds__(kB1Threads, 1)
     const int xoff = (qok ? cl * p.XW + s : 0) + 4 - p.pw;  // ring column 0 is w = -4
     const std::uint32_t tq = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(qt * 32);
     RowWalk1 walk;
-    int g = 0;
+    RingPos rs;
     for (int i = 0; i < my_units; ++i) {
       walk.next(p, u0 + i);
       mbar_wait(&loaded[i % kNB], (i / kNB) & 1);
       int prow = walk.vstart % p.RR + (qok ? r : 0);
       if (prow >= p.RR) prow -= p.RR;
       const std::uint32_t xb = smem_u32(ring) + std::uint32_t((prow * p.RS + xoff) * 4);
-      for (int b = 0; b < p.nblk; ++b, ++g) {
-        const int slot = g % p.nslots;
-        mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1);
+      for (int b = 0; b < p.nblk; ++b, rs.step(p.nslots)) {
+        const int slot = rs.slot;
+        mbar_wait(&aempty[slot], rs.ph ^ 1);
         tc_fence_after();
         const int ow0 = b * 32;
         const std::uint32_t a0 = xb + std::uint32_t(ow0 * 4);
@@ -955,10 +956,11 @@ __global__ void __launch_bounds__(kB1Threads, 1)
     const std::uint64_t dd0 = umma_desc_sw128(smem_u32(dring));
     const std::uint32_t dslot_desc = dslot_bytes >> 4;
     const int total = my_units * p.nblk;
-    for (int g = 0; g < total; ++g) {
-      const int slot = g % p.nslots, ds = g % p.nds;
-      mbar_wait(&afull[slot], (g / p.nslots) & 1);
-      mbar_wait(&dfull[ds], (g / p.nds) & 1);
+    RingPos rs, rd;
+    for (int g = 0; g < total; ++g, rs.step(p.nslots), rd.step(p.nds)) {
+      const int slot = rs.slot, ds = rd.slot;
+      mbar_wait(&afull[slot], rs.ph);
+      mbar_wait(&dfull[ds], rd.ph);
       tc_fence_after();
       const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * QT * 32);
       const std::uint64_t bd = dd0 + std::uint64_t(ds) * dslot_desc;
@@ -1229,20 +1231,22 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16);
     const int k0 = half * 32;
     RowWalkD walk;
-    int g = 0;
+    // slot / parity and tap (t, u) are stepped, not divided: the runtime
+    // divisions were most of this loop's instructions (ResNet conv1 BD, ncu)
+    int slot = 0, sph = 0;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       const int u_ = t0 + i;
       walk.next(p, u_);
       FCT_W(t_w1, mbar_wait(&loaded[i % kNB], (i / kNB) & 1));
-      for (int tu = 0; tu < TU; ++tu, ++g) {
-        const int t = tu / p.U, u = tu - t * p.U;
+      const int row0 = (walk.vstart + rl + p.T - 1) % p.RR;
+      const std::uint32_t col0 = smem_u32(ring) + std::uint32_t(((jl + p.U - 1) * kBdKS + k0) * 4);
+      int t = 0, u = 0;
+      for (int tu = 0; tu < TU; ++tu) {
         // ring row of dy row i - t, position j - u (+ U - 1): its 32 channels are contiguous
-        const int prow = (walk.vstart + rl + p.T - 1 - t) % p.RR;
-        const std::uint32_t addr =
-            smem_u32(ring) + std::uint32_t(((prow * p.XP + jl - u + p.U - 1) * kBdKS + k0) * 4);
-        const int slot = g % p.nslots;
-        FCT_W(t_w2, mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1));
+        const int prow = row0 - t < 0 ? row0 - t + p.RR : row0 - t;
+        const std::uint32_t addr = col0 + std::uint32_t((prow * p.XP - u) * kBdKS * 4);
+        FCT_W(t_w2, mbar_wait(&aempty[slot], sph ^ 1));
         tc_fence_after();
         float v[32];
 #pragma unroll
@@ -1255,6 +1259,14 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         tc_fence_before();
         if constexpr (PAIR) mbar_arrive_remote(afull0 + std::uint32_t(slot) * 8);
         else mbar_arrive(&afull[slot]);
+        if (++u == p.U) {
+          u = 0;
+          ++t;
+        }
+        if (++slot == p.nslots) {
+          slot = 0;
+          sph ^= 1;
+        }
       }
       mbar_arrive(&consumed[i % kNB]);
     }
@@ -1338,7 +1350,7 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
     const std::uint32_t idesc = idesc_tf32(PAIR ? 2 * kBM : kBM, p.BN);
     const std::uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem));
     const std::uint32_t chunk_desc = std::uint32_t(BH * 128) >> 4;
-    int g = 0;
+    int slot = 0, sph = 0;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
       const int acc = i & 1;
@@ -1346,9 +1358,8 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
       tc_fence_after();
       const std::uint32_t d = tmem + std::uint32_t(acc * p.AS);
       std::uint64_t bd = bdesc0;
-      for (int tu = 0; tu < TU; ++tu, ++g) {
-        const int slot = g % p.nslots;
-        FCT_W(t_w2, mbar_wait(&afull[slot], (g / p.nslots) & 1));
+      for (int tu = 0; tu < TU; ++tu) {
+        FCT_W(t_w2, mbar_wait(&afull[slot], sph));
         tc_fence_after();
         const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * kBdKp);
 #pragma unroll
@@ -1369,6 +1380,10 @@ __global__ void __launch_bounds__(kBdThreads, 1) fct_bwdd_kernel(const DParams p
         }
         __syncwarp();
         bd += (kBdKp / 32) * chunk_desc;
+        if (++slot == p.nslots) {
+          slot = 0;
+          sph ^= 1;
+        }
       }
     }
     FCT_PRINT("bd mma (tempty, afull)");

@@ -167,14 +167,15 @@ __global__ void __launch_bounds__(kThreads1, 1) fct1_kernel(const __grid_constan
     const std::uint32_t lane_off = std::uint32_t(((m * p.TRo + rl) * p.XW + ow) * 4);
     const std::uint32_t tlane = tmem + (std::uint32_t(quarter * 32) << 16) + a_col0 + std::uint32_t(m * 32);
     int g = 0, f = 0;
+    RingPos rs;
     for (int i = 0; i < my_units; ++i) {
       for (int cc = 0; cc < p.nchunks; ++cc, ++f) {
         const int rb = f & 1;
         mbar_wait(&rfull[rb], (f >> 1) & 1);
         const std::uint32_t base = smem_u32(ring) + std::uint32_t(rb * ring_floats * 4) + lane_off;
-        for (int sl = 0; sl < p.spc; ++sl, ++g) {
-          const int slot = g % p.nslots;
-          mbar_wait(&aempty[slot], ((g / p.nslots) & 1) ^ 1);
+        for (int sl = 0; sl < p.spc; ++sl, ++g, rs.step(p.nslots)) {
+          const int slot = rs.slot;
+          mbar_wait(&aempty[slot], rs.ph ^ 1);
           tc_fence_after();
           float v[32];
           const int4* tq = reinterpret_cast<const int4*>(tab + sl * 32);
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kThreads1, 1) fct1_kernel(const __grid_constan
     const std::uint64_t bd0 = umma_desc_sw128(smem_u32(bring));
     const std::uint32_t bst_desc = bst_bytes >> 4;
     int g = 0;
+    RingPos rs, rb;
     for (int i = 0; i < my_units; ++i) {
       const int acc = p.nacc == 2 ? (i & 1) : 0;
       const int use = p.nacc == 2 ? (i >> 1) : i;
@@ -206,10 +208,10 @@ __global__ void __launch_bounds__(kThreads1, 1) fct1_kernel(const __grid_constan
       tc_fence_after();
       const std::uint32_t d = tmem + std::uint32_t(acc * p.msub * p.BN);
       const int nsl = p.nchunks * p.spc;
-      for (int k0 = 0; k0 < nsl; ++k0, ++g) {
-        const int slot = g % p.nslots, bs = g % p.nbst;
-        mbar_wait(&afull[slot], (g / p.nslots) & 1);
-        mbar_wait(&bfull[bs], (g / p.nbst) & 1);
+      for (int k0 = 0; k0 < nsl; ++k0, ++g, rs.step(p.nslots), rb.step(p.nbst)) {
+        const int slot = rs.slot, bs = rb.slot;
+        mbar_wait(&afull[slot], rs.ph);
+        mbar_wait(&bfull[bs], rb.ph);
         tc_fence_after();
         const std::uint32_t ta = tmem + a_col0 + std::uint32_t(slot * p.msub * 32);
         const std::uint64_t bd = bd0 + std::uint64_t(bs) * bst_desc;

@@ -271,6 +271,19 @@ __device__ __forceinline__ void red_add(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// Ring position (slot, parity) stepped once per use: the kernels' hot
+// producer / issuer loops used g % n and g / n with a runtime n, a software
+// division each that was a large share of their issued instructions.
+struct RingPos {
+  int slot = 0, ph = 0;
+  __device__ __forceinline__ void step(int n) {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1;
+    }
+  }
+};
+
 }  // namespace sm100
 }  // namespace ucudnn
 

@@ -30,7 +30,10 @@ h = Handle()
 from paper_1804_04806_b200 import algorithm_workspace
 ws_b, _ = algorithm_workspace(a.op, s, a.algo, s.N)
 ws = torch.empty(max(ws_b, 4) // 4 + 1, device=dev)
+from paper_1804_04806_b200.api import set_trace, take_trace
+set_trace(True)
 for _ in range(a.reps):
     h.run(a.op, s, ins[0], ins[1], out, a.algo, ws)
 torch.cuda.synchronize()
+print("trace", take_trace()[:2])
 print("ok")

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ producer
       int it = 0;
+      RingOwner ro;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int mt, nt;
         tile_coords(p, t, mt, nt);
@@ -263,10 +264,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const float* bsrc = p.btiles + std::size_t(nt) * p.ksteps * (b_bytes / 4);
-        for (int j = 0; j < jsteps; ++j, ++it) {
-          if ((it % kStages) % nprod != pq) continue;
-          const int s = it % kStages;
-          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        for (int j = 0; j < jsteps; ++j, ++it, ro.step(kStages, nprod)) {
+          if (ro.own != pq) continue;
+          const int s = ro.slot;
+          mbar_wait(&empty[s], ro.ph ^ 1);
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
           mbar_expect_tx(&full[s], nsub * (msub * a_bytes + b_bytes));
           for (int sub = 0; sub < nsub; ++sub) {
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t idesc = idesc_tf32(kBM, p.BN);
     const std::uint32_t sbase = smem_u32(smem);
     int it = 0, tl = 0;
+    RingPos rp;
     long long c_data = 0, c_issue = 0, c_acc = 0, t_start = clock64();
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       const int acc = tl % nacc;
@@ -310,10 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (p.prof) c_acc += clock64() - c0;
       const std::uint32_t dtm = tmem + std::uint32_t(acc) * acc_cols;
-      for (int j = 0; j < jsteps; ++j, ++it) {
-        const int s = it % kStages;
+      for (int j = 0; j < jsteps; ++j, ++it, rp.step(kStages)) {
+        const int s = rp.slot;
         long long c1 = p.prof ? clock64() : 0;
-        mbar_wait(&full[s], (it / kStages) & 1);
+        mbar_wait(&full[s], rp.ph);
         tc_fence_after();
         long long c2 = p.prof ? clock64() : 0;
         if (p.prof) c_data += c2 - c1;
@@ -511,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nprod = kStages < 3 ? kStages : 3;
     if (lane == 0) {
       int it = 0;
+      RingOwner ro;
       for (int t = cid; t < total_tiles; t += ncl) {
         int mt, nt;
         tile_coords(p, t, mt, nt);
@@ -524,10 +527,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ns[m] = int(n);
         }
         const int brow0 = nt * p.ksteps * p.BN + int(rank) * bh;
-        for (int j = 0; j < jsteps; ++j, ++it) {
-          if ((it % kStages) % nprod != pq) continue;
-          const int s = it % kStages;
-          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        for (int j = 0; j < jsteps; ++j, ++it, ro.step(kStages, nprod)) {
+          if (ro.own != pq) continue;
+          const int s = ro.slot;
+          mbar_wait(&empty[s], ro.ph ^ 1);
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
           if (rank == 0) mbar_expect_tx(&full[s], 2u * nsub * (msub * a_bytes + b_bytes));
           const std::uint32_t bar = mapa(smem_u32(&full[s]), 0);
@@ -553,14 +556,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const std::uint64_t da0 = umma_desc_sw128(sbase), db0 = umma_desc_sw128(sbase + msub * a_bytes);
       const int nacc = p.nacc2;
       int it = 0, tl = 0;
+    RingPos rp;
       for (int t = cid; t < total_tiles; t += ncl, ++tl) {
         const int acc = tl % nacc, use = tl / nacc;
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const std::uint32_t dtm = tmem + std::uint32_t(acc * msub * p.BN);
-        for (int j = 0; j < jsteps; ++j, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&full[s], (it / kStages) & 1);
+        for (int j = 0; j < jsteps; ++j, ++it, rp.step(kStages)) {
+          const int s = rp.slot;
+          mbar_wait(&full[s], rp.ph);
           tc_fence_after();
           const int k0 = j * kSub, nsub = min(kSub, p.ksteps - k0);
           {  // whole warp, one elected lane issues
@@ -1057,15 +1061,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int pq = warp == 0 ? 0 : 1, nprod = kStages < 2 ? 1 : 2;
     if (lane == 0) {
       int it = 0;
+      RingOwner ro;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const int nt = t / p.m_tiles;
         const float* bsrc = p.btiles + std::size_t(nt) * p.c_chunks * p.taps * (tap_bytes / 4);
         for (int cc = 0; cc < p.c_chunks; ++cc)
-          for (int ts = 0; ts < tsteps; ++ts, ++it) {
-            if ((it % kStages) % nprod != pq) continue;
-            const int st = it % kStages;
+          for (int ts = 0; ts < tsteps; ++ts, ++it, ro.step(kStages, nprod)) {
+            if (ro.own != pq) continue;
+            const int st = ro.slot;
             const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
-            mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+            mbar_wait(&empty[st], ro.ph ^ 1);
             mbar_expect_tx(&full[st], ntap * tap_bytes);
             for (int i = 0; i < ntap; ++i)
               bulk_g2s(ring + st * stage_bytes + i * tap_bytes,
@@ -1079,6 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t idesc = idesc_tf32(kBM, p.swap ? 2 * kBM : p.BN);
     const std::uint32_t sbase = smem_u32(strips), rbase = smem_u32(ring);
     int it = 0, sc = 0, tl = 0;
+    RingPos rp;
     long long c_strip = 0, c_stage = 0, c_acc = 0, t_start = clock64(), cq = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tl) {
       const int acc = tl & 1;
@@ -1093,11 +1099,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sfull[sb], (sc / p.nsb) & 1);
         if (p.prof) c_strip += clock64() - cq;
         tc_fence_after();
-        for (int ts = 0; ts < tsteps; ++ts, ++it) {
-          const int st = it % kStages;
+        for (int ts = 0; ts < tsteps; ++ts, ++it, rp.step(kStages)) {
+          const int st = rp.slot;
           const int tap0 = ts * kTapsPerStage, ntap = min(kTapsPerStage, p.taps - tap0);
           if (p.prof) cq = clock64();
-          mbar_wait(&full[st], (it / kStages) & 1);
+          mbar_wait(&full[st], rp.ph);
           if (p.prof) c_stage += clock64() - cq;
           tc_fence_after();
           if (p.swap) {  // whole warp, one elected lane issues

@@ -283,6 +283,19 @@ struct RingPos {
     }
   }
 };
+// ... and the producer (of np sharing the ring round-robin) that owns slot
+struct RingOwner {
+  int slot = 0, ph = 0, own = 0;
+  __device__ __forceinline__ void step(int n, int np) {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1;
+      own = 0;
+    } else if (++own == np) {
+      own = 0;
+    }
+  }
+};
 
 }  // namespace sm100
 }  // namespace ucudnn

@@ -212,14 +212,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ TMA producers
       int it = 0;
+      RingOwner ro;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-        for (int g = g0; g < g1; ++g, ++it) {
-          if ((it % kStages) % nprod != pq) continue;
-          const int st = it % kStages;
-          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+        for (int g = g0; g < g1; ++g, ++it, ro.step(kStages, nprod)) {
+          if (ro.own != pq) continue;
+          const int st = ro.slot;
+          mbar_wait(&empty[st], ro.ph ^ 1);
           mbar_expect_tx(&full[st], a_bytes + b_bytes);
           unsigned char* sa = smem + st * stage_bytes;
           // first output pixel of the step -> im2col start (its window corner)
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t sbase = smem_u32(smem);
     const int ksub = p.px / 8;
     int it = 0, tl = 0;
+    RingPos rp;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tl) {
       const int split = u / p.tiles;
       const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
@@ -264,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
       const std::uint32_t dtm = tmem + std::uint32_t(acc * p.msub * p.BN);
-      for (int g = g0; g < g1; ++g, ++it) {
-        const int st = it % kStages;
-        mbar_wait(&full[st], (it / kStages) & 1);
+      for (int g = g0; g < g1; ++g, ++it, rp.step(kStages)) {
+        const int st = rp.slot;
+        mbar_wait(&full[st], rp.ph);
         tc_fence_after();
         if (lane == 0) {
           const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
@@ -381,14 +383,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nprod = kStages < 3 ? kStages : 3;
     if (lane == 0) {
       int it = 0;
+      RingOwner ro;
       for (int u = cid; u < units; u += ncl) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
-        for (int g = g0; g < g1; ++g, ++it) {
-          if ((it % kStages) % nprod != pq) continue;
-          const int st = it % kStages;
-          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+        for (int g = g0; g < g1; ++g, ++it, ro.step(kStages, nprod)) {
+          if (ro.own != pq) continue;
+          const int st = ro.slot;
+          mbar_wait(&empty[st], ro.ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[st], 2u * (a_bytes + b_bytes));
           const std::uint32_t bar = mapa(smem_u32(&full[st]), 0);
           unsigned char* sa = smem + st * stage_bytes;
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const std::uint32_t sbase = smem_u32(smem);
       const int ksub = p.px / 8;
       int it = 0, tl = 0;
+    RingPos rp;
       for (int u = cid; u < units; u += ncl, ++tl) {
         const int split = u / p.tiles;
         const int g0 = split * p.steps_per_unit, g1 = min(p.steps, g0 + p.steps_per_unit);
@@ -435,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const std::uint32_t dtm = tmem + std::uint32_t(acc * p.msub * p.BN);
-        for (int g = g0; g < g1; ++g, ++it) {
-          const int st = it % kStages;
-          mbar_wait(&full[st], (it / kStages) & 1);
+        for (int g = g0; g < g1; ++g, ++it, rp.step(kStages)) {
+          const int st = rp.slot;
+          mbar_wait(&full[st], rp.ph);
           tc_fence_after();
           if (lane == 0) {
             const std::uint32_t sa = sbase + st * stage_bytes, sb = sa + a_bytes;
@@ -537,17 +541,20 @@ struct NFinal {
   int C, Cp, RS, rpad;
   std::int64_t n;
   int s2d, S, sh, sw, Bw, Tw;  // s2d: dW[k][c][r][s] from phase-channel (r % sh, s % sw, c) at tap (r / sh, s / sw)
+  FastDiv fd_RS, fd_C;        // 32-bit index math (dW has < 2^31 elements): the 64-bit % and / made this an
+                              // instruction-bound kernel
 };
 
 // dW[k][c][r][s] = beta * dW + alpha * acc[k][(r*S+s)*Cp + c]
 __global__ void __launch_bounds__(256) bfn_finalize_kernel(const NFinal f) {
   pdl_wait();
   pdl_trigger();
-  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < f.n;
-       i += std::int64_t(gridDim.x) * blockDim.x) {
-    const int tap = int(i % f.RS);
-    const std::int64_t t = i / f.RS;
-    const int c = int(t % f.C), k = int(t / f.C);
+  const std::uint32_t n = std::uint32_t(f.n);
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    std::uint32_t t, tap_, k_, c_;
+    f.fd_RS.divmod(i, t, tap_);
+    f.fd_C.divmod(t, k_, c_);
+    const int tap = int(tap_), c = int(c_), k = int(k_);
     int row = tap * f.Cp + c;
     if (f.s2d) {
       const int r = tap / f.S, s = tap - r * f.S;
@@ -737,6 +744,8 @@ cudaError_t bfn_run(const ConvShape& s, const float* x, const float* dy, float* 
   f.C = g.C0; f.Cp = g.Cp; f.RS = g.R0 * g.S0; f.rpad = rows_pad(g);
   f.n = std::int64_t(g.K) * g.C0 * g.R0 * g.S0;
   f.s2d = g.s2d; f.S = g.S0; f.sh = g.sh; f.sw = g.sw; f.Bw = g.Bw; f.Tw = g.S;
+  f.fd_RS = FastDiv(std::uint32_t(f.RS));
+  f.fd_C = FastDiv(std::uint32_t(f.C));
   return launch_pdl(bfn_finalize_kernel, dim3(int(std::min<std::int64_t>((f.n + 255) / 256, 8 * sms))), dim3(256),
                     0, st, f);
 }

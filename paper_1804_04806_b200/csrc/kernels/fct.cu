@@ -1037,12 +1037,15 @@ struct B1Final {
   float* dw;
   float alpha, beta;
   int rows, K, QG, cpg, CR, R, S;
+  FastDiv fd_K;  // 32-bit index math (dW has < 2^31 elements)
 };
 __global__ void __launch_bounds__(256) fct_bwdf1_finalize_kernel(const B1Final f) {
   pdl_wait();
-  const long long n = (long long)f.rows * f.K;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int q = int(i / f.K), k = int(i - (long long)q * f.K);
+  const std::uint32_t n = std::uint32_t(f.rows) * std::uint32_t(f.K);
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    std::uint32_t q_, k_;
+    f.fd_K.divmod(i, q_, k_);
+    const int q = int(q_), k = int(k_);
     const int RS = f.R * f.S, c = q / RS, rs = q - c * RS, r = rs / f.S, s = rs - r * f.S;
     const int grp = c / f.CR, ql = (r * f.CR + (c - grp * f.CR)) * f.S + s;  // the kernel's lane order
     const float* sl = f.slices + ((long long)grp * f.cpg * f.QG + ql) * f.K + k;
@@ -1066,12 +1069,15 @@ struct BFinal {
   float* dw;
   float alpha, beta;
   int rows, K, nslices;
+  FastDiv fd_K;  // 32-bit index math (dW has < 2^31 elements)
 };
 __global__ void __launch_bounds__(256) fct_bwdf_finalize_kernel(const BFinal f) {
   pdl_wait();
   const long long n = (long long)f.rows * f.K;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int q = int(i / f.K), k = int(i - (long long)q * f.K);
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < std::uint32_t(n); i += gridDim.x * blockDim.x) {
+    std::uint32_t q_, k_;
+    f.fd_K.divmod(i, q_, k_);
+    const int q = int(q_), k = int(k_);
     // eight interleaved partial sums (loads in flight instead of one
     // dependent chain of ~148), combined in a fixed order: deterministic
     float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1633,7 +1639,7 @@ cudaError_t fct_bwdf_run(const ConvShape& s, const float* x, const float* dy, fl
                 g.grid, g.rows, g.QT, g.BN, g.nblk, g.pitch, g.RR, g.nslots, p.dtma);
   e = launch_pdl(kern, dim3(g.grid), dim3(kBfThreads), g.smem, st, dmap, p);
   if (e != cudaSuccess) return e;
-  BFinal f{p.slices, dw, alpha, beta, g.rows, s.K, g.grid};
+  BFinal f{p.slices, dw, alpha, beta, g.rows, s.K, g.grid, FastDiv(std::uint32_t(s.K))};
   const long long n = (long long)g.rows * s.K;
   return launch_pdl(fct_bwdf_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
                     dim3(256), 0, st, f);
@@ -1846,7 +1852,7 @@ cudaError_t fct_bwdf1_run(const ConvShape& s, const float* x, const float* dy, f
                 g.G, g.cpg, g.QT, g.BN, g.CR, g.XW, g.RR, g.nslots, g.nds);
   e = launch_pdl(kern, dim3(g.G * g.cpg), dim3(kB1Threads), g.smem, st, xmap, dmap, p);
   if (e != cudaSuccess) return e;
-  B1Final f{p.slices, dw, alpha, beta, g.rows, s.K, g.QG, g.cpg, g.CR, s.R, s.S};
+  B1Final f{p.slices, dw, alpha, beta, g.rows, s.K, g.QG, g.cpg, g.CR, s.R, s.S, FastDiv(std::uint32_t(s.K))};
   const long long n = (long long)g.rows * s.K;
   return launch_pdl(fct_bwdf1_finalize_kernel, dim3(int(std::min<long long>((n + 255) / 256, 4 * sm_count()))),
                     dim3(256), 0, st, f);

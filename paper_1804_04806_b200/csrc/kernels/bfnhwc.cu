@@ -92,8 +92,16 @@ NGeo make_geo(const ConvShape& s) {
   // (AlexNet BF at 256 images, 1-SM vs pair) conv4 (M = 3456) 233 -> 206 us,
   // but conv2 / conv3 / conv5 with 256-row pair tiles 378 -> 423, 194 -> 220,
   // 144 -> 153 us
+  // Round 2 (warp-wide issue, scripts/r02_run85.sh): pairs now also win for
+  // >= 192 output channels with 3x3 / 5x5 filters at 256-row pair tiles --
+  // conv2 BF at 64 images 414 -> 373 us per 256, conv3 at 128 215 -> 182,
+  // conv5 170 -> 150, ResNet l3 195 -> 178 -- but not at 128 channels
+  // (ResNet l2 264 -> 297); 1x1 and space-to-depth layers were not measured
+  // and keep the padding rule
   const int knob = tune("bfn2", -1);
-  g.two = knob >= 0 ? (knob > 0 && g.M >= 2 * kBM) : round_up(g.M, 4 * kBM) <= round_up(g.M, 2 * kBM);
+  const bool pad_pair = round_up(g.M, 4 * kBM) <= round_up(g.M, 2 * kBM);
+  const bool wide_pair = g.Kp >= 192 && g.M >= 2 * kBM && g.R * g.S > 1 && !g.s2d;
+  g.two = knob >= 0 ? (knob > 0 && g.M >= 2 * kBM) : (pad_pair || wide_pair);
   const int bq = g.two ? 64 : 32;  // pairs: each CTA holds BN/2 columns, whole 32-column blocks
   g.n_tiles = (g.Kp + kMaxBN - 1) / kMaxBN;
   g.BN = round_up((g.Kp + g.n_tiles - 1) / g.n_tiles, bq);
@@ -101,7 +109,7 @@ NGeo make_geo(const ConvShape& s) {
   const int pair_rows = (g.two ? 2 : 1) * kBM;
   if (g.M <= pair_rows) {
     g.msub = 1;
-  } else if (g.two && knob < 0) {
+  } else if (g.two && knob < 0 && pad_pair) {
     g.msub = 2;
   } else {
     // fewest padded rows, ties to 2 sub-tiles (more MMA work per dy box)

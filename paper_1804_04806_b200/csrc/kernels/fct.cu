@@ -185,6 +185,7 @@ struct RowWalk {
 struct BParams;
 struct RowWalkB {
   int vstart = 0, vend = 0, n = -1;
+  int oh = 0, vmod = 0;  // step(): row within the image, vstart % RR
   template <typename P>
   __device__ __forceinline__ bool next(const P& p, int u) {
     const int nn = u / p.OH;
@@ -192,6 +193,28 @@ struct RowWalkB {
     vstart = fresh ? vend : vstart + p.sh;
     vend = vstart + p.R;
     n = nn;
+    return fresh;
+  }
+  // next() for consecutive units u, u + 1, ...: the image / row and the ring
+  // row of vstart are stepped (one division on the first call only)
+  template <typename P>
+  __device__ __forceinline__ bool step(const P& p, int u) {
+    bool fresh;
+    if (n < 0) {
+      n = u / p.OH;
+      oh = u - n * p.OH;
+      fresh = true;
+    } else if (++oh == p.OH) {
+      oh = 0;
+      ++n;
+      fresh = true;
+    } else {
+      fresh = false;
+    }
+    vmod += fresh ? vend - vstart : p.sh;
+    while (vmod >= p.RR) vmod -= p.RR;
+    vstart = fresh ? vend : vstart + p.sh;
+    vend = vstart + p.R;
     return fresh;
   }
 };
@@ -600,9 +623,9 @@ __global__ void __launch_bounds__(kBfThreads, 1)
     RingPos ra;
     FCT_T0;
     for (int i = 0; i < my_units; ++i) {
-      walk.next(p, u0 + i);
+      walk.step(p, u0 + i);
       FCT_W(t_w1, mbar_wait(&loaded[i % kNB], (i / kNB) & 1));
-      int prow = walk.vstart % p.RR + r;
+      int prow = walk.vmod + r;
       if (prow >= p.RR) prow -= p.RR;
       // the ring row's data offset (bulk copies land 16 B aligned), -1: off the image
       const int e = eshift[c * p.RR + prow];
@@ -621,6 +644,8 @@ __global__ void __launch_bounds__(kBfThreads, 1)
         // (padding columns, rows off the image, pixels past the row end) may
         // hold anything
         const int iw0 = ow0 * SW + s - p.pw;
+        // (skipping this test for interior blocks measured slower: ResNet
+        // conv1 BF 392 -> 466 us -- the branch splits the warp's lanes)
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (!live || ow0 + j >= p.OW || unsigned(iw0 + j * SW) >= unsigned(p.W)) v[j] = 0.f;
@@ -832,12 +857,33 @@ __device__ __forceinline__ void tma_3d(std::uint32_t dst, const void* tmap, std:
 
 struct RowWalk1 {
   int vstart = 0, vend = 0, n = -1;
+  int oh = 0, vmod = 0;  // step(): row within the image, vstart % RR
   __device__ __forceinline__ bool next(const B1Params& p, int u) {
     const int nn = u / p.OH;
     const bool fresh = nn != n;
     vstart = fresh ? vend : vstart + 1;
     vend = vstart + p.R;
     n = nn;
+    return fresh;
+  }
+  // next() for consecutive units (RowWalkB::step)
+  __device__ __forceinline__ bool step(const B1Params& p, int u) {
+    bool fresh;
+    if (n < 0) {
+      n = u / p.OH;
+      oh = u - n * p.OH;
+      fresh = true;
+    } else if (++oh == p.OH) {
+      oh = 0;
+      ++n;
+      fresh = true;
+    } else {
+      fresh = false;
+    }
+    vmod += fresh ? vend - vstart : 1;
+    while (vmod >= p.RR) vmod -= p.RR;
+    vstart = fresh ? vend : vstart + 1;
+    vend = vstart + p.R;
     return fresh;
   }
 };
@@ -907,9 +953,9 @@ __global__ void __launch_bounds__(kB1Threads, 1)
     RowWalk1 walk;
     RingPos rs;
     for (int i = 0; i < my_units; ++i) {
-      walk.next(p, u0 + i);
+      walk.step(p, u0 + i);
       mbar_wait(&loaded[i % kNB], (i / kNB) & 1);
-      int prow = walk.vstart % p.RR + (qok ? r : 0);
+      int prow = walk.vmod + (qok ? r : 0);
       if (prow >= p.RR) prow -= p.RR;
       const std::uint32_t xb = smem_u32(ring) + std::uint32_t((prow * p.RS + xoff) * 4);
       for (int b = 0; b < p.nblk; ++b, rs.step(p.nslots)) {

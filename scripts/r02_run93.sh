@@ -1,0 +1,3 @@
+#!/bin/bash
+timeout 600 python scripts/time_table.py 256,3,224,224,64,11,11,2,4 256,3,224,224,64,7,7,3,2 256,64,56,56,64,3,3,1,1 256,128,28,28,128,3,3,1,1 --ops 2 --algos 6 --batches 256
+timeout 900 python -m pytest tests/test_algos_gpu.py -q -p no:cacheprovider -k "knob and (2-6 or bf)" 2>&1 | tail -2

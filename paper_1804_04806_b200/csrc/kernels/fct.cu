@@ -1632,6 +1632,10 @@ BGeo make_bgeo(const ConvShape& s) {
   const std::size_t row_bytes = std::size_t(s.C) * g.pitch * 4;
   int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
   rr = std::min(rr, s.R + (kHist - 2) * s.sh);
+  // a shallow ring is faster (less shared memory, more L1 for the row
+  // loads): AlexNet conv1 BF 273 -> 263 us at R + 2 sh - 1 rows, ResNet
+  // conv1 398 -> 378 (scripts/r02_run98.sh)
+  rr = std::min(rr, s.R + 2 * s.sh - 1);
   rr = std::min(rr, tune("fct_bf_ring", rr));
   g.RR = std::max(rr, 1);
   g.smem = fixed + row_bytes * g.RR;

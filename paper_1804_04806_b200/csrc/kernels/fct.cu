@@ -1841,6 +1841,10 @@ B1Geo make_b1geo(const ConvShape& s) {
   const std::size_t row_bytes = std::size_t(g.RS) * 4;
   int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
   rr = std::min(rr, s.R + (kHist - 2));
+  // one 32-pixel block per output row: a shallow ring is faster (ResNet l2
+  // 3x3 BF at 256 images 253 -> 216 us at R + 2 rows); two blocks per row
+  // keep the deep ring (l1: 273 vs 286 us, scripts/r02_run100.sh)
+  if (g.nblk == 1) rr = std::min(rr, s.R + 2);
   rr = std::min(rr, tune("fct_bf1_ring", rr));
   g.RR = std::max(rr, 1);
   g.smem = fixed + row_bytes * g.RR;

@@ -1561,6 +1561,10 @@ TGeo make_tgeo(const ConvShape& s) {
   const int step = g.TR * s.sh;
   int rr = int((220 * 1024 - std::min<std::size_t>(fixed, 220 * 1024)) / row_bytes);
   rr = std::min(rr, g.PH + (kHist - 2) * step);
+  // one output row per tile: the shallowest ring is fastest (ResNet conv1 F
+  // 451 -> 426 us); AlexNet's two-row tiles are indifferent
+  // (scripts/r02_run102.sh)
+  if (g.TR == 1) rr = std::min(rr, g.PH + step);
   rr = std::min(rr, tune("fct_ring", rr));
   g.RR = std::max(rr, 1);
   g.r_bytes = row_bytes * g.RR;

@@ -1644,7 +1644,10 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.nacc2 = 2 * p.msub * ((BN + 31) & ~31) <= 512 ? 2 : 1;  // tmem_ld32 reads whole 32-column groups
     p.m_tiles = (p.M + 2 * p.msub * kBM - 1) / (2 * p.msub * kBM);
     p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
-    p.ksub = std::max(1, std::min(2, tune("pc2_ksub", p.msub == 2 ? 1 : 2)));
+    // one reduction step per stage at BN >= 256 (3 -> 6 stages): AlexNet
+    // conv5 F / BD 122 -> 116 / 120 -> 112 us, ResNet l3b1c1 BD 195 -> 182;
+    // two at BN <= 192 (ResNet l2 F 199 vs 219 with one; scripts/r02_run107.sh)
+    p.ksub = std::max(1, std::min(2, tune("pc2_ksub", p.msub == 2 || BN >= 256 ? 1 : 2)));
     const int stage2 = p.ksub * (p.msub * kBM * 128 + ((BN / 2 * 128 + 1023) & ~1023));
     p.stages = ring_stages(std::min(tune("pc2_stages", 8), (200 * 1024) / stage2));
     const int smem2 = std::max(p.stages * stage2 + 1024 + 256, 116 * 1024);
@@ -1687,7 +1690,12 @@ cudaError_t run_geo(const Geo& g, const float* act, const float* w, int flip, fl
     p.fd_mt = FastDiv(std::uint32_t(p.m_tiles));
   }
   p.cps = tune("pc_cps", p.msub == 1 && p.m_tiles * p.n_tiles > sm_count() ? 2 : 1) == 2 ? 2 : 1;
-  p.ksub = std::max(1, std::min(4, tune("pc_ksub", (p.cps == 2 && BN > 128) || p.msub == 2 ? 1 : 2)));
+  // one reduction step per stage: twice the stages in the same shared
+  // memory (two CTAs per SM with BN = 64 had only two 48 KB stages);
+  // measured equal or faster on every planned call (AlexNet conv2 BD 7@256
+  // 452 -> 417 us, ResNet l1 F / BD 5@64 340 -> 324, scripts/r02_run105.sh,
+  // r02_run106.sh)
+  p.ksub = std::max(1, std::min(4, tune("pc_ksub", 1)));
   const int stage_bytes = p.ksub * (p.msub * kBM * 128 + ((BN * 128 + 1023) & ~1023));
   p.stages = ring_stages(std::min(tune("pc_stages", 8), (p.cps == 2 ? 100 * 1024 : 200 * 1024) / stage_bytes));
   // >= 116 KB so the persistent grid lands one CTA per SM (each owns all
